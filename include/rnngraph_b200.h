@@ -1,0 +1,116 @@
+/* rnngraph_b200.h -- C ABI of the B200-native graph-RNN BPTT(h; h') training step.
+ *
+ * Drop-in boundary for the forward / backward / update path of the reference
+ * package `rnngraph` (arXiv 1503.02852).  The reference has no FFI: its
+ * boundary is the Python API in /root/reference/pkg/src/rnngraph/engine.py.
+ * Each entry point below replaces one of those functions; the Python mirror
+ * (paper_1503_02852_b200/engine.py) binds them with ctypes exactly as a
+ * maintainer would.
+ *
+ * Conventions
+ *  - All tensors are caller-owned fp32 device buffers (plain pointers); the
+ *    plan owns only its parsed schedule.  The activation history, error
+ *    buffers and scratch live in ONE caller-allocated device workspace whose
+ *    size rgb_plan_workspace_bytes() reports and whose internal layout is
+ *    fixed by the schedule program (emitted by paper_1503_02852_b200/schedule.py).
+ *  - Weights: one flat fp32 buffer W holding every dense connection's
+ *    (dst_size x src_size) row-major matrix at the offset the program's weight
+ *    table gives, a same-layout buffer WT holding the transposes (the
+ *    reference keeps the same cache, engine.py:111-139), and a same-layout
+ *    gradient buffer G.
+ *  - Work is enqueued on `stream` (a cudaStream_t); nothing synchronises
+ *    except rgb_read_loss().
+ *  - Every function returns RGB_OK (0) or an error code; rgb_last_error()
+ *    returns the thread-local message of the last failure.  No CPU fallback:
+ *    rgb_plan_create() fails when no sm_100 device is present.
+ */
+#ifndef RNNGRAPH_B200_H
+#define RNNGRAPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGB_ABI_VERSION 1
+
+enum rgb_status {
+  RGB_OK = 0,
+  RGB_ERR_ENGINE = 1,  /* guard violation -> EngineError (engine.py:86-87) */
+  RGB_ERR_KERNEL = 2,  /* shape / argument misuse -> KernelError (kernels.py:54-55) */
+  RGB_ERR_CUDA = 3,    /* CUDA runtime failure or no sm_100 device */
+  RGB_ERR_FLOAT = 4    /* non-finite values -> FloatingPointError (kernels.py:344-348) */
+};
+
+typedef struct rgb_plan rgb_plan;
+
+int rgb_abi_version(void);
+const char* rgb_last_error(void);
+
+/* Parse a schedule program (int32 words emitted by schedule.py) for one
+ * network, stream count S and BPTT horizon h.  Replaces the per-call
+ * schedule walk of forward_chunk/backward_window (engine.py:405-413,
+ * 568-576) and StreamState's layout (engine.py:197-229). */
+int rgb_plan_create(const int32_t* program, int64_t n_words, rgb_plan** out);
+int rgb_plan_destroy(rgb_plan* plan);
+int rgb_plan_workspace_bytes(const rgb_plan* plan, int64_t* bytes);
+/* Bind a zero-filled device workspace of at least workspace_bytes. */
+int rgb_plan_bind(rgb_plan* plan, void* workspace);
+int rgb_plan_get_cursor(const rgb_plan* plan, int64_t* cursor);
+int rgb_plan_set_cursor(rgb_plan* plan, int64_t cursor);
+
+/* forward_chunk (engine.py:352-418): advance every stream by `frames`
+ * frames.  `x` is (frames*S, n_in) fp32, frame-major; x_on_host != 0 means
+ * a host pointer (copied inside this call).  sequential != 0 runs the
+ * paper's frame-by-frame baseline schedule (frame_parallel=False). */
+int rgb_forward_chunk(rgb_plan* plan, const float* w, const float* x, int x_on_host, int frames,
+                      int sequential, void* stream);
+
+/* inject_output_error + loss_value (engine.py:425-474) for the newest
+ * `frames` frames: delta_out = d - y into the plan's injection buffer and
+ * the summed loss into the plan's device loss slot.  target_kind: 0 int64
+ * class ids, 1 int32 class ids, 2 dense fp32 (frames*S, n_out).
+ * criterion: 0 cross-entropy/softmax, 1 mse/identity. */
+int rgb_inject_output_error(rgb_plan* plan, const void* target, int target_kind, int target_on_host,
+                            int criterion, int frames, void* stream);
+/* Read the last loss (synchronises the stream). */
+int rgb_read_loss(rgb_plan* plan, double* loss, void* stream);
+/* Copy the plan's injection buffer rows in/out (frames*S, n_out), device
+ * pointers; used when the caller supplies its own delta_out. */
+int rgb_set_injection(rgb_plan* plan, const float* delta_out, int frames, void* stream);
+int rgb_get_injection(rgb_plan* plan, float* delta_out, int frames, void* stream);
+
+/* Plan-free inject_output_error / loss_value on arbitrary (rows, width)
+ * output rows: delta = d - y, per-row loss into row_loss[rows] (fp64
+ * scratch) and their fixed-order sum into *loss (device). */
+int rgb_inject_rows(const float* y, const void* target, int target_kind, int criterion, float* delta,
+                    double* row_loss, double* loss, int rows, int width, void* stream);
+
+/* Token-id chunk -> dense one-hot rows (rows, width) on the device; id -1
+ * gives a zero row.  Feeds forward_chunk's id-input mode (engine.py:372-403;
+ * bitwise equal to one-hot dense input in the reference, test_engine.py:277-312). */
+int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* stream);
+
+/* backward_window (engine.py:481-599) for the window (t1-h, t1], t1 = the
+ * cursor, errors injected on (t1-h', t1].  Writes the loss gradient
+ * dE/dW (= -sum eps y^T, engine.py:13-21) into G for every dense edge. */
+int rgb_backward_window(rgb_plan* plan, const float* wt, float* g, int h, int h_prime, int sequential,
+                        void* stream);
+
+/* sgd_update (engine.py:606-612): W -= lr*G, then WT = W^T. */
+int rgb_sgd_update(rgb_plan* plan, float* w, float* wt, const float* g, float lr, void* stream);
+/* Weights.refresh (engine.py:138-139): WT = W^T. */
+int rgb_refresh_transpose(rgb_plan* plan, const float* w, float* wt, void* stream);
+
+/* StreamState.reset_stream (engine.py:267-276). */
+int rgb_reset_stream(rgb_plan* plan, int stream_index, void* stream);
+
+/* Count non-finite values of one buffer over frames [t_lo, t_hi] (the
+ * check_finite guard, engine.py:415-417); result copied to *count (sync). */
+int rgb_count_nonfinite(rgb_plan* plan, int buffer, int64_t t_lo, int64_t t_hi, int64_t* count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNNGRAPH_B200_H */

@@ -1,5 +1,19 @@
-"""B200-native generalized graph-RNN BPTT(h; h') training step (arXiv 1503.02852)."""
-from .netdef import (Activation, Aggregation, ConnectionDef, LayerDef, NetworkDef, Role, WeightKind,
-                     infer_shapes, load_network, save_network, validate)
-from .condense import CondensedGraph, SuperNode, condense, export_dot, tarjan_scc, schedule_text
-from .builders import build_elman, build_lstm, build_stacked_lstm, build_custom_graph, count_params
+"""B200-native generalized graph-RNN BPTT(h; h') training step (arXiv 1503.02852).
+
+Drop-in for the forward / backward / update path of the reference package
+``rnngraph``: the same graph API (``netdef``, ``builders``, ``condense``) and
+engine API (``engine``), executed by hand-written sm_100a CUDA kernels behind
+the C ABI in ``include/rnngraph_b200.h``.
+"""
+
+from .netdef import (Activation, Aggregation, ConnectionDef, LayerDef, NetdefError, NetworkDef, ParseError, Role,
+                     SemanticError, ValidationReport, Violation, WeightKind, from_reference, infer_shapes,
+                     load_network, save_network, validate)
+from .condense import CondensedGraph, SuperNode, condense, export_dot, schedule_text, tarjan_scc
+from .builders import build_custom_graph, build_elman, build_lstm, build_stacked_lstm, count_params
+from .schedule import EngineError, build_program
+from .engine import (Batch, BpttWindow, Criterion, GradStore, IterationMetrics, StreamState, TrainConfig, Trainer,
+                     Weights, backward_window, forward_chunk, inject_output_error, loss_value, sgd_update,
+                     train_loop)
+
+__version__ = "0.1.0"

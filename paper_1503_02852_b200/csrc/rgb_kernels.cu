@@ -1,0 +1,394 @@
+// SIMT fp32 kernels of the graph-RNN step.  See rgb_kernels.cuh for the list.
+// Reference semantics cited per function (/root/reference/pkg/src/rnngraph/).
+#include "rgb_kernels.cuh"
+
+#include <cmath>
+
+namespace rgb {
+
+// ---------------------------------------------------------------------------
+// activations (kernels.py:143-189): accurate expf/tanhf, no fast-math
+
+__device__ __forceinline__ float act_apply(int act, float x) {
+  if (act == ACT_SIGMOID) return 1.0f / (1.0f + expf(-x));
+  if (act == ACT_TANH) return tanhf(x);
+  return x;  // identity (softmax is a separate row kernel)
+}
+
+// f'(s) from the stored output y (kernels.py:176-189)
+__device__ __forceinline__ float act_deriv(int act, float y) {
+  if (act == ACT_SIGMOID) return y * (1.0f - y);
+  if (act == ACT_TANH) return 1.0f - y * y;
+  return 1.0f;  // identity; softmax only ever appears fused with CE (engine.py:537-543)
+}
+
+__device__ __forceinline__ void ring_store(float* out, int64_t e, int64_t r, int width, bool is_ring,
+                                           const RingWrite& ring, float v) {
+  out[e] = v;
+  if (is_ring) {
+    const int64_t moff = ring.frame_rows * width;
+    out[e + (r < ring.split ? moff : -moff)] = v;
+  }
+}
+
+// One elementwise op at (row r, unit j).  `acc` replaces op.base when has_acc.
+__device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
+                                         bool has_acc, float acc) {
+  const int64_t e = r * width + j;
+  switch (op.kind) {
+    case EW_CONST1:
+      ring_store(op.out, e, r, width, op.out_is_ring, ring, 1.0f);
+      return;
+    case EW_FWD_MUL: {
+      float v = op.fac[0][e];
+      for (int i = 1; i < op.nfac; ++i) v *= op.fac[i][e];
+      ring_store(op.out, e, r, width, op.out_is_ring, ring, v);
+      return;
+    }
+    case EW_FWD_ADD: {
+      float v = has_acc ? acc : (op.base ? op.base[e] : 0.0f);
+      for (int i = 0; i < op.nterm; ++i) v += op.term[i][e];
+      for (int i = 0; i < op.nrank1; ++i) v += op.r1w[i][j] * op.r1src[i][r];
+      ring_store(op.out, e, r, width, op.out_is_ring, ring, act_apply(op.act, v));
+      return;
+    }
+    case EW_BWD: {
+      float v = has_acc ? acc : (op.base ? op.base[e] : 0.0f);
+      for (int i = 0; i < op.nterm; ++i) v += op.term[i][e];
+      if (op.act != ACT_SOFTMAX) v *= act_deriv(op.act, op.y[e]);
+      if (op.inj && r >= op.inj_row0) v += op.inj[(r - op.inj_row0) * width + j];  // after f' (engine.py:548-554)
+      op.out[e] = v;
+      for (int i = 0; i < op.nfac; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
+        if (!op.eps[i]) continue;
+        float p = v;
+        for (int k = 0; k < op.nfac; ++k)
+          if (k != i) p *= op.fac[k][e];
+        op.eps[i][e] = p;
+      }
+      return;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ EwLaunch p) {
+  const EwChain& ch = p.chain[blockIdx.y];
+  const int64_t total = (int64_t)p.rows * ch.width;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ch.width;
+    const int j = (int)(e - r * ch.width);
+    for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, r, j, p.ring, false, 0.0f);
+  }
+}
+
+void launch_ew(const EwLaunch& p, cudaStream_t s) {
+  int64_t maxw = 1;
+  for (int c = 0; c < p.nchains; ++c) maxw = maxw > p.chain[c].width ? maxw : p.chain[c].width;
+  int64_t total = (int64_t)p.rows * maxw;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  ew_chain_kernel<<<dim3(blocks, p.nchains), 256, 0, s>>>(p);
+}
+
+// ---------------------------------------------------------------------------
+// grouped NT GEMM: C[r, n] = sum_seg sum_k A[r, k] * B[n, k], epilogue = EW chain
+// (the per-edge products of _accum_z / backward_layer, engine.py:304-321, 525-535)
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__device__ __forceinline__ void find_job(const int* tile_start, int njobs, int bid, int& job, int& tile) {
+  job = 0;
+  while (job + 1 < njobs && bid >= tile_start[job + 1]) ++job;
+  tile = bid - tile_start[job];
+}
+
+__global__ void __launch_bounds__(256) gemm_nt_kernel(const __grid_constant__ GemmGroup p) {
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN + 4];
+  int jid, tile;
+  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  const GemmJob& job = p.job[jid];
+  const int tm = tile / p.tiles_n[jid], tn = tile % p.tiles_n[jid];
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  const int lrow = threadIdx.x / 4, lk = (threadIdx.x % 4) * 4;
+  for (int s = 0; s < job.nseg; ++s) {
+    const Seg sg = job.seg[s];
+    for (int k0 = 0; k0 < sg.k; k0 += BK) {
+      {
+        const int gr = m0 + lrow;
+        #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int gk = k0 + lk + i;
+          As[lk + i][lrow] = (gr < p.rows && gk < sg.k) ? sg.a[(int64_t)gr * sg.k + gk] : 0.0f;
+        }
+        const int gn = n0 + lrow;
+        #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int gk = k0 + lk + i;
+          Bs[lk + i][lrow] = (gn < job.n && gk < sg.k) ? sg.b[(int64_t)gn * sg.k + gk] : 0.0f;
+        }
+      }
+      __syncthreads();
+      #pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        #pragma unroll
+        for (int i = 0; i < 4; ++i)
+          #pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+  #pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + ty * 4 + i;
+    if (r >= p.rows) continue;
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = n0 + tx * 4 + j;
+      if (c >= job.n) continue;
+      for (int k = 0; k < job.epi.nops; ++k) ew_apply(job.epi.op[k], job.n, r, c, p.ring, k == 0, acc[i][j]);
+    }
+  }
+}
+
+void launch_gemm_nt(const GemmGroup& p, cudaStream_t s) {
+  const int tiles = p.tile_start[p.njobs];
+  if (tiles > 0) gemm_nt_kernel<<<tiles, 256, 0, s>>>(p);
+}
+
+// ---------------------------------------------------------------------------
+// dW: G[m, n] = alpha * sum_k E[k, m] * Y[k, n]   (engine.py:578-599, paper Eq. 19)
+
+__global__ void __launch_bounds__(256) gemm_dw_kernel(const __grid_constant__ DwGroup p) {
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN + 4];
+  int jid, tile;
+  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  const DwJob& job = p.job[jid];
+  const int tm = tile / p.tiles_n[jid], tn = tile % p.tiles_n[jid];
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  const int lk = threadIdx.x / 16, lc = (threadIdx.x % 16) * 4;  // 16 k-rows x 64 columns
+  for (int k0 = 0; k0 < p.k; k0 += BK) {
+    const int gk = k0 + lk;
+    #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + lc + i, gn = n0 + lc + i;
+      As[lk][lc + i] = (gk < p.k && gm < job.m) ? job.e[(int64_t)gk * job.m + gm] : 0.0f;
+      Bs[lk][lc + i] = (gk < p.k && gn < job.n) ? job.y[(int64_t)gk * job.n + gn] : 0.0f;
+    }
+    __syncthreads();
+    #pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+      #pragma unroll
+      for (int i = 0; i < 4; ++i)
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  #pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= job.m) continue;
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n < job.n) job.g[(int64_t)m * job.n + n] = p.alpha * acc[i][j];
+    }
+  }
+}
+
+void launch_gemm_dw(const DwGroup& p, cudaStream_t s) {
+  const int tiles = p.tile_start[p.njobs];
+  if (tiles > 0) gemm_dw_kernel<<<tiles, 256, 0, s>>>(p);
+}
+
+// ---------------------------------------------------------------------------
+// softmax over each row, max-subtracted (kernels.py:159-173); one warp per row
+
+__global__ void softmax_rows_kernel(float* y, int rows, int width, RingWrite ring, int is_ring) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  float* row = y + (int64_t)warp * width;
+  float m = -INFINITY;
+  for (int j = lane; j < width; j += 32) m = fmaxf(m, row[j]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.0f;
+  for (int j = lane; j < width; j += 32) s += expf(row[j] - m);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = 1.0f / s;
+  for (int j = lane; j < width; j += 32) {
+    const float v = expf(row[j] - m) * inv;
+    ring_store(y, (int64_t)warp * width + j, warp, width, is_ring != 0, ring, v);
+  }
+}
+
+void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s) {
+  const int threads = 256, per = threads / 32;
+  softmax_rows_kernel<<<(rows + per - 1) / per, threads, 0, s>>>(y, rows, width, ring, is_ring ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------
+// delta_out = d - y and the per-row loss (engine.py:425-474)
+
+__global__ void inject_loss_kernel(const float* y, const void* target, int target_kind, int criterion, float* inj,
+                                   double* row_loss, int rows, int width) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* yr = y + (int64_t)warp * width;
+  float* ir = inj + (int64_t)warp * width;
+  double loss = 0.0;
+  if (target_kind == 2) {
+    const float* dr = static_cast<const float*>(target) + (int64_t)warp * width;
+    for (int j = lane; j < width; j += 32) {
+      const float d = dr[j], v = yr[j];
+      ir[j] = d - v;
+      if (criterion == 1) {
+        const double diff = (double)d - (double)v;
+        loss += 0.5 * diff * diff;
+      } else if (d != 0.0f) {
+        loss -= (double)d * log((double)v);
+      }
+    }
+  } else {
+    const long long id = target_kind == 0 ? static_cast<const long long*>(target)[warp]
+                                          : (long long)static_cast<const int*>(target)[warp];
+    for (int j = lane; j < width; j += 32) ir[j] = (j == id ? 1.0f : 0.0f) - yr[j];
+    if (lane == 0 && id >= 0 && id < width) loss = -log((double)yr[id]);
+  }
+  for (int o = 16; o; o >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, o);
+  if (lane == 0) row_loss[warp] = loss;
+}
+
+void launch_inject_loss(const float* y, const void* target, int target_kind, int criterion, float* inj,
+                        double* row_loss, int rows, int width, cudaStream_t s) {
+  const int threads = 256, per = threads / 32;
+  inject_loss_kernel<<<(rows + per - 1) / per, threads, 0, s>>>(y, target, target_kind, criterion, inj, row_loss,
+                                                                rows, width);
+}
+
+// fixed-order fp64 sum (deterministic run to run)
+__global__ void sum_rows_kernel(const double* v, int n, double* out) {
+  __shared__ double part[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) s += v[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = part[0];
+}
+
+void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t s) {
+  sum_rows_kernel<<<1, 256, 0, s>>>(row_loss, rows, out);
+}
+
+// ---------------------------------------------------------------------------
+// W <- W - lr * G (engine.py:606-612)
+
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, int64_t n) {
+  const int64_t n4 = n / 4;
+  float4* w4 = reinterpret_cast<float4*>(w);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = w4[i];
+    const float4 b = g4[i];
+    a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+    w4[i] = a;
+  }
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] -= lr * g[i];
+}
+
+void launch_sgd(float* w, const float* g, float lr, int64_t n, cudaStream_t s) {
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  sgd_kernel<<<(int)blocks, 256, 0, s>>>(w, g, lr, n);
+}
+
+// ---------------------------------------------------------------------------
+// W^T refresh (engine.py:138-139), 32x32 smem tiles, grouped over connections
+
+__global__ void transpose_kernel(const __grid_constant__ TransposeGroup p) {
+  __shared__ float t[32][33];
+  int jid, tile;
+  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  const TransposeJob& jb = p.job[jid];
+  const int r0 = (tile / p.tiles_c[jid]) * 32, c0 = (tile % p.tiles_c[jid]) * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + tx;
+    if (r < jb.rows && c < jb.cols) t[i][tx] = jb.src[(int64_t)r * jb.cols + c];
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + tx;
+    if (r < jb.rows && c < jb.cols) jb.dst[(int64_t)c * jb.rows + r] = t[tx][i];
+  }
+}
+
+void launch_transpose(const TransposeGroup& p, cudaStream_t s) {
+  const int tiles = p.tile_start[p.njobs];
+  if (tiles > 0) transpose_kernel<<<tiles, 256, 0, s>>>(p);
+}
+
+__global__ void fill_kernel(float* p, float v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+void launch_fill(float* p, float v, int64_t n, cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  fill_kernel<<<(int)blocks, 256, 0, s>>>(p, v, n);
+}
+
+// token ids -> one-hot rows; id < 0 means "before the stream started": a zero
+// row (kernels.py:106-115 semantics of rows_gather_add)
+__global__ void onehot_kernel(const int64_t* ids, int rows, int width, float* out) {
+  const int64_t total = (int64_t)rows * width;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / width;
+    out[e] = (ids[r] == e - r * width) ? 1.0f : 0.0f;
+  }
+}
+
+void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s) {
+  int64_t blocks = ((int64_t)rows * width + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  onehot_kernel<<<(int)blocks, 256, 0, s>>>(ids, rows, width, out);
+}
+
+__global__ void count_nonfinite_kernel(const float* p, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += isfinite(p[i]) ? 0ull : 1ull;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+void launch_count_nonfinite(const float* p, int64_t n, unsigned long long* out, cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks < 1) blocks = 1;
+  count_nonfinite_kernel<<<(int)blocks, 256, 0, s>>>(p, n, out);
+}
+
+}  // namespace rgb

@@ -1,0 +1,44 @@
+// CUDA kernels of the graph-RNN training step (SIMT fp32 path).
+//
+//   ew_chain_kernel     elementwise layer ops (activations, gates, f', eps)   K6
+//   gemm_nt_kernel      grouped C = sum_seg A_seg * B_seg^T + fused EW chain   K1/K4 (SIMT)
+//   gemm_dw_kernel      grouped G = alpha * E^T Y (weight gradients)          K5 (SIMT)
+//   softmax_rows_kernel row softmax with mirrored ring write                  K6
+//   inject_loss_kernel  delta_out = d - y and per-row loss                    K6
+//   sum_rows_kernel     deterministic fp64 loss reduction
+//   sgd_kernel          W -= lr * G                                           K6
+//   transpose_kernel    W^T refresh (grouped over connections)
+#pragma once
+#include "rgb_types.cuh"
+
+namespace rgb {
+
+struct TransposeJob {
+  const float* src;  // [rows x cols]
+  float* dst;        // [cols x rows]
+  int rows, cols;
+};
+constexpr int kMaxTr = 48;
+struct TransposeGroup {
+  int njobs, pad;
+  int tile_start[kMaxTr + 1];
+  int tiles_c[kMaxTr];
+  TransposeJob job[kMaxTr];
+};
+
+void launch_ew(const EwLaunch& p, cudaStream_t s);
+void launch_gemm_nt(const GemmGroup& p, cudaStream_t s);
+void launch_gemm_dw(const DwGroup& p, cudaStream_t s);
+void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
+// target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.
+// criterion: 0 = cross entropy (softmax output), 1 = mse (identity output).
+void launch_inject_loss(const float* y, const void* target, int target_kind, int criterion, float* inj,
+                        double* row_loss, int rows, int width, cudaStream_t s);
+void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t s);
+void launch_sgd(float* w, const float* g, float lr, int64_t n, cudaStream_t s);
+void launch_transpose(const TransposeGroup& p, cudaStream_t s);
+void launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s);
+void launch_count_nonfinite(const float* p, int64_t n, unsigned long long* out, cudaStream_t s);
+
+}  // namespace rgb

@@ -1,0 +1,591 @@
+// Schedule executor + C ABI (include/rnngraph_b200.h).
+//
+// The analyser (paper_1503_02852_b200/schedule.py) emits a flat int32
+// program: a header, a buffer table (activation rings, window error buffers,
+// chunk partials), a weight table, and step lists for the forward chunk and the
+// backward window (hoisted schedule and the frame-sequential baseline).  This
+// file resolves the program's symbolic operands (buffer, frame shift) to
+// device pointers for the current cursor and launches the kernels.  It
+// replaces the Python-dispatched loops of forward_chunk / backward_window
+// (/root/reference/pkg/src/rnngraph/engine.py:405-413, 568-599).
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rnngraph_b200.h"
+#include "rgb_kernels.cuh"
+
+using namespace rgb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+constexpr int32_t kMagic = 0x52474231;
+constexpr int kHeader = 32;
+enum BufKind { BUF_RING = 0, BUF_WIN = 1, BUF_CHUNK = 2 };
+enum Step { STEP_EW = 1, STEP_GEMM = 2, STEP_SOFTMAX = 3, STEP_LOOP = 4, STEP_DW = 5 };
+
+struct BufDesc {
+  int kind, width;
+  int64_t off;  // float offset in the workspace
+};
+struct WDesc {
+  int rows, cols;
+  int64_t off;  // float offset in W / WT / G
+};
+
+int64_t join64(int32_t lo, int32_t hi) { return (int64_t)(uint32_t)lo | ((int64_t)hi << 32); }
+int64_t pmod(int64_t a, int64_t m) { return ((a % m) + m) % m; }
+
+struct Ctx {
+  int64_t t_a = 0;        // first frame of the step
+  int frames = 0;         // frames covered by the step
+  int64_t chunk_base = 0; // frame held at index 0 of CHUNK buffers
+  int64_t t1 = 0;         // newest frame of the backward window
+  int64_t t0 = 0;         // errors are injected on (t0, t1]
+  const float* w = nullptr;
+  const float* wt = nullptr;
+  float* g = nullptr;
+};
+
+}  // namespace
+
+struct rgb_plan {
+  int S = 0, hmax = 0, cap = 0, maxd = 0;
+  int in_buf = -1, stage_buf = -1, out_buf = -1, inj_buf = -1, n_in = 0, n_out = 0;
+  int64_t scratch_off = 0, ws_floats = 0, n_params = 0;
+  std::vector<BufDesc> bufs;
+  std::vector<WDesc> wts;
+  std::vector<int32_t> prog[4];  // fwd, bwd, fwd_seq, bwd_seq
+  float* ws = nullptr;
+  int64_t cursor = 0;
+
+  // scratch layout inside the workspace (float offsets)
+  int64_t tgt_off() const { return scratch_off; }
+  int64_t rowloss_off() const {
+    int64_t tgt = (int64_t)hmax * S * (n_out > 2 ? n_out : 2);
+    return scratch_off + ((tgt + 3) & ~int64_t(3));
+  }
+  int64_t loss_off() const { return rowloss_off() + (((int64_t)hmax * S * 2 + 3) & ~int64_t(3)); }
+
+  // ---- operand resolution -------------------------------------------------
+  int resolve(const Ctx& c, int buf, int shift, int frames, float** out) const {
+    if (buf < 0 || buf >= (int)bufs.size()) return fail(RGB_ERR_KERNEL, "bad buffer id %d", buf);
+    const BufDesc& b = bufs[buf];
+    const int64_t t = c.t_a + shift;
+    const int64_t fr = (int64_t)S * b.width;
+    int64_t idx;
+    if (b.kind == BUF_RING) {
+      if (t <= cursor - cap || t + frames - 1 > cursor)
+        return fail(RGB_ERR_ENGINE, "frames [%lld, %lld] outside resident window (%lld, %lld]", (long long)t,
+                    (long long)(t + frames - 1), (long long)(cursor - cap), (long long)cursor);
+      idx = pmod(t, cap);
+    } else if (b.kind == BUF_WIN) {
+      idx = t - c.t1 + hmax - 1;
+      if (idx < 0 || idx + frames > hmax + maxd)
+        return fail(RGB_ERR_KERNEL, "window buffer %d frame %lld out of range", buf, (long long)t);
+    } else {
+      idx = t - c.chunk_base;
+      if (idx < 0 || idx + frames > hmax)
+        return fail(RGB_ERR_KERNEL, "chunk buffer %d frame %lld out of range", buf, (long long)t);
+    }
+    *out = ws + b.off + idx * fr;
+    return RGB_OK;
+  }
+
+  RingWrite ring_for(const Ctx& c) const {
+    RingWrite r;
+    r.split = (int64_t)(cap - pmod(c.t_a, cap)) * S;
+    r.frame_rows = (int64_t)cap * S;
+    return r;
+  }
+
+  // ---- program parsing ----------------------------------------------------
+  struct Reader {
+    const int32_t* p;
+    int64_t n, i = 0;
+    bool ok = true;
+    int32_t next() {
+      if (i >= n) {
+        ok = false;
+        return 0;
+      }
+      return p[i++];
+    }
+  };
+
+  int parse_op(Reader& rd, const Ctx& c, int width, bool in_gemm, EwOp& op) const {
+    std::memset(&op, 0, sizeof op);
+    op.kind = rd.next();
+    op.act = rd.next();
+    const int out_buf = rd.next();
+    float* ptr;
+    int rc = resolve(c, out_buf, 0, c.frames, &ptr);
+    if (rc) return rc;
+    if (bufs[out_buf].width != width) return fail(RGB_ERR_KERNEL, "op output width mismatch");
+    op.out = ptr;
+    op.out_is_ring = bufs[out_buf].kind == BUF_RING;
+    op.nterm = rd.next();
+    if (op.nterm > kMaxTerms) return fail(RGB_ERR_KERNEL, "too many terms");
+    for (int i = 0; i < op.nterm; ++i) {
+      int b = rd.next(), s = rd.next();
+      if ((rc = resolve(c, b, s, c.frames, &ptr))) return rc;
+      op.term[i] = ptr;
+    }
+    op.nrank1 = rd.next();
+    if (op.nrank1 > kMaxRank1) return fail(RGB_ERR_KERNEL, "too many rank-1 terms");
+    for (int i = 0; i < op.nrank1; ++i) {
+      int b = rd.next(), s = rd.next(), cid = rd.next();
+      if ((rc = resolve(c, b, s, c.frames, &ptr))) return rc;
+      op.r1src[i] = ptr;
+      if (cid < 0 || cid >= (int)wts.size() || wts[cid].rows != width)
+        return fail(RGB_ERR_KERNEL, "bad rank-1 weight %d", cid);
+      op.r1w[i] = c.w + wts[cid].off;
+    }
+    op.nfac = rd.next();
+    if (op.nfac > kMaxFac) return fail(RGB_ERR_KERNEL, "too many factors");
+    for (int i = 0; i < op.nfac; ++i) {
+      int b = rd.next(), s = rd.next();
+      if ((rc = resolve(c, b, s, c.frames, &ptr))) return rc;
+      op.fac[i] = ptr;
+    }
+    {
+      int b = rd.next(), s = rd.next();
+      if (b >= 0) {
+        if ((rc = resolve(c, b, s, c.frames, &ptr))) return rc;
+        op.y = ptr;
+      }
+    }
+    {
+      int b = rd.next(), s = rd.next();
+      if (b == -2) {
+        if (!in_gemm) return fail(RGB_ERR_KERNEL, "accumulator base outside a GEMM epilogue");
+      } else if (b >= 0) {
+        if ((rc = resolve(c, b, s, c.frames, &ptr))) return rc;
+        op.base = ptr;
+      }
+    }
+    const int inj = rd.next();
+    if (inj) {
+      const int64_t lo = c.t_a > c.t0 + 1 ? c.t_a : c.t0 + 1;
+      const int64_t hi = c.t_a + c.frames - 1;
+      if (lo <= hi) {
+        Ctx ci = c;
+        ci.t_a = lo;
+        if ((rc = resolve(ci, inj_buf, 0, (int)(hi - lo + 1), &ptr))) return rc;
+        op.inj = ptr;
+        op.inj_row0 = (int)((lo - c.t_a) * S);
+      }
+    }
+    const int neps = rd.next();
+    if (neps && neps != op.nfac) return fail(RGB_ERR_KERNEL, "eps count != factor count");
+    for (int i = 0; i < neps; ++i) {
+      int b = rd.next();
+      if (b >= 0) {
+        if ((rc = resolve(c, b, 0, c.frames, &ptr))) return rc;
+        op.eps[i] = ptr;
+      }
+    }
+    if (op.kind == EW_BWD && op.act != ACT_SOFTMAX && op.act != ACT_IDENTITY && !op.y)
+      return fail(RGB_ERR_KERNEL, "backward op needs y for f'");
+    return rd.ok ? RGB_OK : fail(RGB_ERR_KERNEL, "truncated program");
+  }
+
+  int parse_chain(Reader& rd, const Ctx& c, bool in_gemm, EwChain& ch) const {
+    ch.width = rd.next();
+    ch.nops = rd.next();
+    if (ch.nops < 1 || ch.nops > kMaxChain) return fail(RGB_ERR_KERNEL, "bad chain length %d", ch.nops);
+    for (int k = 0; k < ch.nops; ++k) {
+      int rc = parse_op(rd, c, ch.width, in_gemm && k == 0, ch.op[k]);
+      if (rc) return rc;
+    }
+    return RGB_OK;
+  }
+
+  int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) const {
+    Reader rd{p, n};
+    while (rd.i < n) {
+      const int kind = rd.next();
+      int rc = RGB_OK;
+      if (kind == STEP_EW) {
+        EwLaunch L;
+        std::memset(&L, 0, sizeof L);
+        L.nchains = rd.next();
+        if (L.nchains < 1 || L.nchains > kMaxChains) return fail(RGB_ERR_KERNEL, "bad chain count");
+        L.rows = c.frames * S;
+        L.ring = ring_for(c);
+        for (int i = 0; i < L.nchains; ++i)
+          if ((rc = parse_chain(rd, c, false, L.chain[i]))) return rc;
+        launch_ew(L, st);
+      } else if (kind == STEP_GEMM) {
+        GemmGroup G;
+        std::memset(&G, 0, sizeof G);
+        G.njobs = rd.next();
+        if (G.njobs < 1 || G.njobs > kMaxJobs) return fail(RGB_ERR_KERNEL, "bad job count");
+        G.rows = c.frames * S;
+        G.ring = ring_for(c);
+        G.tile_start[0] = 0;
+        for (int j = 0; j < G.njobs; ++j) {
+          GemmJob& jb = G.job[j];
+          jb.nseg = rd.next();
+          if (jb.nseg < 1 || jb.nseg > kMaxSegs) return fail(RGB_ERR_KERNEL, "bad segment count");
+          for (int s = 0; s < jb.nseg; ++s) {
+            const int ab = rd.next(), ash = rd.next(), cid = rd.next(), trans = rd.next();
+            float* a;
+            if ((rc = resolve(c, ab, ash, c.frames, &a))) return rc;
+            if (cid < 0 || cid >= (int)wts.size() || wts[cid].rows == 0)
+              return fail(RGB_ERR_KERNEL, "bad weight %d", cid);
+            const WDesc& wd = wts[cid];
+            jb.seg[s].a = a;
+            jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
+            jb.seg[s].k = trans ? wd.rows : wd.cols;
+            if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
+          }
+          if ((rc = parse_chain(rd, c, true, jb.epi))) return rc;
+          jb.n = jb.epi.width;
+          const int tm = (G.rows + 63) / 64, tn = (jb.n + 63) / 64;
+          G.tiles_n[j] = tn;
+          G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
+        }
+        launch_gemm_nt(G, st);
+      } else if (kind == STEP_SOFTMAX) {
+        const int b = rd.next();
+        float* y;
+        if ((rc = resolve(c, b, 0, c.frames, &y))) return rc;
+        launch_softmax(y, c.frames * S, bufs[b].width, ring_for(c), bufs[b].kind == BUF_RING, st);
+      } else if (kind == STEP_LOOP) {
+        const int reverse = rd.next();
+        const int len = rd.next();
+        if (rd.i + len > n) return fail(RGB_ERR_KERNEL, "truncated loop body");
+        for (int f = 0; f < c.frames; ++f) {
+          Ctx ci = c;
+          ci.t_a = reverse ? c.t_a + c.frames - 1 - f : c.t_a + f;
+          ci.frames = 1;
+          if ((rc = run(p + rd.i, len, ci, st))) return rc;
+        }
+        rd.i += len;
+      } else if (kind == STEP_DW) {
+        DwGroup D;
+        std::memset(&D, 0, sizeof D);
+        D.njobs = rd.next();
+        if (D.njobs < 1 || D.njobs > kMaxDw) return fail(RGB_ERR_KERNEL, "bad dW job count");
+        D.k = c.frames * S;
+        D.alpha = -1.0f;  // GradStore holds dE/dW = -sum eps y^T (engine.py:13-21)
+        for (int j = 0; j < D.njobs; ++j) {
+          const int eb = rd.next(), esh = rd.next(), yb = rd.next(), ysh = rd.next(), cid = rd.next();
+          float *e, *y;
+          if ((rc = resolve(c, eb, esh, c.frames, &e))) return rc;
+          if ((rc = resolve(c, yb, ysh, c.frames, &y))) return rc;
+          const WDesc& wd = wts[cid];
+          if (bufs[eb].width != wd.rows || bufs[yb].width != wd.cols)
+            return fail(RGB_ERR_KERNEL, "dW shape mismatch (cid %d)", cid);
+          D.job[j] = DwJob{e, y, c.g + wd.off, wd.rows, wd.cols};
+          const int tm = (wd.rows + 63) / 64, tn = (wd.cols + 63) / 64;
+          D.tiles_n[j] = tn;
+          D.tile_start[j + 1] = D.tile_start[j] + tm * tn;
+        }
+        launch_gemm_dw(D, st);
+      } else {
+        return fail(RGB_ERR_KERNEL, "unknown step %d", kind);
+      }
+      if (!rd.ok) return fail(RGB_ERR_KERNEL, "truncated program");
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return fail(RGB_ERR_CUDA, "launch failed (step %d): %s", kind, cudaGetErrorString(e));
+    }
+    return RGB_OK;
+  }
+};
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_device() {
+  int dev = 0, major = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return fail(RGB_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  if (major != 10) return fail(RGB_ERR_CUDA, "needs an sm_100 (B200) device, found compute capability %d.x", major);
+  return RGB_OK;
+}
+
+int cuda_rc(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RGB_OK;
+  return fail(RGB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int rgb_abi_version(void) { return RGB_ABI_VERSION; }
+const char* rgb_last_error(void) { return g_err.c_str(); }
+
+int rgb_plan_create(const int32_t* prog, int64_t n, rgb_plan** out) {
+  if (!prog || !out) return fail(RGB_ERR_KERNEL, "null argument");
+  *out = nullptr;
+  int rc = check_device();
+  if (rc) return rc;
+  if (n < kHeader || prog[0] != kMagic || prog[1] != 1) return fail(RGB_ERR_KERNEL, "not a schedule program");
+  rgb_plan* p = new rgb_plan();
+  p->S = prog[2];
+  p->hmax = prog[3];
+  p->cap = prog[4];
+  p->maxd = prog[5];
+  const int nb = prog[6], nw = prog[7];
+  p->in_buf = prog[8];
+  p->stage_buf = prog[9];
+  p->out_buf = prog[10];
+  p->inj_buf = prog[11];
+  p->n_in = prog[12];
+  p->n_out = prog[13];
+  p->scratch_off = join64(prog[14], prog[15]);
+  p->ws_floats = join64(prog[16], prog[17]);
+  p->n_params = join64(prog[18], prog[19]);
+  int64_t lens[4] = {prog[20], prog[21], prog[22], prog[23]};
+  int64_t pos = kHeader;
+  if (pos + 4LL * nb + 4LL * nw > n) {
+    delete p;
+    return fail(RGB_ERR_KERNEL, "truncated tables");
+  }
+  for (int i = 0; i < nb; ++i, pos += 4) p->bufs.push_back({prog[pos], prog[pos + 1], join64(prog[pos + 2], prog[pos + 3])});
+  for (int i = 0; i < nw; ++i, pos += 4) p->wts.push_back({prog[pos], prog[pos + 1], join64(prog[pos + 2], prog[pos + 3])});
+  for (int k = 0; k < 4; ++k) {
+    if (pos + lens[k] > n) {
+      delete p;
+      return fail(RGB_ERR_KERNEL, "truncated program section %d", k);
+    }
+    p->prog[k].assign(prog + pos, prog + pos + lens[k]);
+    pos += lens[k];
+  }
+  if (p->S < 1 || p->hmax < 1 || p->cap < p->hmax + p->maxd) {
+    delete p;
+    return fail(RGB_ERR_KERNEL, "bad dimensions");
+  }
+  *out = p;
+  return RGB_OK;
+}
+
+int rgb_plan_destroy(rgb_plan* p) {
+  delete p;
+  return RGB_OK;
+}
+
+int rgb_plan_workspace_bytes(const rgb_plan* p, int64_t* bytes) {
+  if (!p || !bytes) return fail(RGB_ERR_KERNEL, "null argument");
+  *bytes = p->ws_floats * 4;
+  return RGB_OK;
+}
+
+int rgb_plan_bind(rgb_plan* p, void* ws) {
+  if (!p || !ws) return fail(RGB_ERR_KERNEL, "null argument");
+  if (reinterpret_cast<uintptr_t>(ws) % 16) return fail(RGB_ERR_KERNEL, "workspace must be 16-byte aligned");
+  p->ws = static_cast<float*>(ws);
+  return RGB_OK;
+}
+
+int rgb_plan_get_cursor(const rgb_plan* p, int64_t* c) {
+  if (!p || !c) return fail(RGB_ERR_KERNEL, "null argument");
+  *c = p->cursor;
+  return RGB_OK;
+}
+
+int rgb_plan_set_cursor(rgb_plan* p, int64_t c) {
+  if (!p) return fail(RGB_ERR_KERNEL, "null argument");
+  p->cursor = c;
+  return RGB_OK;
+}
+
+int rgb_forward_chunk(rgb_plan* p, const float* w, const float* x, int x_on_host, int frames, int sequential,
+                      void* stream) {
+  if (!p || !p->ws || !x) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "advance by %d outside [1, h=%d]", frames, p->hmax);
+  cudaStream_t st = as_stream(stream);
+  float* stage = p->ws + p->bufs[p->stage_buf].off;
+  const size_t bytes = (size_t)frames * p->S * p->n_in * sizeof(float);
+  int rc = cuda_rc(cudaMemcpyAsync(stage, x, bytes, x_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st),
+                   "input copy");
+  if (rc) return rc;
+  p->cursor += frames;
+  Ctx c;
+  c.t_a = p->cursor - frames + 1;
+  c.frames = frames;
+  c.chunk_base = c.t_a;
+  c.t1 = p->cursor;
+  c.t0 = p->cursor;
+  c.w = w;
+  const auto& prog = p->prog[sequential ? 2 : 0];
+  return p->run(prog.data(), (int64_t)prog.size(), c, st);
+}
+
+int rgb_inject_output_error(rgb_plan* p, const void* target, int target_kind, int target_on_host, int criterion,
+                            int frames, void* stream) {
+  if (!p || !p->ws || !target) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "bad frame count %d", frames);
+  if (target_kind < 0 || target_kind > 2) return fail(RGB_ERR_KERNEL, "bad target kind");
+  cudaStream_t st = as_stream(stream);
+  const int rows = frames * p->S;
+  const void* tdev = target;
+  if (target_on_host) {
+    void* dst = p->ws + p->tgt_off();
+    size_t bytes = target_kind == 0 ? rows * 8 : target_kind == 1 ? rows * 4 : (size_t)rows * p->n_out * 4;
+    int rc = cuda_rc(cudaMemcpyAsync(dst, target, bytes, cudaMemcpyHostToDevice, st), "target copy");
+    if (rc) return rc;
+    tdev = dst;
+  }
+  Ctx c;
+  c.t_a = p->cursor - frames + 1;
+  c.frames = frames;
+  c.chunk_base = c.t_a;
+  float *y, *inj;
+  int rc = p->resolve(c, p->out_buf, 0, frames, &y);
+  if (rc) return rc;
+  if ((rc = p->resolve(c, p->inj_buf, 0, frames, &inj))) return rc;
+  double* row_loss = reinterpret_cast<double*>(p->ws + p->rowloss_off());
+  double* loss = reinterpret_cast<double*>(p->ws + p->loss_off());
+  launch_inject_loss(y, tdev, target_kind, criterion, inj, row_loss, rows, p->n_out, st);
+  launch_sum_rows(row_loss, rows, loss, st);
+  return cuda_rc(cudaGetLastError(), "inject launch");
+}
+
+int rgb_read_loss(rgb_plan* p, double* loss, void* stream) {
+  if (!p || !p->ws || !loss) return fail(RGB_ERR_KERNEL, "null argument");
+  cudaStream_t st = as_stream(stream);
+  int rc = cuda_rc(cudaMemcpyAsync(loss, p->ws + p->loss_off(), sizeof(double), cudaMemcpyDeviceToHost, st), "loss copy");
+  if (rc) return rc;
+  return cuda_rc(cudaStreamSynchronize(st), "loss sync");
+}
+
+int rgb_set_injection(rgb_plan* p, const float* d, int frames, void* stream) {
+  if (!p || !p->ws || !d) return fail(RGB_ERR_KERNEL, "null argument");
+  if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "bad frame count %d", frames);
+  float* inj = p->ws + p->bufs[p->inj_buf].off;
+  return cuda_rc(cudaMemcpyAsync(inj, d, (size_t)frames * p->S * p->n_out * 4, cudaMemcpyDeviceToDevice,
+                                 as_stream(stream)),
+                 "injection copy");
+}
+
+int rgb_get_injection(rgb_plan* p, float* d, int frames, void* stream) {
+  if (!p || !p->ws || !d) return fail(RGB_ERR_KERNEL, "null argument");
+  if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "bad frame count %d", frames);
+  const float* inj = p->ws + p->bufs[p->inj_buf].off;
+  return cuda_rc(cudaMemcpyAsync(d, inj, (size_t)frames * p->S * p->n_out * 4, cudaMemcpyDeviceToDevice,
+                                 as_stream(stream)),
+                 "injection copy");
+}
+
+int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_prime, int sequential, void* stream) {
+  if (!p || !p->ws || !wt || !g) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (!(1 <= h_prime && h_prime <= h)) return fail(RGB_ERR_ENGINE, "need 1 <= h'=%d <= h=%d", h_prime, h);
+  if (h > p->hmax) return fail(RGB_ERR_ENGINE, "window h=%d exceeds state h=%d", h, p->hmax);
+  if (p->cursor < h_prime) return fail(RGB_ERR_ENGINE, "t1=%lld leaves no room for %d injected frames",
+                                       (long long)p->cursor, h_prime);
+  Ctx c;
+  c.t1 = p->cursor;
+  c.t_a = c.t1 - h + 1;
+  c.frames = h;
+  c.t0 = c.t1 - h_prime;
+  c.chunk_base = c.t0 + 1;
+  c.wt = wt;
+  c.g = g;
+  const auto& prog = p->prog[sequential ? 3 : 1];
+  return p->run(prog.data(), (int64_t)prog.size(), c, as_stream(stream));
+}
+
+int rgb_sgd_update(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream) {
+  if (!p || !w || !wt || !g) return fail(RGB_ERR_KERNEL, "null argument");
+  if (!(lr > 0.0f)) return fail(RGB_ERR_ENGINE, "learning rate must be positive, got %g", (double)lr);
+  cudaStream_t st = as_stream(stream);
+  launch_sgd(w, g, lr, p->n_params, st);
+  int rc = cuda_rc(cudaGetLastError(), "sgd launch");
+  if (rc) return rc;
+  return rgb_refresh_transpose(p, w, wt, stream);
+}
+
+int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) {
+  if (!p || !w || !wt) return fail(RGB_ERR_KERNEL, "null argument");
+  TransposeGroup T;
+  std::memset(&T, 0, sizeof T);
+  for (size_t cid = 0; cid < p->wts.size(); ++cid) {
+    const WDesc& d = p->wts[cid];
+    if (d.rows == 0) continue;
+    if (T.njobs == kMaxTr) {
+      launch_transpose(T, as_stream(stream));
+      std::memset(&T, 0, sizeof T);
+    }
+    const int j = T.njobs++;
+    T.job[j] = TransposeJob{w + d.off, wt + d.off, d.rows, d.cols};
+    T.tiles_c[j] = (d.cols + 31) / 32;
+    T.tile_start[j + 1] = T.tile_start[j] + ((d.rows + 31) / 32) * T.tiles_c[j];
+  }
+  if (T.njobs) launch_transpose(T, as_stream(stream));
+  return cuda_rc(cudaGetLastError(), "transpose launch");
+}
+
+int rgb_reset_stream(rgb_plan* p, int s, void* stream) {
+  if (!p || !p->ws) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (s < 0 || s >= p->S) return fail(RGB_ERR_ENGINE, "stream %d outside [0, %d)", s, p->S);
+  for (const BufDesc& b : p->bufs) {
+    if (b.kind != BUF_RING) continue;
+    float* base = p->ws + b.off + (int64_t)s * b.width;
+    int rc = cuda_rc(cudaMemset2DAsync(base, (size_t)p->S * b.width * 4, 0, (size_t)b.width * 4, (size_t)2 * p->cap,
+                                       as_stream(stream)),
+                     "reset");
+    if (rc) return rc;
+  }
+  return RGB_OK;
+}
+
+int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* stream) {
+  if (!ids || !out || rows < 1 || width < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
+  launch_onehot(ids, rows, width, out, as_stream(stream));
+  return cuda_rc(cudaGetLastError(), "one-hot launch");
+}
+
+int rgb_inject_rows(const float* y, const void* target, int target_kind, int criterion, float* delta,
+                    double* row_loss, double* loss, int rows, int width, void* stream) {
+  if (!y || !target || !delta || !row_loss || !loss) return fail(RGB_ERR_KERNEL, "null argument");
+  if (target_kind < 0 || target_kind > 2 || rows < 1 || width < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
+  cudaStream_t st = as_stream(stream);
+  launch_inject_loss(y, target, target_kind, criterion, delta, row_loss, rows, width, st);
+  launch_sum_rows(row_loss, rows, loss, st);
+  return cuda_rc(cudaGetLastError(), "inject launch");
+}
+
+int rgb_count_nonfinite(rgb_plan* p, int buffer, int64_t t_lo, int64_t t_hi, int64_t* count, void* stream) {
+  if (!p || !p->ws || !count) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (buffer < 0 || buffer >= (int)p->bufs.size() || p->bufs[buffer].kind != 0 || t_hi < t_lo)
+    return fail(RGB_ERR_KERNEL, "bad buffer or frame range");
+  cudaStream_t st = as_stream(stream);
+  Ctx c;
+  c.t_a = t_lo;
+  c.frames = (int)(t_hi - t_lo + 1);
+  float* y;
+  int rc = p->resolve(c, buffer, 0, c.frames, &y);
+  if (rc) return rc;
+  unsigned long long* slot = reinterpret_cast<unsigned long long*>(p->ws + p->loss_off() + 2);
+  if ((rc = cuda_rc(cudaMemsetAsync(slot, 0, 8, st), "memset"))) return rc;
+  launch_count_nonfinite(y, (int64_t)c.frames * p->S * p->bufs[buffer].width, slot, st);
+  unsigned long long h = 0;
+  if ((rc = cuda_rc(cudaMemcpyAsync(&h, slot, 8, cudaMemcpyDeviceToHost, st), "count copy"))) return rc;
+  if ((rc = cuda_rc(cudaStreamSynchronize(st), "count sync"))) return rc;
+  *count = (int64_t)h;
+  return RGB_OK;
+}
+
+}  // extern "C"

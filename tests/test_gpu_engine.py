@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a path through the reference-compatible API (and so the
+C ABI) against the float64 oracle, on the same seeded inputs and weights.
+
+Tolerance (north_star): fp32 path <= 1e-4 normwise
+(||a - b||_inf / ||b||_inf) on outputs, every delta and every dW, after several
+iterations including SGD."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from golden_cases import CASES  # noqa: E402
+from oracle import engine_np as O  # noqa: E402
+from oracle_util import case_inputs, case_net, load_golden, normwise  # noqa: E402
+
+import paper_1503_02852_b200 as P  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+CE = P.Criterion.CROSS_ENTROPY_SOFTMAX
+MSE = P.Criterion.MSE_IDENTITY
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def run_pair(net, S, h, hp, iters, lr, seed, *, frame_parallel=True, crit=O.CE, hw=None, ids=False, chunk=True):
+    """Drive engine and oracle side by side; return the worst normwise error."""
+    cg = P.condense(net)
+    W = O.init_weights(net, seed)
+    st_o = O.History(net, S, h)
+    w = P.Weights(net, W)
+    st = P.StreamState(net, S, h, chunk=hp if chunk else None)
+    lin, lout = net.input_layers()[0], net.output_layers()[0]
+    rng = np.random.default_rng(seed + 99)
+    hw = hw or h
+    worst = 0.0
+    for _ in range(iters):
+        if ids:
+            xi = rng.integers(0, lin.size, size=hp * S)
+            x = np.eye(lin.size)[xi]
+        else:
+            x = rng.uniform(-1, 1, size=(hp * S, lin.size))
+        t = rng.integers(0, lout.size, size=hp * S) if crit == O.CE else rng.uniform(-1, 1, size=(hp * S, lout.size))
+        out_o = O.forward_chunk(net, cg, W, st_o, x)
+        g_o = O.backward_window(net, cg, W, st_o, st_o.cursor, hw, hp, O.inject_output_error(t, out_o))
+        inp = xi if ids else P.Batch(x, hp, S)
+        out = P.forward_chunk(net, cg, w, st, inp, frame_parallel=frame_parallel)
+        worst = max(worst, normwise(out.numpy(), out_o))
+        crit_p = CE if crit == O.CE else MSE
+        tgt = t if crit == O.CE else P.Batch(t, hp, S)
+        d = P.inject_output_error(tgt, out, crit_p, lout.activation)
+        loss = P.loss_value(tgt, out, crit_p)
+        assert abs(loss - O.loss_value(t, out_o, crit)) <= 1e-4 * max(1.0, abs(loss))
+        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, hw, hp), d, frame_parallel=frame_parallel)
+        gn = g.numpy()
+        for cid in g_o:
+            worst = max(worst, normwise(gn[cid], g_o[cid]))
+        O.sgd_update(W, g_o, lr)
+        P.sgd_update(w, g, lr)
+    wn = w.numpy()
+    for cid in W:
+        worst = max(worst, normwise(wn[cid], W[cid]))
+        assert np.array_equal(w.wt[cid].cpu().numpy(), w.w[cid].cpu().numpy().T)
+    return worst
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_cases(name):
+    spec = CASES[name]
+    net = case_net(name)
+    worst = run_pair(net, spec["S"], spec["h"], spec["hp"], spec["iters"] + 2, spec["lr"], spec["seed"],
+                     frame_parallel=spec.get("frame_parallel", True), crit=spec.get("criterion", O.CE))
+    assert worst < TOL, worst
+
+
+def test_against_reference_golden_directly():
+    """cfg1 outputs/grads of the reference itself (no oracle in between)."""
+    spec = CASES["cfg1"]
+    gold = load_golden("cfg1")
+    net = case_net("cfg1")
+    cg = P.condense(net)
+    w = P.Weights.init(net, spec["seed"])
+    st = P.StreamState(net, spec["S"], spec["h"], chunk=spec["hp"])
+    for it, (x, t) in enumerate(case_inputs("cfg1", net)):
+        out = P.forward_chunk(net, cg, w, st, P.Batch(x, spec["hp"], spec["S"]))
+        assert normwise(out.numpy(), gold[f"out_{it}"]) < TOL
+        d = P.inject_output_error(t, out, CE, P.Activation.SOFTMAX)
+        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, spec["h"], spec["hp"]), d)
+        gn = g.numpy()
+        for cid in gn:
+            assert normwise(gn[cid], gold[f"g_{it}_{cid}"]) < TOL, (it, cid)
+        P.sgd_update(w, g, spec["lr"])
+
+
+@pytest.mark.parametrize("seq", [False, True])
+def test_configs_small_scale(seq):
+    """cfg5 (custom graph, d=1/2 edges) and stacked LSTMs, both schedules."""
+    assert run_pair(P.build_custom_graph(), 1, 32, 16, 4, 1e-3, 0, frame_parallel=not seq) < TOL
+    assert run_pair(P.build_stacked_lstm(32, [32, 32], 32), 4, 8, 4, 4, 1e-2, 1, frame_parallel=not seq) < TOL
+
+
+def test_cfg1_many_iterations():
+    assert run_pair(P.build_lstm(39, 128, 39), 1, 32, 16, 8, 1e-3, 0) < TOL
+
+
+def test_multistream_and_windows():
+    net = P.build_lstm(9, 24, 7)
+    assert run_pair(net, 16, 12, 4, 6, 1e-2, 2) < TOL
+    assert run_pair(net, 3, 12, 4, 6, 1e-2, 2, hw=7) < TOL       # window shorter than state
+    assert run_pair(net, 3, 10, 3, 6, 1e-2, 2, chunk=False) < TOL  # ring capacity not a multiple of h'
+
+
+def test_mse_identity_output():
+    net = P.build_elman(4, 6, 3, output_activation=P.Activation.IDENTITY)
+    assert run_pair(net, 2, 6, 3, 5, 0.05, 4, crit=O.MSE) < TOL
+
+
+def test_id_inputs_equal_one_hot():
+    assert run_pair(P.build_lstm(11, 8, 11), 2, 6, 3, 4, 0.05, 5, ids=True) < TOL
+
+
+def test_multi_stream_equals_sum_of_single_runs():
+    """reference tests/test_acceptance.py:180-207, with tolerance."""
+    net = P.build_elman(5, 4, 5)
+    cg = P.condense(net)
+    rng = np.random.default_rng(11)
+    S, hp, h = 4, 3, 6
+    xs = rng.uniform(-1, 1, size=(3, S, hp, 5))
+    ts = rng.integers(0, 5, size=(3, S, hp))
+    w = P.Weights.init(net, 9)
+
+    def run(streams):
+        st = P.StreamState(net, len(streams), h)
+        g = None
+        for c in range(3):
+            x = np.stack([xs[c, s] for s in streams], axis=1).reshape(-1, 5)
+            t = np.stack([ts[c, s] for s in streams], axis=1).reshape(-1)
+            out = P.forward_chunk(net, cg, w, st, P.Batch(x, hp, len(streams)))
+            d = P.inject_output_error(t, out, CE, P.Activation.SOFTMAX)
+            g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, h, hp), d)
+        return g
+
+    multi = run([0, 1, 2, 3])
+    single = run([0])
+    for s in (1, 2, 3):
+        single.add_(run([s]))
+    assert multi.frames_streams == single.frames_streams == 6 * 4
+    a, b = multi.numpy(), single.numpy()
+    for cid in a:
+        assert normwise(a[cid], b[cid]) < 1e-5
+
+
+def test_chunking_does_not_change_activations():
+    net = P.build_lstm(3, 4, 3)
+    cg = P.condense(net)
+    w = P.Weights.init(net, 2)
+    xs = np.random.default_rng(3).uniform(-1, 1, size=(12, 3))
+    whole = P.forward_chunk(net, cg, w, P.StreamState(net, 1, 12), P.Batch(xs, 12, 1)).numpy()
+    st = P.StreamState(net, 1, 12)
+    parts = [P.forward_chunk(net, cg, w, st, P.Batch(xs[i:i + 4], 4, 1)).numpy() for i in range(0, 12, 4)]
+    assert normwise(np.vstack(parts), whole) < 1e-6
+
+
+def test_reset_stream_restores_fresh_context():
+    net = P.build_lstm(3, 3, 3)
+    cg = P.condense(net)
+    w = P.Weights.init(net, 5)
+    warm = P.StreamState(net, 1, 4)
+    P.forward_chunk(net, cg, w, warm, np.array([0, 1, 2, 0]))
+    warm.reset_stream(0)
+    a = P.forward_chunk(net, cg, w, warm, np.array([2, 1])).numpy()
+    b = P.forward_chunk(net, cg, w, P.StreamState(net, 1, 4), np.array([2, 1])).numpy()
+    assert np.array_equal(a, b)
+
+
+def test_backward_is_pure_and_deterministic():
+    net = P.build_lstm(6, 10, 6)
+    cg = P.condense(net)
+    w = P.Weights.init(net, 1)
+    st = P.StreamState(net, 3, 8)
+    x = np.random.default_rng(0).uniform(-1, 1, size=(8 * 3, 6))
+    out = P.forward_chunk(net, cg, w, st, P.Batch(x, 8, 3))
+    d = P.inject_output_error(np.zeros(24, dtype=np.int64), out, CE, P.Activation.SOFTMAX)
+    g1 = P.backward_window(net, cg, w, st, P.BpttWindow(8, 8, 8), d).numpy()
+    g2 = P.backward_window(net, cg, w, st, P.BpttWindow(8, 8, 8), d).numpy()
+    for cid in g1:
+        assert np.array_equal(g1[cid], g2[cid])
+
+
+def test_guards():
+    net = P.build_elman(2, 2, 2)
+    cg = P.condense(net)
+    w = P.Weights.init(net, 0)
+    st = P.StreamState(net, 2, h=4)
+    with pytest.raises(P.EngineError, match="streams"):
+        P.forward_chunk(net, cg, w, st, P.Batch(np.zeros((3, 2)), 3, 1))
+    with pytest.raises(P.EngineError, match="width"):
+        P.forward_chunk(net, cg, w, st, P.Batch(np.zeros((4, 3)), 2, 2))
+    with pytest.raises(P.EngineError, match="ids outside"):
+        P.forward_chunk(net, cg, w, st, np.array([0, 5, 0, 1]))
+    with pytest.raises(P.EngineError, match="tile"):
+        P.forward_chunk(net, cg, w, st, np.array([0, 1, 0]))
+    P.forward_chunk(net, cg, w, st, np.array([0, 1, 0, 1]))
+    with pytest.raises(P.EngineError, match="mode"):
+        P.forward_chunk(net, cg, w, st, P.Batch(np.zeros((4, 2)), 2, 2))
+    st1 = P.StreamState(net, 1, h=4)
+    P.forward_chunk(net, cg, w, st1, np.array([0, 1]))
+    delta = P.Batch(torch.zeros((2, 2), device="cuda"), 2, 1)
+    with pytest.raises(P.EngineError, match="cursor"):
+        P.backward_window(net, cg, w, st1, P.BpttWindow(4, 4, 2), delta)
+    with pytest.raises(P.EngineError, match="exceeds state"):
+        P.backward_window(net, cg, w, st1, P.BpttWindow(2, 6, 2), delta)
+    with pytest.raises(P.EngineError, match="delta_out"):
+        P.backward_window(net, cg, w, st1, P.BpttWindow(2, 2, 1), delta)
+    with pytest.raises(P.EngineError, match="positive"):
+        P.sgd_update(w, P.GradStore.zeros(net), 0.0)
+
+
+def test_check_finite_names_the_layer():
+    net = P.build_elman(2, 3, 2)
+    cg = P.condense(net)
+    w = P.Weights.init(net, 0)
+    w.w[net.find_connection("in", "hidden").id][0, 0] = float("nan")
+    w.refresh()
+    st = P.StreamState(net, 1, h=2)
+    with pytest.raises(FloatingPointError, match="hidden"):
+        P.forward_chunk(net, cg, w, st, P.Batch(np.ones((2, 2)), 2, 1), check_finite=True)
+
+
+def test_softmax_feeding_other_layers_cannot_backpropagate():
+    from paper_1503_02852_b200.netdef import ConnectionDef, LayerDef, NetworkDef, Role
+    net = NetworkDef(
+        layers=(LayerDef(0, "in", 2, role=Role.INPUT),
+                LayerDef(1, "out", 2, activation=P.Activation.SOFTMAX, role=Role.OUTPUT), LayerDef(2, "tap", 2)),
+        connections=(ConnectionDef(0, 0, 1), ConnectionDef(1, 1, 2)),
+    )
+    cg = P.condense(net)
+    w = P.Weights.init(net, 0)
+    st = P.StreamState(net, 1, h=2)
+    out = P.forward_chunk(net, cg, w, st, P.Batch(np.ones((2, 2)), 2, 1))
+    d = P.inject_output_error(np.array([0, 1]), out, CE, P.Activation.SOFTMAX)
+    with pytest.raises(P.EngineError, match="softmax"):
+        P.backward_window(net, cg, w, st, P.BpttWindow(2, 2, 2), d)
+
+
+def test_train_loop_matches_oracle_training():
+    """train_loop (fused inject + lazy loss) tracks the oracle's SGD run."""
+    net = P.build_lstm(6, 12, 6)
+    cfg = P.TrainConfig(h=8, h_prime=4, lr=0.05, iterations=10, seed=3)
+
+    class Src:
+        n_streams = 3
+
+        def __init__(self):
+            self.rng = np.random.default_rng(1)
+
+        def next_batch(self, hp):
+            from types import SimpleNamespace
+            rows = hp * self.n_streams
+            return SimpleNamespace(inputs=P.Batch(self.rng.uniform(-1, 1, size=(rows, 6)), hp, 3),
+                                   targets=self.rng.integers(0, 6, size=rows), new_sequence=None)
+
+    w, metrics = P.train_loop(net, Src(), cfg)
+    W = O.init_weights(net, 3)
+    st = O.History(net, 3, 8)
+    cg = P.condense(net)
+    src = Src()
+    for m in metrics:
+        b = src.next_batch(4)
+        loss, _, _ = O.train_step(net, cg, W, st, b.inputs.values, b.targets, 8, 0.05)
+        assert abs(m.loss - loss / 12) < 1e-4 * max(1.0, abs(loss / 12))
+    wn = w.numpy()
+    for cid in W:
+        assert normwise(wn[cid], W[cid]) < TOL
