@@ -110,6 +110,19 @@ int rgb_reset_stream(rgb_plan* plan, int stream_index, void* stream);
  * check_finite guard, engine.py:415-417); result copied to *count (sync). */
 int rgb_count_nonfinite(rgb_plan* plan, int buffer, int64_t t_lo, int64_t t_hi, int64_t* count, void* stream);
 
+/* Instrumentation (no reference counterpart; the reference times whole
+ * iterations with perf_counter, engine.py:733-758).  rgb_launch_count: kernel
+ * launches issued by this library since load.  When profiling is enabled
+ * every launch is bracketed by CUDA events on its stream; collect()
+ * synchronises and accumulates device time, algorithmic FLOPs and bytes per
+ * category (0 ew, 1 hoisted gemm, 2 per-frame gemm, 3 per-frame ew, 4 dW,
+ * 5 softmax, 6 inject, 7 sgd, 8 transpose, 9 persistent SCC). */
+int rgb_launch_count(int64_t* n);
+int rgb_profile_enable(int on);
+int rgb_profile_collect(void);
+int rgb_profile_reset(void);
+int rgb_profile_read(int category, double* ms, int64_t* launches, double* flops, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

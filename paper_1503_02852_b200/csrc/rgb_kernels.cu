@@ -55,7 +55,7 @@ __device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, i
     case EW_BWD: {
       float v = has_acc ? acc : (op.base ? op.base[e] : 0.0f);
       for (int i = 0; i < op.nterm; ++i) v += op.term[i][e];
-      if (op.act != ACT_SOFTMAX) v *= act_deriv(op.act, op.y[e]);
+      if (op.act == ACT_SIGMOID || op.act == ACT_TANH) v *= act_deriv(op.act, op.y[e]);
       if (op.inj && r >= op.inj_row0) v += op.inj[(r - op.inj_row0) * width + j];  // after f' (engine.py:548-554)
       op.out[e] = v;
       for (int i = 0; i < op.nfac; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)

@@ -18,6 +18,7 @@
 
 #include "../../include/rnngraph_b200.h"
 #include "rgb_kernels.cuh"
+#include "rgb_prof.cuh"
 
 using namespace rgb;
 
@@ -61,7 +62,22 @@ struct Ctx {
   const float* w = nullptr;
   const float* wt = nullptr;
   float* g = nullptr;
+  bool in_loop = false;
 };
+
+// algorithmic bytes of one elementwise chain over `rows` rows (reads + one
+// write per output; the ring mirror copy is an implementation cost, not counted)
+double ew_bytes(const EwChain& ch, int64_t rows) {
+  double words = 0;
+  for (int k = 0; k < ch.nops; ++k) {
+    const EwOp& o = ch.op[k];
+    int rd = o.nterm + o.nfac + (o.y ? 1 : 0) + (o.base ? 1 : 0) + (o.inj ? 1 : 0);
+    int wr = 1;
+    for (int i = 0; i < kMaxFac; ++i) wr += o.eps[i] ? 1 : 0;
+    words += rd + wr;
+  }
+  return 4.0 * words * (double)rows * ch.width;
+}
 
 }  // namespace
 
@@ -231,7 +247,12 @@ struct rgb_plan {
         L.ring = ring_for(c);
         for (int i = 0; i < L.nchains; ++i)
           if ((rc = parse_chain(rd, c, false, L.chain[i]))) return rc;
+        double bytes = 0;
+        for (int i = 0; i < L.nchains; ++i) bytes += ew_bytes(L.chain[i], L.rows);
+        const int slot = prof_start(st);
         launch_ew(L, st);
+        note_launch();
+        prof_stop(slot, st, c.in_loop ? PROF_EW_FRAME : PROF_EW, 0.0, bytes);
       } else if (kind == STEP_GEMM) {
         GemmGroup G;
         std::memset(&G, 0, sizeof G);
@@ -262,12 +283,25 @@ struct rgb_plan {
           G.tiles_n[j] = tn;
           G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
         }
+        double flops = 0, bytes = 0;
+        for (int j = 0; j < G.njobs; ++j) {
+          int64_t ksum = 0;
+          for (int s = 0; s < G.job[j].nseg; ++s) ksum += G.job[j].seg[s].k;
+          flops += 2.0 * G.rows * G.job[j].n * (double)ksum;
+          bytes += 4.0 * ((double)G.rows * ksum + (double)G.job[j].n * ksum) + ew_bytes(G.job[j].epi, G.rows);
+        }
+        const int slot = prof_start(st);
         launch_gemm_nt(G, st);
+        note_launch();
+        prof_stop(slot, st, c.in_loop ? PROF_GEMM_FRAME : PROF_GEMM, flops, bytes);
       } else if (kind == STEP_SOFTMAX) {
         const int b = rd.next();
         float* y;
         if ((rc = resolve(c, b, 0, c.frames, &y))) return rc;
+        const int slot = prof_start(st);
         launch_softmax(y, c.frames * S, bufs[b].width, ring_for(c), bufs[b].kind == BUF_RING, st);
+        note_launch();
+        prof_stop(slot, st, PROF_SOFTMAX, 0.0, 8.0 * c.frames * S * bufs[b].width);
       } else if (kind == STEP_LOOP) {
         const int reverse = rd.next();
         const int len = rd.next();
@@ -276,6 +310,7 @@ struct rgb_plan {
           Ctx ci = c;
           ci.t_a = reverse ? c.t_a + c.frames - 1 - f : c.t_a + f;
           ci.frames = 1;
+          ci.in_loop = true;
           if ((rc = run(p + rd.i, len, ci, st))) return rc;
         }
         rd.i += len;
@@ -299,7 +334,15 @@ struct rgb_plan {
           D.tiles_n[j] = tn;
           D.tile_start[j + 1] = D.tile_start[j] + tm * tn;
         }
+        double flops = 0, bytes = 0;
+        for (int j = 0; j < D.njobs; ++j) {
+          flops += 2.0 * D.k * (double)D.job[j].m * D.job[j].n;
+          bytes += 4.0 * ((double)D.k * (D.job[j].m + D.job[j].n) + (double)D.job[j].m * D.job[j].n);
+        }
+        const int slot = prof_start(st);
         launch_gemm_dw(D, st);
+        note_launch();
+        prof_stop(slot, st, PROF_DW, flops, bytes);
       } else {
         return fail(RGB_ERR_KERNEL, "unknown step %d", kind);
       }
@@ -458,8 +501,12 @@ int rgb_inject_output_error(rgb_plan* p, const void* target, int target_kind, in
   if ((rc = p->resolve(c, p->inj_buf, 0, frames, &inj))) return rc;
   double* row_loss = reinterpret_cast<double*>(p->ws + p->rowloss_off());
   double* loss = reinterpret_cast<double*>(p->ws + p->loss_off());
+  const int slot = prof_start(st);
   launch_inject_loss(y, tdev, target_kind, criterion, inj, row_loss, rows, p->n_out, st);
   launch_sum_rows(row_loss, rows, loss, st);
+  note_launch();
+  note_launch();
+  prof_stop(slot, st, PROF_INJECT, 0.0, 8.0 * rows * p->n_out);
   return cuda_rc(cudaGetLastError(), "inject launch");
 }
 
@@ -511,7 +558,10 @@ int rgb_sgd_update(rgb_plan* p, float* w, float* wt, const float* g, float lr, v
   if (!p || !w || !wt || !g) return fail(RGB_ERR_KERNEL, "null argument");
   if (!(lr > 0.0f)) return fail(RGB_ERR_ENGINE, "learning rate must be positive, got %g", (double)lr);
   cudaStream_t st = as_stream(stream);
+  const int slot = prof_start(st);
   launch_sgd(w, g, lr, p->n_params, st);
+  note_launch();
+  prof_stop(slot, st, PROF_SGD, 2.0 * p->n_params, 12.0 * p->n_params);
   int rc = cuda_rc(cudaGetLastError(), "sgd launch");
   if (rc) return rc;
   return rgb_refresh_transpose(p, w, wt, stream);
@@ -526,6 +576,7 @@ int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) 
     if (d.rows == 0) continue;
     if (T.njobs == kMaxTr) {
       launch_transpose(T, as_stream(stream));
+      note_launch();
       std::memset(&T, 0, sizeof T);
     }
     const int j = T.njobs++;
@@ -533,7 +584,14 @@ int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) 
     T.tiles_c[j] = (d.cols + 31) / 32;
     T.tile_start[j + 1] = T.tile_start[j] + ((d.rows + 31) / 32) * T.tiles_c[j];
   }
-  if (T.njobs) launch_transpose(T, as_stream(stream));
+  if (T.njobs) {
+    int64_t elems = 0;
+    for (int j = 0; j < T.njobs; ++j) elems += (int64_t)T.job[j].rows * T.job[j].cols;
+    const int slot = prof_start(as_stream(stream));
+    launch_transpose(T, as_stream(stream));
+    note_launch();
+    prof_stop(slot, as_stream(stream), PROF_TRANSPOSE, 0.0, 8.0 * elems);
+  }
   return cuda_rc(cudaGetLastError(), "transpose launch");
 }
 
@@ -554,6 +612,7 @@ int rgb_reset_stream(rgb_plan* p, int s, void* stream) {
 int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* stream) {
   if (!ids || !out || rows < 1 || width < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
   launch_onehot(ids, rows, width, out, as_stream(stream));
+  note_launch();
   return cuda_rc(cudaGetLastError(), "one-hot launch");
 }
 
@@ -564,6 +623,8 @@ int rgb_inject_rows(const float* y, const void* target, int target_kind, int cri
   cudaStream_t st = as_stream(stream);
   launch_inject_loss(y, target, target_kind, criterion, delta, row_loss, rows, width, st);
   launch_sum_rows(row_loss, rows, loss, st);
+  note_launch();
+  note_launch();
   return cuda_rc(cudaGetLastError(), "inject launch");
 }
 
@@ -581,6 +642,7 @@ int rgb_count_nonfinite(rgb_plan* p, int buffer, int64_t t_lo, int64_t t_hi, int
   unsigned long long* slot = reinterpret_cast<unsigned long long*>(p->ws + p->loss_off() + 2);
   if ((rc = cuda_rc(cudaMemsetAsync(slot, 0, 8, st), "memset"))) return rc;
   launch_count_nonfinite(y, (int64_t)c.frames * p->S * p->bufs[buffer].width, slot, st);
+  note_launch();
   unsigned long long h = 0;
   if ((rc = cuda_rc(cudaMemcpyAsync(&h, slot, 8, cudaMemcpyDeviceToHost, st), "count copy"))) return rc;
   if ((rc = cuda_rc(cudaStreamSynchronize(st), "count sync"))) return rc;
