@@ -1,0 +1,398 @@
+"""Benchmark: BPTT(h; h') training frames/s of the graph-RNN step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+A *step* is one training iteration: forward over h' new frames per stream,
+fused softmax-xent error injection + loss, backward over the h-frame window,
+weight gradients, (N > 1: NCCL all-reduce of the flat gradient), SGD and the
+W^T refresh -- the reference's train_loop iteration (engine.py:732-758).
+frames/s = h' * S_total / seconds per step (engine.py:751-757, cli.py:335-346).
+
+``value`` is measured with inputs resident in HBM (a pool of device batches),
+CUDA events on the launching stream, max over ranks.  ``e2e`` is the same
+metric through the public API (Trainer.step = the C-ABI calls) with pinned
+HOST inputs/targets copied in and the loss read back every step.  The CPU
+baseline is the float64 oracle (oracle/engine_np.py, numpy BLAS, all host
+threads) on a bounded sample of the same workload -- the only place bench.py
+executes oracle/.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "cfg1": dict(desc="1-layer LSTM 128 (peepholes, forget gate), 39 in/out, 1 stream, h=32, h'=16",
+                 n_in=39, cells=[128], n_out=39, S=1, h=32, hp=16, lr=1e-3),
+    "cfg2": dict(desc="2-layer LSTM 512, 512 in/out, 1 stream, h'=T=256, h=512",
+                 n_in=512, cells=[512, 512], n_out=512, S=1, h=512, hp=256, lr=1e-3),
+    "cfg3": dict(desc="2-layer LSTM 512, 512 in/out, 64 streams, h=32, h'=16",
+                 n_in=512, cells=[512, 512], n_out=512, S=64, h=32, hp=16, lr=1e-3),
+    "cfg4": dict(desc="3-layer LSTM 1024, 1024 in/out, 512 streams (sharded over the GPUs), h=32, h'=16",
+                 n_in=1024, cells=[1024, 1024, 1024], n_out=1024, S=512, h=32, hp=16, lr=1e-3),
+    "cfg5": dict(desc="custom graph RNN (mult. layers, d=1,2 edges), 39-128-39, 1 stream, h=32, h'=16",
+                 custom=True, n_in=39, n_out=39, S=1, h=32, hp=16, lr=1e-3),
+}
+METRIC = "BPTT training frames/sec (LSTM, fwd+bwd+update) at 1/2/4/8 B200 vs CPU oracle"
+
+
+def build_net(cfg):
+    import paper_1503_02852_b200 as P
+    if cfg.get("custom"):
+        return P.build_custom_graph(cfg["n_in"], 128, cfg["n_out"])
+    return P.build_stacked_lstm(cfg["n_in"], cfg["cells"], cfg["n_out"])
+
+
+def algorithmic_flops(net, S, h, hp):
+    """F_iter = S * sum_dense R*C*[2h' + 2(h-d)[src in Delta] + 2h[dst in Delta]]."""
+    from paper_1503_02852_b200.netdef import Role
+    delta = {l.id for l in net.layers if l.role is not Role.INPUT and net.anterior(l.id)}
+    tot = 0
+    for c in net.iter_dense():
+        rc = net.layer(c.dst).size * net.layer(c.src).size
+        tot += rc * (2 * hp + (2 * (h - c.delay) if c.src in delta else 0) + (2 * h if c.dst in delta else 0))
+    return S * tot
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (oracle)
+
+
+def cpu_oracle_rate(cfg, n_streams, min_seconds=10.0, max_iters=12, warm=2, seed=0):
+    """Oracle iterations/s on ``n_streams`` streams of the workload -> frames/s."""
+    from oracle import engine_np as O
+    import paper_1503_02852_b200 as P
+    net = build_net(cfg)
+    cg = P.condense(net)
+    W = O.init_weights(net, seed)
+    st = O.History(net, n_streams, cfg["h"])
+    rng = np.random.default_rng(seed)
+    hp = cfg["hp"]
+    times = []
+    for it in range(warm + max_iters):
+        x = rng.uniform(-1, 1, size=(hp * n_streams, cfg["n_in"]))
+        t = rng.integers(0, cfg["n_out"], size=hp * n_streams)
+        t0 = time.perf_counter()
+        O.train_step(net, cg, W, st, x, t, cfg["h"], cfg["lr"])
+        dt = time.perf_counter() - t0
+        if it >= warm:
+            times.append(dt)
+            if sum(times) >= min_seconds:
+                break
+    return hp * n_streams / (sum(times) / len(times)), len(times), sum(times)
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:  # noqa: BLE001
+        pass
+    return os.cpu_count() or 1
+
+
+def cpu_sample_streams(cfg) -> int:
+    """Bounded sample: streams of the workload the oracle runs (~10-30 s)."""
+    return {"cfg4": 32, "cfg3": 64, "cfg2": 1}.get(cfg["name"], cfg["S"])
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n = cpu_sample_streams(cfg)
+    if cfg["name"] == "cfg2":
+        cfg = dict(cfg, hp=32, h=64)  # bounded: a 1/8 slice of the T=256 window
+    rates = []
+    from oracle import engine_np as O
+    import paper_1503_02852_b200 as P
+    net = build_net(cfg)
+    cg = P.condense(net)
+    W = O.init_weights(net, 0)
+    st = O.History(net, n, cfg["h"])
+    rng = np.random.default_rng(0)
+    for it in range(args.warmup + args.steps):
+        x = rng.uniform(-1, 1, size=(cfg["hp"] * n, cfg["n_in"]))
+        t = rng.integers(0, cfg["n_out"], size=cfg["hp"] * n)
+        t0 = time.perf_counter()
+        O.train_step(net, cg, W, st, x, t, cfg["h"], cfg["lr"])
+        if it >= args.warmup:
+            rates.append(cfg["hp"] * n / (time.perf_counter() - t0))
+    value = len(rates) / sum(1.0 / r for r in rates)
+    sample = f"{n} of {cfg['S']} streams of {cfg['name']}, h={cfg['h']}, h'={cfg['hp']}, float64 numpy"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["hp"] * n / value,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg["name"] + ": " + cfg["desc"]},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def prof_snapshot(L):
+    import ctypes
+    out = {}
+    for i, name in enumerate(("ew", "gemm", "gemm_frame", "ew_frame", "dw", "softmax", "inject", "sgd", "transpose",
+                              "scc")):
+        ms, n, fl, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        L.rgb_profile_read(i, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl), ctypes.byref(by))
+        if n.value:
+            out[name] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+    return out
+
+
+def launches(L):
+    import ctypes
+    v = ctypes.c_int64()
+    L.rgb_launch_count(ctypes.byref(v))
+    return v.value
+
+
+def measure_intra_stream(P, steps=2):
+    """cfg2 single stream: hoisted (paper) vs frame-sequential (baseline) schedule."""
+    import torch
+    cfg = CONFIGS["cfg2"]
+    net = build_net(dict(cfg, name="cfg2"))
+    res = {}
+    for label, fp in (("hoisted", True), ("sequential", False)):
+        w = P.Weights.init(net, 0)
+        tr = P.Trainer(net, w, 1, P.TrainConfig(h=cfg["h"], h_prime=cfg["hp"], lr=cfg["lr"], iterations=1,
+                                                 frame_parallel=fp))
+        g = torch.Generator(device="cuda").manual_seed(1)
+        x = torch.rand((cfg["hp"], cfg["n_in"]), device="cuda", generator=g) * 2 - 1
+        t = torch.randint(0, cfg["n_out"], (cfg["hp"],), device="cuda", generator=g)
+        for _ in range(3):  # fill the 512-frame window
+            tr.step(x, t)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            tr.step(x, t)
+        e1.record()
+        torch.cuda.synchronize()
+        res[label] = cfg["hp"] / (e0.elapsed_time(e1) / steps / 1000.0)
+    return {"workload": "cfg2: " + cfg["desc"], "hoisted_frames_per_s": res["hoisted"],
+            "sequential_frames_per_s": res["sequential"], "speedup": res["hoisted"] / res["sequential"],
+            "steps": steps}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1503_02852_b200 as P
+    from paper_1503_02852_b200 import _lib
+    from paper_1503_02852_b200.dist import GradientExchange, init_from_env, shard_streams
+
+    rank, world, local = init_from_env("nccl")
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L = _lib.lib()
+    ex = GradientExchange()
+    S_total = cfg["S"] * (world if args.scaling == "weak" else 1)
+    lo, hi = shard_streams(S_total, world, rank)
+    S = hi - lo
+    h, hp = cfg["h"], cfg["hp"]
+    net = build_net(cfg)
+    w = P.Weights.init(net, 0)  # identical on every rank (same seed)
+    tr = P.Trainer(net, w, S, P.TrainConfig(h=h, h_prime=hp, lr=cfg["lr"], iterations=1))
+    pool = 4
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    xs = [torch.rand((hp * S, cfg["n_in"]), device=dev, generator=g) * 2 - 1 for _ in range(pool)]
+    ts = [torch.randint(0, cfg["n_out"], (hp * S,), device=dev, generator=g) for _ in range(pool)]
+    exch = ex if world > 1 else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also fills the h-frame window: ceil(h/h') iterations)
+    for i in range(max(args.warmup, math.ceil(h / hp) + 1)):
+        tr.step(xs[i % pool], ts[i % pool], exch)
+    torch.cuda.synchronize()
+
+    # (A) headline: device-resident inputs, CUDA events, max over ranks
+    n0 = launches(L)
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            tr.step(xs[i % pool], ts[i % pool], exch)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    n_launch = launches(L) - n0
+    ms = ex.max_(e0.elapsed_time(e1) / args.steps, dev)
+    value = hp * S_total / (ms / 1000.0)
+
+    # (B) profiled pass: per-launch CUDA events -> per-kernel device time
+    L.rgb_profile_reset()
+    L.rgb_profile_enable(1)
+    for i in range(args.steps):
+        tr.step(xs[i % pool], ts[i % pool], exch)
+    L.rgb_profile_collect()
+    L.rgb_profile_enable(0)
+    prof = prof_snapshot(L)
+
+    # (C) e2e through the public API with pinned HOST buffers + loss read-back
+    hx = [x.cpu().pin_memory() for x in xs]
+    ht = [t.cpu().pin_memory() for t in ts]
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        tr.step(hx[i % pool], ht[i % pool], exch)
+        tr.loss()
+    e2e_s = ex.max_((time.perf_counter() - t0) / args.steps, dev)
+    e2e = {"value": hp * S_total / e2e_s, "unit": "frames/s",
+           "h2d_bytes_per_step": int(hx[0].numel() * 4 + ht[0].numel() * 8), "d2h_bytes_per_step": 8}
+
+    if rank != 0:
+        return 0
+    peaks = {}
+    pk = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tflops = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    peak_src = "measured" if peaks else "fallback"
+    top = max(prof, key=lambda k: prof[k]["ms"])
+    p = prof[top]
+    per_launch_s = p["ms"] / 1000.0 / p["launches"]
+    if p["flops"] > 0:
+        achieved = p["flops"] / p["launches"] / per_launch_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tflops, "unit": "TFLOP/s", "frac": achieved / tflops}
+    else:
+        achieved = p["bytes"] / p["launches"] / per_launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm}
+    roof.update({"traffic": None, "kernel": top, "peak_source": peak_src + " (MEASURED_PEAKS.json)",
+                 "share_of_step": p["ms"] / sum(v["ms"] for v in prof.values())})
+    F_iter = algorithmic_flops(net, S_total, h, hp)
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic (U(-1,1) inputs, uniform class targets, "
+                                                     "Weights.init seed 0)",
+        "config": {"workload": cfg["name"] + ": " + cfg["desc"], "streams_total": S_total, "streams_per_gpu": S,
+                   "h": h, "h_prime": hp, "global_batch_frames": hp * S_total,
+                   "parallelism": f"dp{world} (streams sharded, NCCL all-reduce of dW)",
+                   "l2": "no flush: per-step working set (history + W + W^T + dW) exceeds the 126 MB L2",
+                   "schedule": "hoisted (paper §3.1)"},
+        "algorithmic_tflops": F_iter / (ms / 1000.0) / 1e12,
+        "roofline": roof,
+        "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps}
+                    for k, v in prof.items()},
+        "e2e": e2e,
+        "clocks": clocks.summary(),
+        "gpu_launches": n_launch,
+    }
+    if world == 1 and not args.no_cpu:
+        n = cpu_sample_streams(cfg)
+        rate, iters, secs = cpu_oracle_rate(cfg, n, min_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
+                                "sample": f"oracle (float64 numpy) on {n} of {cfg['S']} streams of {cfg['name']}, "
+                                          f"{iters} iterations after 2 warm-up, {secs:.1f} s"}
+    if world == 1 and not args.no_intra:
+        line["intra_stream"] = measure_intra_stream(P)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-intra", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

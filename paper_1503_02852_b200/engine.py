@@ -571,7 +571,9 @@ class Trainer:
         self._lib = _lib.lib()
         self._seq = 0 if config.frame_parallel else 1
 
-    def step(self, inputs, targets) -> None:
+    def step(self, inputs, targets, exchange=None) -> None:
+        """One iteration.  ``exchange`` (dist.GradientExchange) sums the
+        gradient buffer over ranks between backward and SGD."""
         L, st, plan = self._lib, self._stream(), self.state._plan.handle
         hp = self.cfg.h_prime
         if isinstance(inputs, torch.Tensor) and inputs.is_cuda:
@@ -601,6 +603,8 @@ class Trainer:
             raise EngineError(f"softmax layer {self.state.program.softmax_feeds!r} feeds other layers")
         _lib.check(L.rgb_backward_window(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat), self.cfg.h, hp,
                                          self._seq, st))
+        if exchange is not None:
+            exchange.allreduce_(self.grads.flat)
         _lib.check(L.rgb_sgd_update(self.weights._plan.handle, _ptr(self.weights.flat), _ptr(self.weights.flat_t),
                                     _ptr(self.grads.flat), ctypes.c_float(self.cfg.lr), st))
 
