@@ -110,6 +110,16 @@ int rgb_reset_stream(rgb_plan* plan, int stream_index, void* stream);
  * check_finite guard, engine.py:415-417); result copied to *count (sync). */
 int rgb_count_nonfinite(rgb_plan* plan, int buffer, int64_t t_lo, int64_t t_hi, int64_t* count, void* stream);
 
+/* GEMM engine: 0 auto (tcgen05 3xTF32 above a work threshold, SIMT fp32
+ * for latency-bound small products), 1 SIMT only, 2 tcgen05 only.  The
+ * reference's deterministic k-ascending GEMMs are kernels.py:84-103. */
+int rgb_set_gemm_mode(int mode);
+/* Stand-alone GEMM forms (kernel-level parity tests): C[m,n] = A[m,k] . B[n,k]
+ * (both row-major) and G[m,n] = alpha * sum_r E[r,m] Y[r,n]; mode 1 SIMT,
+ * 2 tcgen05. */
+int rgb_gemm_nt(const float* a, const float* b, float* c, int m, int n, int k, int mode, void* stream);
+int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, float alpha, int mode, void* stream);
+
 /* Instrumentation (no reference counterpart; the reference times whole
  * iterations with perf_counter, engine.py:733-758).  rgb_launch_count: kernel
  * launches issued by this library since load.  When profiling is enabled

@@ -29,6 +29,10 @@ struct TransposeGroup {
 void launch_ew(const EwLaunch& p, cudaStream_t s);
 void launch_gemm_nt(const GemmGroup& p, cudaStream_t s);
 void launch_gemm_dw(const DwGroup& p, cudaStream_t s);
+// tcgen05 (3xTF32, TMEM accumulator) versions of the two GEMM forms; same
+// descriptors, tiles recomputed for 128 x {64,128,256} (rgb_tc_gemm.cu).
+void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s);
+void launch_tc_gemm_dw(DwGroup p, cudaStream_t s);
 void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.
 // criterion: 0 = cross entropy (softmax output), 1 = mse (identity output).

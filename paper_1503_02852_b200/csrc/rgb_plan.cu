@@ -79,6 +79,13 @@ double ew_bytes(const EwChain& ch, int64_t rows) {
   return 4.0 * words * (double)rows * ch.width;
 }
 
+// GEMM engine selection: 0 auto (tcgen05 above a work threshold, SIMT for the
+// latency-bound small products), 1 SIMT only, 2 tcgen05 only.
+int g_gemm_mode = 0;
+constexpr double kTcMinFlops = 32.0 * 1024 * 1024;
+
+bool use_tc(double flops) { return g_gemm_mode == 2 || (g_gemm_mode == 0 && flops >= kTcMinFlops); }
+
 }  // namespace
 
 struct rgb_plan {
@@ -291,7 +298,8 @@ struct rgb_plan {
           bytes += 4.0 * ((double)G.rows * ksum + (double)G.job[j].n * ksum) + ew_bytes(G.job[j].epi, G.rows);
         }
         const int slot = prof_start(st);
-        launch_gemm_nt(G, st);
+        if (use_tc(flops)) launch_tc_gemm_nt(G, st);
+        else launch_gemm_nt(G, st);
         note_launch();
         prof_stop(slot, st, c.in_loop ? PROF_GEMM_FRAME : PROF_GEMM, flops, bytes);
       } else if (kind == STEP_SOFTMAX) {
@@ -340,7 +348,8 @@ struct rgb_plan {
           bytes += 4.0 * ((double)D.k * (D.job[j].m + D.job[j].n) + (double)D.job[j].m * D.job[j].n);
         }
         const int slot = prof_start(st);
-        launch_gemm_dw(D, st);
+        if (use_tc(flops)) launch_tc_gemm_dw(D, st);
+        else launch_gemm_dw(D, st);
         note_launch();
         prof_stop(slot, st, PROF_DW, flops, bytes);
       } else {
@@ -377,6 +386,54 @@ int cuda_rc(cudaError_t e, const char* what) {
 extern "C" {
 
 int rgb_abi_version(void) { return RGB_ABI_VERSION; }
+
+int rgb_set_gemm_mode(int mode) {
+  if (mode < 0 || mode > 2) return fail(RGB_ERR_KERNEL, "gemm mode must be 0 (auto), 1 (simt) or 2 (tcgen05)");
+  g_gemm_mode = mode;
+  return RGB_OK;
+}
+
+int rgb_gemm_nt(const float* a, const float* b, float* c, int m, int n, int k, int mode, void* stream) {
+  if (!a || !b || !c || m < 1 || n < 1 || k < 1 || mode < 1 || mode > 2) return fail(RGB_ERR_KERNEL, "bad arguments");
+  GemmGroup G;
+  std::memset(&G, 0, sizeof G);
+  G.njobs = 1;
+  G.rows = m;
+  GemmJob& jb = G.job[0];
+  jb.nseg = 1;
+  jb.seg[0] = Seg{a, b, k, 0};
+  jb.n = n;
+  jb.epi.width = n;
+  jb.epi.nops = 1;
+  jb.epi.op[0].kind = EW_FWD_ADD;
+  jb.epi.op[0].out = c;
+  G.tiles_n[0] = (n + 63) / 64;
+  G.tile_start[1] = ((m + 63) / 64) * G.tiles_n[0];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (mode == 2) launch_tc_gemm_nt(G, st);
+  else launch_gemm_nt(G, st);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+}
+
+int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, float alpha, int mode, void* stream) {
+  if (!e || !y || !g || m < 1 || n < 1 || k < 1 || mode < 1 || mode > 2) return fail(RGB_ERR_KERNEL, "bad arguments");
+  DwGroup D;
+  std::memset(&D, 0, sizeof D);
+  D.njobs = 1;
+  D.k = k;
+  D.alpha = alpha;
+  D.job[0] = DwJob{e, y, g, m, n};
+  D.tiles_n[0] = (n + 63) / 64;
+  D.tile_start[1] = ((m + 63) / 64) * D.tiles_n[0];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (mode == 2) launch_tc_gemm_dw(D, st);
+  else launch_gemm_dw(D, st);
+  note_launch();
+  cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "dW launch: %s", cudaGetErrorString(err));
+}
 const char* rgb_last_error(void) { return g_err.c_str(); }
 
 int rgb_plan_create(const int32_t* prog, int64_t n, rgb_plan** out) {

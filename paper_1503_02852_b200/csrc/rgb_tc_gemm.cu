@@ -1,0 +1,394 @@
+// tcgen05 grouped GEMMs for sm_100a (5th-gen tensor cores, TMEM accumulators).
+//
+// fp32-exact mode = 3xTF32: every fp32 operand x is split on the fly into
+// hi = tf32(x) and lo = tf32(x - hi); the tile product is accumulated in fp32
+// TMEM as hi*hi + hi*lo + lo*hi (the lo*lo term is below fp32 rounding of the
+// result), which keeps the normwise error ~1e-6 -- inside the fp32 path's
+// 1e-4 bound, unlike single-pass TF32 (~1e-3).
+//
+// Roles (256 threads, one CTA per output tile, 1 CTA/SM by smem):
+//   warps 0-3  producers: coalesced 16-B global loads of the fp32 A/B tiles,
+//              split into hi/lo, stored into the 128-byte-swizzled UMMA
+//              canonical layout (K-major or MN-major, so dW's transposed
+//              operands need no transpose pass), fence.proxy.async, arrive
+//              on the stage's "full" mbarrier;
+//   warp 4     one elected thread issues 3 x (BK/8) tcgen05.mma.kind::tf32
+//              per stage and tcgen05.commit's the stage back to the
+//              producers ("empty"), and the accumulator to the epilogue;
+//   warps 0-7  epilogue: tcgen05.ld the accumulator (32x32b.x16) and run the
+//              fused elementwise chain (bias, identity terms, activation,
+//              f', gate co-factors, eps) or the dW store.
+//
+// Descriptor bit layouts follow the SM100 UMMA smem / instruction descriptor
+// formats (vendored CUTLASS cute/arch/mma_sm100_desc.hpp); all code here is
+// hand-written.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rgb_ew.cuh"
+#include "rgb_kernels.cuh"
+
+namespace rgb {
+namespace tc {
+
+constexpr int BM = 128;   // UMMA M, cta_group::1
+constexpr int BK = 32;    // fp32 per stage along K: one 128-byte swizzle row
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// SM100 shared-memory matrix descriptor, SWIZZLE_128B, version 1.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, M x N, majors.
+__device__ __forceinline__ uint32_t idesc_tf32(int m, int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// One operand tile source: `rows` is the valid extent along M (or N), `kv` the
+// valid extent along K, ld the global leading dimension (elements).
+struct Src {
+  const float* p;
+  int64_t ld;
+  int rows, kv;
+  bool vec;  // 16-byte loads allowed
+};
+
+// Load the [MN x BK] tile (MN = TILE rows starting at mn0, K from k0) of one
+// operand, split it, and store hi/lo into swizzled smem.  K-major source: the
+// K index is contiguous in global memory; MN-major: the MN index is.
+template <int TILE, bool MN_MAJOR>
+__device__ __forceinline__ void produce(const Src& s, int mn0, int k0, float* hi, float* lo, int tid) {
+  constexpr int CH = TILE * BK / 4;  // 16-byte chunks in the tile
+#pragma unroll 4
+  for (int q = tid; q < CH; q += 128) {
+    int r, kk, byte;  // r: MN index in tile, kk: K index in tile (multiple of 4 along the chunk dim)
+    float4 v;
+    if (!MN_MAJOR) {
+      r = q >> 3;
+      const int c = q & 7;
+      kk = c * 4;
+      byte = r * 128 + ((c ^ (r & 7)) << 4);
+      const int gr = mn0 + r, gk = k0 + kk;
+      const float* src = s.p + (int64_t)gr * s.ld + gk;
+      if (gr < s.rows && s.vec && gk + 3 < s.kv) {
+        v = __ldg(reinterpret_cast<const float4*>(src));
+      } else {
+        v.x = (gr < s.rows && gk + 0 < s.kv) ? src[0] : 0.f;
+        v.y = (gr < s.rows && gk + 1 < s.kv) ? src[1] : 0.f;
+        v.z = (gr < s.rows && gk + 2 < s.kv) ? src[2] : 0.f;
+        v.w = (gr < s.rows && gk + 3 < s.kv) ? src[3] : 0.f;
+      }
+    } else {
+      constexpr int CPR = TILE / 4;  // chunks per K row
+      kk = q / CPR;
+      const int cm = q % CPR;
+      r = cm * 4;
+      byte = ((kk >> 3) * (TILE / 32) + (cm >> 3)) * 1024 + (kk & 7) * 128 + (((cm & 7) ^ (kk & 7)) << 4);
+      const int gk = k0 + kk, gr = mn0 + r;
+      const float* src = s.p + (int64_t)gk * s.ld + gr;
+      if (gk < s.kv && s.vec && gr + 3 < s.rows) {
+        v = __ldg(reinterpret_cast<const float4*>(src));
+      } else {
+        v.x = (gk < s.kv && gr + 0 < s.rows) ? src[0] : 0.f;
+        v.y = (gk < s.kv && gr + 1 < s.rows) ? src[1] : 0.f;
+        v.z = (gk < s.kv && gr + 2 < s.rows) ? src[2] : 0.f;
+        v.w = (gk < s.kv && gr + 3 < s.rows) ? src[3] : 0.f;
+      }
+    }
+    float4 h, l;
+    h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+    h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+    h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+    h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+    *reinterpret_cast<float4*>(reinterpret_cast<char*>(hi) + byte) = h;
+    *reinterpret_cast<float4*>(reinterpret_cast<char*>(lo) + byte) = l;
+  }
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 2 : (BN == 128 ? 3 : 4);
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ void find_job(const int* tile_start, int njobs, int bid, int& job, int& tile) {
+  job = 0;
+  while (job + 1 < njobs && bid >= tile_start[job + 1]) ++job;
+  tile = bid - tile_start[job];
+}
+
+// IS_DW = false: C[r, n] = sum_seg A_seg[r, :] . B_seg[n, :] (both K-major), EW-chain epilogue.
+// IS_DW = true:  G[m, n] = alpha * sum_k E[k, m] Y[k, n] (both MN-major), plain store.
+template <int BN, bool IS_DW, class P>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ P p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* done = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int jid, tile;
+  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  const int tiles_n = p.tiles_n[jid];
+  const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+
+  // problem geometry for this job
+  int M, N, nstages;
+  if constexpr (IS_DW) {
+    M = p.job[jid].m;
+    N = p.job[jid].n;
+    nstages = (p.k + BK - 1) / BK;
+  } else {
+    M = p.rows;
+    N = p.job[jid].n;
+    nstages = 0;
+    for (int s = 0; s < p.job[jid].nseg; ++s) nstages += (p.job[jid].seg[s].k + BK - 1) / BK;
+  }
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 128);  // every producer thread arrives after its own proxy fence
+      mbar_init(&empty[s], 1);  // tcgen05.commit
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- producers ----------------
+    int seg = 0, k0 = 0;
+    for (int it = 0; it < nstages; ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+      uint8_t* base = smem + s * C::STAGE_BYTES;
+      float* a_hi = reinterpret_cast<float*>(base);
+      float* a_lo = reinterpret_cast<float*>(base + C::A_BYTES);
+      float* b_hi = reinterpret_cast<float*>(base + 2 * C::A_BYTES);
+      float* b_lo = reinterpret_cast<float*>(base + 2 * C::A_BYTES + C::B_BYTES);
+      if constexpr (IS_DW) {
+        const auto& jb = p.job[jid];
+        const bool va = (jb.m % 4 == 0) && (reinterpret_cast<uintptr_t>(jb.e) % 16 == 0);
+        const bool vb = (jb.n % 4 == 0) && (reinterpret_cast<uintptr_t>(jb.y) % 16 == 0);
+        produce<BM, true>(Src{jb.e, jb.m, M, p.k, va}, m0, k0, a_hi, a_lo, threadIdx.x);
+        produce<BN, true>(Src{jb.y, jb.n, N, p.k, vb}, n0, k0, b_hi, b_lo, threadIdx.x);
+        k0 += BK;
+      } else {
+        const Seg& sg = p.job[jid].seg[seg];
+        const bool va = (sg.k % 4 == 0) && (reinterpret_cast<uintptr_t>(sg.a) % 16 == 0);
+        const bool vb = (sg.k % 4 == 0) && (reinterpret_cast<uintptr_t>(sg.b) % 16 == 0);
+        produce<BM, false>(Src{sg.a, sg.k, M, sg.k, va}, m0, k0, a_hi, a_lo, threadIdx.x);
+        produce<BN, false>(Src{sg.b, sg.k, N, sg.k, vb}, n0, k0, b_hi, b_lo, threadIdx.x);
+        k0 += BK;
+        if (k0 >= sg.k) {
+          k0 = 0;
+          ++seg;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+    }
+  } else if (warp == 4 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
+    const uint32_t idesc = idesc_tf32(BM, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+    for (int it = 0; it < nstages; ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait(&full[s], (it / C::STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+      const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
+      const uint32_t b_hi = base + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
+#pragma unroll
+      for (int j = 0; j < BK / 8; ++j) {
+        // K-major: +32 B per k-step inside the swizzled row; MN-major: next 8-row K group
+        const uint32_t ao = IS_DW ? j * (BM / 32) * 1024 : j * 32;
+        const uint32_t bo = IS_DW ? j * (BN / 32) * 1024 : j * 32;
+        const uint32_t albo = IS_DW ? 1024 : 16, asbo = IS_DW ? (BM / 32) * 1024 : 1024;
+        const uint32_t blbo = IS_DW ? 1024 : 16, bsbo = IS_DW ? (BN / 32) * 1024 : 1024;
+        const uint64_t dah = smem_desc(a_hi + ao, albo, asbo), dal = smem_desc(a_lo + ao, albo, asbo);
+        const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo), dbl = smem_desc(b_lo + bo, blbo, bsbo);
+        const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+        mma_tf32(tmem, dal, dbh, idesc, acc0);  // small terms first
+        mma_tf32(tmem, dah, dbl, idesc, 1u);
+        mma_tf32(tmem, dah, dbh, idesc, 1u);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(done);
+  }
+
+  // ---------------- epilogue (all 8 warps) ----------------
+  mbar_wait(done, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = m0 + quarter * 32 + lane;
+  for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
+    if (n0 + cc >= N) break;  // warp-uniform
+    float v[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+    if (row >= M) continue;
+    if constexpr (IS_DW) {
+      const auto& jb = p.job[jid];
+      float* g = jb.g + (int64_t)row * N + n0 + cc;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n0 + cc + j < N) g[j] = p.alpha * v[j];
+    } else {
+      const auto& epi = p.job[jid].epi;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = n0 + cc + j;
+        if (col >= N) break;
+        for (int k = 0; k < epi.nops; ++k) ew_apply(epi.op[k], N, row, col, p.ring, k == 0, v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+template <int BN, bool IS_DW, class P>
+void launch_one(P p, int tiles, cudaStream_t s) {
+  static bool configured = false;
+  auto k = tc_gemm_kernel<BN, IS_DW, P>;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+    configured = true;
+  }
+  k<<<tiles, kThreads, Cfg<BN>::SMEM, s>>>(p);
+}
+
+// Widest N tile that still gives most SMs a tile.
+template <class F>
+int pick_bn(F tiles_for) {
+  if (tiles_for(256) >= 120) return 256;
+  if (tiles_for(128) >= 120) return 128;
+  return 64;
+}
+
+}  // namespace tc
+
+void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
+  auto tiles_for = [&](int bn) {
+    int t = 0;
+    for (int j = 0; j < p.njobs; ++j) t += ((p.rows + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
+    return t;
+  };
+  const int bn = tc::pick_bn(tiles_for);
+  p.tile_start[0] = 0;
+  for (int j = 0; j < p.njobs; ++j) {
+    p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
+    p.tile_start[j + 1] = p.tile_start[j] + ((p.rows + tc::BM - 1) / tc::BM) * p.tiles_n[j];
+  }
+  const int tiles = p.tile_start[p.njobs];
+  if (tiles == 0) return;
+  if (bn == 256) tc::launch_one<256, false>(p, tiles, s);
+  else if (bn == 128) tc::launch_one<128, false>(p, tiles, s);
+  else tc::launch_one<64, false>(p, tiles, s);
+}
+
+void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
+  auto tiles_for = [&](int bn) {
+    int t = 0;
+    for (int j = 0; j < p.njobs; ++j) t += ((p.job[j].m + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
+    return t;
+  };
+  const int bn = tc::pick_bn(tiles_for);
+  p.tile_start[0] = 0;
+  for (int j = 0; j < p.njobs; ++j) {
+    p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
+    p.tile_start[j + 1] = p.tile_start[j] + ((p.job[j].m + tc::BM - 1) / tc::BM) * p.tiles_n[j];
+  }
+  const int tiles = p.tile_start[p.njobs];
+  if (tiles == 0) return;
+  if (bn == 256) tc::launch_one<256, true>(p, tiles, s);
+  else if (bn == 128) tc::launch_one<128, true>(p, tiles, s);
+  else tc::launch_one<64, true>(p, tiles, s);
+}
+
+}  // namespace rgb

@@ -1,0 +1,94 @@
+"""Kernel-level parity of the two GEMM engines (SIMT fp32 and tcgen05 3xTF32)
+against float64 numpy, through the C ABI's stand-alone GEMM entry points, and
+full-engine parity with every GEMM forced onto the tensor cores."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle_util import normwise  # noqa: E402
+
+import paper_1503_02852_b200 as P  # noqa: E402
+from paper_1503_02852_b200 import _lib  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 256, 32), (256, 512, 1024), (200, 300, 70), (1, 64, 512), (77, 39, 39), (1024, 2048, 1024),
+          (513, 130, 257)]
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("m,n,k", SHAPES)
+def test_gemm_nt(mode, m, n, k):
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    a = rng.uniform(-1, 1, size=(m, k))
+    b = rng.uniform(-1, 1, size=(n, k))
+    ta = torch.tensor(a, dtype=torch.float32, device="cuda")
+    tb = torch.tensor(b, dtype=torch.float32, device="cuda")
+    tc = torch.full((m, n), float("nan"), device="cuda")
+    _lib.check(_lib.lib().rgb_gemm_nt(ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()),
+                                      ctypes.c_void_p(tc.data_ptr()), m, n, k, mode, _stream()))
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    err = normwise(tc.cpu().numpy(), ref)
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("m,n,k", SHAPES)
+def test_gemm_dw(mode, m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    e = rng.uniform(-1, 1, size=(k, m))
+    y = rng.uniform(-1, 1, size=(k, n))
+    te = torch.tensor(e, dtype=torch.float32, device="cuda")
+    ty = torch.tensor(y, dtype=torch.float32, device="cuda")
+    tg = torch.full((m, n), float("nan"), device="cuda")
+    _lib.check(_lib.lib().rgb_gemm_dw(ctypes.c_void_p(te.data_ptr()), ctypes.c_void_p(ty.data_ptr()),
+                                      ctypes.c_void_p(tg.data_ptr()), m, n, k, ctypes.c_float(-1.0), mode,
+                                      _stream()))
+    ref = -(e.astype(np.float32).astype(np.float64).T @ y.astype(np.float32).astype(np.float64))
+    err = normwise(tg.cpu().numpy(), ref)
+    assert err < 1e-5, err
+
+
+def test_engine_parity_with_tensor_cores_forced():
+    """Every GEMM of the step (hoisted, per-frame, dW) on tcgen05."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_gemm_mode(2))
+    try:
+        assert run_pair(P.build_lstm(39, 128, 39), 2, 32, 16, 4, 1e-3, 0) < 1e-4
+        assert run_pair(P.build_custom_graph(), 3, 16, 8, 4, 1e-3, 1) < 1e-4
+        assert run_pair(P.build_stacked_lstm(64, [96, 64], 48), 5, 12, 4, 4, 1e-2, 2) < 1e-4
+        assert run_pair(P.build_elman(5, 7, 6), 3, 6, 3, 4, 0.05, 3) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_gemm_mode(0))
+
+
+def test_engine_parity_simt_forced():
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_gemm_mode(1))
+    try:
+        assert run_pair(P.build_stacked_lstm(256, [256, 256], 256), 64, 8, 4, 3, 1e-3, 4) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_gemm_mode(0))
+
+
+def test_engine_parity_large_auto():
+    """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
+    from test_gpu_engine import run_pair
+    assert run_pair(P.build_stacked_lstm(512, [512, 512], 512), 64, 32, 16, 3, 1e-3, 5) < 1e-4
