@@ -8,10 +8,12 @@
 //
 // Roles (256 threads, one CTA per output tile, 1 CTA/SM by smem):
 //   warps 0-3  producers: coalesced 16-B global loads of the fp32 A/B tiles,
-//              split into hi/lo, stored into the 128-byte-swizzled UMMA
-//              canonical layout (K-major or MN-major, so dW's transposed
-//              operands need no transpose pass), fence.proxy.async, arrive
-//              on the stage's "full" mbarrier;
+//              split into hi/lo, stored into the 128-byte-swizzled K-major
+//              UMMA canonical layout (dW's MN-contiguous operands are
+//              transposed while loading, so there is no transpose pass;
+//              kind::tf32 with MN-major SW128 descriptors returns zeros on
+//              sm_100a -- tools/tc_probe.cu), fence.proxy.async, arrive on
+//              the stage's "full" mbarrier;
 //   warp 4     one elected thread issues 3 x (BK/8) tcgen05.mma.kind::tf32
 //              per stage and tcgen05.commit's the stage back to the
 //              producers ("empty"), and the accumulator to the epilogue;
@@ -145,21 +147,21 @@ __device__ __forceinline__ void produce(const Src& s, int mn0, int k0, float* hi
         v.w = (gr < s.rows && gk + 3 < s.kv) ? src[3] : 0.f;
       }
     } else {
-      constexpr int CPR = TILE / 4;  // chunks per K row
-      kk = q / CPR;
-      const int cm = q % CPR;
-      r = cm * 4;
-      byte = ((kk >> 3) * (TILE / 32) + (cm >> 3)) * 1024 + (kk & 7) * 128 + (((cm & 7) ^ (kk & 7)) << 4);
-      const int gk = k0 + kk, gr = mn0 + r;
+      // MN-contiguous source, transposed on the fly into the K-major layout:
+      // lane -> consecutive MN rows, so each of the four k loads is one
+      // coalesced 128-byte row segment across the warp, and the 16-byte
+      // stores of 8 consecutive rows hit 8 distinct swizzled chunks.
+      r = q % TILE;
+      const int c = q / TILE;
+      kk = c * 4;
+      byte = r * 128 + ((c ^ (r & 7)) << 4);
+      const int gr = mn0 + r, gk = k0 + kk;
       const float* src = s.p + (int64_t)gk * s.ld + gr;
-      if (gk < s.kv && s.vec && gr + 3 < s.rows) {
-        v = __ldg(reinterpret_cast<const float4*>(src));
-      } else {
-        v.x = (gk < s.kv && gr + 0 < s.rows) ? src[0] : 0.f;
-        v.y = (gk < s.kv && gr + 1 < s.rows) ? src[1] : 0.f;
-        v.z = (gk < s.kv && gr + 2 < s.rows) ? src[2] : 0.f;
-        v.w = (gk < s.kv && gr + 3 < s.rows) ? src[3] : 0.f;
-      }
+      const bool okr = gr < s.rows;
+      v.x = (okr && gk + 0 < s.kv) ? __ldg(src) : 0.f;
+      v.y = (okr && gk + 1 < s.kv) ? __ldg(src + s.ld) : 0.f;
+      v.z = (okr && gk + 2 < s.kv) ? __ldg(src + 2 * s.ld) : 0.f;
+      v.w = (okr && gk + 3 < s.kv) ? __ldg(src + 3 * s.ld) : 0.f;
     }
     float4 h, l;
     h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
@@ -187,7 +189,8 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
 }
 
 // IS_DW = false: C[r, n] = sum_seg A_seg[r, :] . B_seg[n, :] (both K-major), EW-chain epilogue.
-// IS_DW = true:  G[m, n] = alpha * sum_k E[k, m] Y[k, n] (both MN-major), plain store.
+// IS_DW = true:  G[m, n] = alpha * sum_k E[k, m] Y[k, n] (both MN-contiguous in
+//                global memory, K-major in smem), plain store.
 template <int BN, bool IS_DW, class P>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ P p) {
   using C = Cfg<BN>;
@@ -271,7 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   } else if (warp == 4 && lane == 0) {
     // ---------------- MMA issuer ----------------
     const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
-    const uint32_t idesc = idesc_tf32(BM, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+    // both operands are K-major in smem (the dW producer transposes while loading)
+    const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
       mbar_wait(&full[s], (it / C::STAGES) & 1);
@@ -281,13 +285,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const uint32_t b_hi = base + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
 #pragma unroll
       for (int j = 0; j < BK / 8; ++j) {
-        // K-major: +32 B per k-step inside the swizzled row; MN-major: next 8-row K group
-        const uint32_t ao = IS_DW ? j * (BM / 32) * 1024 : j * 32;
-        const uint32_t bo = IS_DW ? j * (BN / 32) * 1024 : j * 32;
-        const uint32_t albo = IS_DW ? 1024 : 16, asbo = IS_DW ? (BM / 32) * 1024 : 1024;
-        const uint32_t blbo = IS_DW ? 1024 : 16, bsbo = IS_DW ? (BN / 32) * 1024 : 1024;
-        const uint64_t dah = smem_desc(a_hi + ao, albo, asbo), dal = smem_desc(a_lo + ao, albo, asbo);
-        const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo), dbl = smem_desc(b_lo + bo, blbo, bsbo);
+        // K-major SW128: the j-th 8-deep k-step starts 32 B into each swizzled
+        // 128-byte row; 8-row groups are 1024 B apart (SBO); LBO unused.
+        const uint32_t off = j * 32;
+        const uint64_t dah = smem_desc(a_hi + off, 16, 1024), dal = smem_desc(a_lo + off, 16, 1024);
+        const uint64_t dbh = smem_desc(b_hi + off, 16, 1024), dbl = smem_desc(b_lo + off, 16, 1024);
         const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
         mma_tf32(tmem, dal, dbh, idesc, acc0);  // small terms first
         mma_tf32(tmem, dah, dbl, idesc, 1u);
