@@ -36,7 +36,7 @@ namespace tc {
 
 constexpr int BM = 128;   // UMMA M, cta_group::1
 constexpr int BK = 32;    // fp32 per stage along K: one 128-byte swizzle row
-constexpr int kThreads = 256;
+constexpr int kThreads = 288;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -121,57 +121,65 @@ struct Src {
   bool vec;  // 16-byte loads allowed
 };
 
-// Load the [MN x BK] tile (MN = TILE rows starting at mn0, K from k0) of one
-// operand, split it, and store hi/lo into swizzled smem.  K-major source: the
-// K index is contiguous in global memory; MN-major: the MN index is.
+constexpr int kProducers = 256;  // warps 0-7 produce (and run the epilogue); warp 8 issues MMAs
+
+// Two-phase tile producer: every global load of a stage is issued before any
+// of them is consumed (one memory latency per stage instead of one per
+// chunk), then the fp32 values are split into tf32 hi/lo and stored into the
+// 128-byte-swizzled K-major layout: row r at r*128 B, 16-byte chunk c at
+// (c ^ (r & 7)).  K-major source: the chunk is one 16-B load; MN-contiguous
+// source (dW operands): lanes walk consecutive rows and gather the chunk's four
+// k values with coalesced 4-B loads, i.e. the tile is transposed on the fly.
 template <int TILE, bool MN_MAJOR>
-__device__ __forceinline__ void produce(const Src& s, int mn0, int k0, float* hi, float* lo, int tid) {
-  constexpr int CH = TILE * BK / 4;  // 16-byte chunks in the tile
-#pragma unroll 4
-  for (int q = tid; q < CH; q += 128) {
-    int r, kk, byte;  // r: MN index in tile, kk: K index in tile (multiple of 4 along the chunk dim)
-    float4 v;
-    if (!MN_MAJOR) {
-      r = q >> 3;
-      const int c = q & 7;
-      kk = c * 4;
-      byte = r * 128 + ((c ^ (r & 7)) << 4);
-      const int gr = mn0 + r, gk = k0 + kk;
-      const float* src = s.p + (int64_t)gr * s.ld + gk;
-      if (gr < s.rows && s.vec && gk + 3 < s.kv) {
-        v = __ldg(reinterpret_cast<const float4*>(src));
+struct TileLoad {
+  static constexpr int NPT = TILE * BK / 4 / kProducers;  // 16-B chunks per producer thread
+  float4 v[NPT];
+
+  __device__ __forceinline__ void load(const Src& s, int mn0, int k0, int tid) {
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      const int q = tid + i * kProducers;
+      int r, c;
+      if (!MN_MAJOR) { r = q >> 3; c = q & 7; } else { r = q % TILE; c = q / TILE; }
+      const int gr = mn0 + r, gk = k0 + c * 4;
+      if (!MN_MAJOR) {
+        const float* src = s.p + (int64_t)gr * s.ld + gk;
+        if (gr < s.rows && s.vec && gk + 3 < s.kv) {
+          v[i] = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          v[i].x = (gr < s.rows && gk + 0 < s.kv) ? src[0] : 0.f;
+          v[i].y = (gr < s.rows && gk + 1 < s.kv) ? src[1] : 0.f;
+          v[i].z = (gr < s.rows && gk + 2 < s.kv) ? src[2] : 0.f;
+          v[i].w = (gr < s.rows && gk + 3 < s.kv) ? src[3] : 0.f;
+        }
       } else {
-        v.x = (gr < s.rows && gk + 0 < s.kv) ? src[0] : 0.f;
-        v.y = (gr < s.rows && gk + 1 < s.kv) ? src[1] : 0.f;
-        v.z = (gr < s.rows && gk + 2 < s.kv) ? src[2] : 0.f;
-        v.w = (gr < s.rows && gk + 3 < s.kv) ? src[3] : 0.f;
+        const float* src = s.p + (int64_t)gk * s.ld + gr;
+        const bool ok = gr < s.rows;
+        v[i].x = (ok && gk + 0 < s.kv) ? __ldg(src) : 0.f;
+        v[i].y = (ok && gk + 1 < s.kv) ? __ldg(src + s.ld) : 0.f;
+        v[i].z = (ok && gk + 2 < s.kv) ? __ldg(src + 2 * s.ld) : 0.f;
+        v[i].w = (ok && gk + 3 < s.kv) ? __ldg(src + 3 * s.ld) : 0.f;
       }
-    } else {
-      // MN-contiguous source, transposed on the fly into the K-major layout:
-      // lane -> consecutive MN rows, so each of the four k loads is one
-      // coalesced 128-byte row segment across the warp, and the 16-byte
-      // stores of 8 consecutive rows hit 8 distinct swizzled chunks.
-      r = q % TILE;
-      const int c = q / TILE;
-      kk = c * 4;
-      byte = r * 128 + ((c ^ (r & 7)) << 4);
-      const int gr = mn0 + r, gk = k0 + kk;
-      const float* src = s.p + (int64_t)gk * s.ld + gr;
-      const bool okr = gr < s.rows;
-      v.x = (okr && gk + 0 < s.kv) ? __ldg(src) : 0.f;
-      v.y = (okr && gk + 1 < s.kv) ? __ldg(src + s.ld) : 0.f;
-      v.z = (okr && gk + 2 < s.kv) ? __ldg(src + 2 * s.ld) : 0.f;
-      v.w = (okr && gk + 3 < s.kv) ? __ldg(src + 3 * s.ld) : 0.f;
     }
-    float4 h, l;
-    h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
-    h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
-    h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
-    h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
-    *reinterpret_cast<float4*>(reinterpret_cast<char*>(hi) + byte) = h;
-    *reinterpret_cast<float4*>(reinterpret_cast<char*>(lo) + byte) = l;
   }
-}
+
+  __device__ __forceinline__ void store(float* hi, float* lo, int tid) const {
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      const int q = tid + i * kProducers;
+      int r, c;
+      if (!MN_MAJOR) { r = q >> 3; c = q & 7; } else { r = q % TILE; c = q / TILE; }
+      const int byte = r * 128 + ((c ^ (r & 7)) << 4);
+      float4 h, l;
+      h.x = tf32_rna(v[i].x); l.x = tf32_rna(v[i].x - h.x);
+      h.y = tf32_rna(v[i].y); l.y = tf32_rna(v[i].y - h.y);
+      h.z = tf32_rna(v[i].z); l.z = tf32_rna(v[i].z - h.z);
+      h.w = tf32_rna(v[i].w); l.w = tf32_rna(v[i].w - h.w);
+      *reinterpret_cast<float4*>(reinterpret_cast<char*>(hi) + byte) = h;
+      *reinterpret_cast<float4*>(reinterpret_cast<char*>(lo) + byte) = l;
+    }
+  }
+};
 
 template <int BN>
 struct Cfg {
@@ -180,6 +188,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_LD = BN + 4;  // padded staging row (conflict-free 16-B stores)
+  static_assert(BM * EPI_LD * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit in the pipeline smem");
 };
 
 __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int bid, int& job, int& tile) {
@@ -207,7 +217,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int tiles_n = p.tiles_n[jid];
   const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
 
-  // problem geometry for this job
   int M, N, nstages;
   if constexpr (IS_DW) {
     M = p.job[jid].m;
@@ -222,13 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 128);  // every producer thread arrives after its own proxy fence
-      mbar_init(&empty[s], 1);  // tcgen05.commit
+      mbar_init(&full[s], kProducers);  // every producer thread arrives after its own proxy fence
+      mbar_init(&empty[s], 1);          // tcgen05.commit
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -238,44 +247,43 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
+  if (warp < 8) {
     // ---------------- producers ----------------
+    TileLoad<BM, IS_DW> la;
+    TileLoad<BN, IS_DW> lb;
     int seg = 0, k0 = 0;
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
-      mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-      uint8_t* base = smem + s * C::STAGE_BYTES;
-      float* a_hi = reinterpret_cast<float*>(base);
-      float* a_lo = reinterpret_cast<float*>(base + C::A_BYTES);
-      float* b_hi = reinterpret_cast<float*>(base + 2 * C::A_BYTES);
-      float* b_lo = reinterpret_cast<float*>(base + 2 * C::A_BYTES + C::B_BYTES);
+      // issue this stage's global loads before waiting for the slot to drain
       if constexpr (IS_DW) {
         const auto& jb = p.job[jid];
-        const bool va = (jb.m % 4 == 0) && (reinterpret_cast<uintptr_t>(jb.e) % 16 == 0);
-        const bool vb = (jb.n % 4 == 0) && (reinterpret_cast<uintptr_t>(jb.y) % 16 == 0);
-        produce<BM, true>(Src{jb.e, jb.m, M, p.k, va}, m0, k0, a_hi, a_lo, threadIdx.x);
-        produce<BN, true>(Src{jb.y, jb.n, N, p.k, vb}, n0, k0, b_hi, b_lo, threadIdx.x);
+        la.load(Src{jb.e, jb.m, M, p.k, false}, m0, k0, threadIdx.x);
+        lb.load(Src{jb.y, jb.n, N, p.k, false}, n0, k0, threadIdx.x);
         k0 += BK;
       } else {
         const Seg& sg = p.job[jid].seg[seg];
         const bool va = (sg.k % 4 == 0) && (reinterpret_cast<uintptr_t>(sg.a) % 16 == 0);
         const bool vb = (sg.k % 4 == 0) && (reinterpret_cast<uintptr_t>(sg.b) % 16 == 0);
-        produce<BM, false>(Src{sg.a, sg.k, M, sg.k, va}, m0, k0, a_hi, a_lo, threadIdx.x);
-        produce<BN, false>(Src{sg.b, sg.k, N, sg.k, vb}, n0, k0, b_hi, b_lo, threadIdx.x);
+        la.load(Src{sg.a, sg.k, M, sg.k, va}, m0, k0, threadIdx.x);
+        lb.load(Src{sg.b, sg.k, N, sg.k, vb}, n0, k0, threadIdx.x);
         k0 += BK;
         if (k0 >= sg.k) {
           k0 = 0;
           ++seg;
         }
       }
+      mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+      uint8_t* base = smem + s * C::STAGE_BYTES;
+      la.store(reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + C::A_BYTES), threadIdx.x);
+      lb.store(reinterpret_cast<float*>(base + 2 * C::A_BYTES),
+               reinterpret_cast<float*>(base + 2 * C::A_BYTES + C::B_BYTES), threadIdx.x);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&full[s]);
     }
-  } else if (warp == 4 && lane == 0) {
-    // ---------------- MMA issuer ----------------
+  } else if (lane == 0) {
+    // ---------------- MMA issuer (warp 8) ----------------
     const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
-    // both operands are K-major in smem (the dW producer transposes while loading)
-    const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);
+    const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);  // both operands K-major in smem
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
       mbar_wait(&full[s], (it / C::STAGES) & 1);
@@ -300,36 +308,46 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     mma_commit(done);
   }
 
-  // ---------------- epilogue (all 8 warps) ----------------
-  mbar_wait(done, 0);
-  __syncwarp();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int quarter = warp & 3, half = warp >> 2;
-  const int row = m0 + quarter * 32 + lane;
-  for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
-    if (n0 + cc >= N) break;  // warp-uniform
-    float v[16];
-    tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
-    if (row >= M) continue;
-    if constexpr (IS_DW) {
-      const auto& jb = p.job[jid];
-      float* g = jb.g + (int64_t)row * N + n0 + cc;
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (n0 + cc + j < N) g[j] = p.alpha * v[j];
-    } else {
-      const auto& epi = p.job[jid].epi;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + cc + j;
-        if (col >= N) break;
-        for (int k = 0; k < epi.nops; ++k) ew_apply(epi.op[k], N, row, col, p.ring, k == 0, v[j]);
+  // ---------------- epilogue (warps 0-7) ----------------
+  if (warp < 8) {
+    mbar_wait(done, 0);
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // 1) TMEM -> padded smem tile (all MMAs are complete: the pipeline smem is free)
+    float* tile_s = reinterpret_cast<float*>(smem);
+    const int quarter = warp & 3, half = warp >> 2;
+    const int r_loc = quarter * 32 + lane;
+    for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
+      if (n0 + cc >= N) break;  // warp-uniform
+      float v[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+      float4* dst = reinterpret_cast<float4*>(tile_s + r_loc * C::EPI_LD + cc);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+      dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+      dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // 2) rows across warps, columns across lanes: coalesced operand traffic
+    const int ncols = (N - n0) < BN ? (N - n0) : BN;
+    const int nrows = (M - m0) < BM ? (M - m0) : BM;
+#pragma unroll 1
+    for (int r = warp; r < nrows; r += 8) {
+#pragma unroll 1
+      for (int c = lane; c < ncols; c += 32) {
+        const float acc = tile_s[r * C::EPI_LD + c];
+        if constexpr (IS_DW) {
+          p.job[jid].g[(int64_t)(m0 + r) * N + n0 + c] = p.alpha * acc;
+        } else {
+          const auto& epi = p.job[jid].epi;
+          for (int k = 0; k < epi.nops; ++k) ew_apply(epi.op[k], N, m0 + r, n0 + c, p.ring, k == 0, acc);
+        }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
   }
 }

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <vector>
+#include <cstring>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, int layout) {
@@ -107,7 +108,32 @@ __global__ void probe(const float* A, const float* B, float* C, int a_mn, int b_
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
 }
 
+// How does kind::tf32 consume the low 13 mantissa bits of an fp32 operand?
+// A = x (row 0), B = identity-like column e0 -> C[0][0] = tf32view(x).
+void rounding_probe() {
+  constexpr int M = 128, N = 64, K = 32;
+  std::vector<float> A(M * K, 0.f), B(N * K, 0.f), C(M * N);
+  const float xs[6] = {1.0f + 0x1p-12f, 1.0f + 3 * 0x1p-12f, 1.0f + 0x1p-11f, 1.0f + 0x1.8p-11f,
+                       1.0f + 5 * 0x1p-13f, -(1.0f + 3 * 0x1p-12f)};
+  for (int i = 0; i < 6; ++i) A[i * K + 0] = xs[i];
+  B[0 * K + 0] = 1.0f;
+  float *dA, *dB, *dC;
+  cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dC, C.size() * 4);
+  cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  probe<M, N, K><<<1, 256>>>(dA, dB, dC, 0, 0, 0);
+  cudaDeviceSynchronize();
+  cudaMemcpy(C.data(), dC, C.size() * 4, cudaMemcpyDeviceToHost);
+  for (int i = 0; i < 6; ++i) {
+    float x = xs[i];
+    uint32_t u; memcpy(&u, &x, 4);
+    uint32_t t = u & 0xFFFFE000u; float tr; memcpy(&tr, &t, 4);
+    printf("x=%.10f  mma=%.10f  trunc=%.10f  %s\n", x, C[i * N + 0], tr, C[i * N] == tr ? "TRUNCATES" : "rounds");
+  }
+}
+
 int main() {
+  rounding_probe();
   constexpr int M = 128, N = 64, K = 32;
   std::vector<float> A(M * K), B(N * K), C(M * N), R(M * N);
   srand(1);
