@@ -13,11 +13,14 @@
  *    buffers and scratch live in ONE caller-allocated device workspace whose
  *    size rgb_plan_workspace_bytes() reports and whose internal layout is
  *    fixed by the schedule program (emitted by paper_1503_02852_b200/schedule.py).
- *  - Weights: one flat fp32 buffer W holding every dense connection's
- *    (dst_size x src_size) row-major matrix at the offset the program's weight
- *    table gives, a same-layout buffer WT holding the transposes (the
- *    reference keeps the same cache, engine.py:111-139), and a same-layout
- *    gradient buffer G.
+ *  - Weights: one flat fp32 buffer W of 2*n_params floats: every dense
+ *    connection's (dst_size x src_size) row-major matrix at the offset the
+ *    program's weight table gives, followed (at +n_params) by its tf32
+ *    residual W - trunc_tf32(W) that the 3xTF32 tensor-core GEMMs consume; a
+ *    same-layout buffer WT holding the transposes (the reference keeps the
+ *    same cache, engine.py:111-139) and their residuals; and a gradient
+ *    buffer G of n_params floats.  rgb_sgd_update / rgb_refresh_transpose
+ *    maintain the residual halves.
  *  - Work is enqueued on `stream` (a cudaStream_t); nothing synchronises
  *    except rgb_read_loss().
  *  - Every function returns RGB_OK (0) or an error code; rgb_last_error()

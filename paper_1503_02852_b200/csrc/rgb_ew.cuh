@@ -69,4 +69,96 @@ __device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, i
   }
 }
 
+// The same op over U independent elements at once.  Every operand stream is
+// gathered for all U elements before anything is stored, so one op costs one
+// memory latency per operand instead of one per element -- the GEMM epilogues
+// run on a single CTA per SM and cannot hide latency with more warps.
+template <int U>
+__device__ __forceinline__ void ew_apply_batch(const EwOp& op, int width, const int64_t (&r)[U], const int (&j)[U],
+                                               const bool (&ok)[U], const RingWrite& ring, bool has_acc,
+                                               const float (&acc)[U]) {
+  int64_t e[U];
+  float v[U], t[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) e[u] = r[u] * width + j[u];
+  const int kind = op.kind;
+  if (kind == EW_CONST1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) ring_store(op.out, e[u], r[u], width, op.out_is_ring, ring, 1.0f);
+    return;
+  }
+  if (kind == EW_FWD_MUL) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ok[u] ? op.fac[0][e[u]] : 0.0f;
+    for (int i = 1; i < op.nfac; ++i) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u] = ok[u] ? op.fac[i][e[u]] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] *= t[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) ring_store(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = has_acc ? acc[u] : ((op.base && ok[u]) ? op.base[e[u]] : 0.0f);
+  for (int i = 0; i < op.nterm; ++i) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) t[u] = ok[u] ? op.term[i][e[u]] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] += t[u];
+  }
+  if (kind == EW_FWD_ADD) {
+    for (int i = 0; i < op.nrank1; ++i) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u] = ok[u] ? op.r1w[i][j[u]] * op.r1src[i][r[u]] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] += t[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) ring_store(op.out, e[u], r[u], width, op.out_is_ring, ring, act_apply(op.act, v[u]));
+    return;
+  }
+  // EW_BWD
+  if (op.act == ACT_SIGMOID || op.act == ACT_TANH) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) t[u] = ok[u] ? op.y[e[u]] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] *= act_deriv(op.act, t[u]);
+  }
+  if (op.inj) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      t[u] = (ok[u] && r[u] >= op.inj_row0) ? op.inj[(r[u] - op.inj_row0) * width + j[u]] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] += t[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (ok[u]) op.out[e[u]] = v[u];
+  if (op.nfac == 0) return;
+  // eps_m = delta * prod_{other} z: gather every factor once, then form the products
+  float f[kMaxFac][U];  // fully unrolled: stays in registers
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) f[i][u] = (i < op.nfac && ok[u]) ? op.fac[i][e[u]] : 1.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+    if (i >= op.nfac || !op.eps[i]) continue;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float p = v[u];
+#pragma unroll
+      for (int k = 0; k < kMaxFac; ++k)
+        if (k != i) p *= f[k][u];
+      if (ok[u]) op.eps[i][e[u]] = p;
+    }
+  }
+}
+
 }  // namespace rgb

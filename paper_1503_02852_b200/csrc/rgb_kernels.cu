@@ -239,25 +239,37 @@ void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t
 // ---------------------------------------------------------------------------
 // W <- W - lr * G (engine.py:606-612)
 
-__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, int64_t n) {
+// tf32 residual consumed by the tcgen05 3xTF32 GEMMs (the tensor core truncates
+// its fp32 operands to tf32; see rgb_tc_gemm.cu)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// lr == 0: only recompute the residual half lo = W - trunc(W) (Weights refresh).
+__global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ lo, const float* __restrict__ g, float lr,
+                           int64_t n) {
   const int64_t n4 = n / 4;
   float4* w4 = reinterpret_cast<float4*>(w);
+  float4* l4 = reinterpret_cast<float4*>(lo);
   const float4* g4 = reinterpret_cast<const float4*>(g);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = w4[i];
-    const float4 b = g4[i];
-    a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
-    w4[i] = a;
+    if (g) {
+      const float4 b = g4[i];
+      a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+      w4[i] = a;
+    }
+    l4[i] = make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w));
   }
-  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    w[i] -= lr * g[i];
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (g) w[i] -= lr * g[i];
+    lo[i] = tf32_lo(w[i]);
+  }
 }
 
-void launch_sgd(float* w, const float* g, float lr, int64_t n, cudaStream_t s) {
+void launch_sgd(float* w, float* lo, const float* g, float lr, int64_t n, cudaStream_t s) {
   int64_t blocks = (n / 4 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  sgd_kernel<<<(int)blocks, 256, 0, s>>>(w, g, lr, n);
+  sgd_kernel<<<(int)blocks, 256, 0, s>>>(w, lo, g, lr, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -277,7 +289,11 @@ __global__ void transpose_kernel(const __grid_constant__ TransposeGroup p) {
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
     const int c = c0 + i, r = r0 + tx;
-    if (r < jb.rows && c < jb.cols) jb.dst[(int64_t)c * jb.rows + r] = t[tx][i];
+    if (r < jb.rows && c < jb.cols) {
+      const float v = t[tx][i];
+      jb.dst[(int64_t)c * jb.rows + r] = v;
+      if (jb.dst_lo) jb.dst_lo[(int64_t)c * jb.rows + r] = tf32_lo(v);
+    }
   }
 }
 

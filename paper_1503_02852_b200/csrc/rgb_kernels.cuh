@@ -16,6 +16,7 @@ namespace rgb {
 struct TransposeJob {
   const float* src;  // [rows x cols]
   float* dst;        // [cols x rows]
+  float* dst_lo;     // tf32 residual of dst (or null)
   int rows, cols;
 };
 constexpr int kMaxTr = 48;
@@ -39,7 +40,8 @@ void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring,
 void launch_inject_loss(const float* y, const void* target, int target_kind, int criterion, float* inj,
                         double* row_loss, int rows, int width, cudaStream_t s);
 void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t s);
-void launch_sgd(float* w, const float* g, float lr, int64_t n, cudaStream_t s);
+// W -= lr * G over n floats and lo = W - trunc_tf32(W); g == nullptr: residual only.
+void launch_sgd(float* w, float* lo, const float* g, float lr, int64_t n, cudaStream_t s);
 void launch_transpose(const TransposeGroup& p, cudaStream_t s);
 void launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s);

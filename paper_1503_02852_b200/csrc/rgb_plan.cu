@@ -9,6 +9,7 @@
 // replaces the Python-dispatched loops of forward_chunk / backward_window
 // (/root/reference/pkg/src/rnngraph/engine.py:405-413, 568-599).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdarg>
 #include <cstdio>
@@ -86,6 +87,35 @@ constexpr double kTcMinFlops = 32.0 * 1024 * 1024;
 
 bool use_tc(double flops) { return g_gemm_mode == 2 || (g_gemm_mode == 0 && flops >= kTcMinFlops); }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Row-major fp32 [rows x width] matrix, boxes of {32 fp32, box_rows} with the
+// 128-byte swizzle the UMMA K-major descriptors expect; out-of-range boxes fill 0.
+bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc || width % 4 || reinterpret_cast<uintptr_t>(base) % 16 || rows == 0) return false;
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {width * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 struct rgb_plan {
@@ -97,6 +127,64 @@ struct rgb_plan {
   std::vector<int32_t> prog[4];  // fwd, bwd, fwd_seq, bwd_seq
   float* ws = nullptr;
   int64_t cursor = 0;
+
+  // TMA tensor maps (device copy + host mirror): one per workspace buffer
+  // (box 128 rows, the GEMM A operand) at [0, nbufs), then four per dense
+  // connection (W, W_lo, W^T, W^T_lo; box 32 rows) at nbufs + 4 * cid.
+  std::vector<CUtensorMap> maps;
+  std::vector<char> map_ok;
+  CUtensorMap* maps_dev = nullptr;
+  const float* map_w = nullptr;
+  const float* map_wt = nullptr;
+
+  ~rgb_plan() {
+    if (maps_dev) cudaFree(maps_dev);
+  }
+
+  int frames_of(int kind) const { return kind == BUF_RING ? 2 * cap : (kind == BUF_WIN ? hmax + maxd : hmax); }
+
+  int build_buffer_maps() {
+    const size_t nb = bufs.size(), total = nb + 4 * wts.size();
+    maps.assign(total, CUtensorMap{});
+    map_ok.assign(total, 0);
+    for (size_t i = 0; i < nb; ++i)
+      map_ok[i] = encode_map(&maps[i], ws + bufs[i].off, (uint64_t)frames_of(bufs[i].kind) * S, bufs[i].width, 128);
+    if (!maps_dev && cudaMalloc(&maps_dev, total * sizeof(CUtensorMap)) != cudaSuccess)
+      return fail(RGB_ERR_CUDA, "tensor-map table allocation failed");
+    map_w = map_wt = nullptr;
+    if (cudaMemcpy(maps_dev, maps.data(), total * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(RGB_ERR_CUDA, "tensor-map upload failed");
+    return RGB_OK;
+  }
+
+  // (Re)build the weight maps when the caller's W / W^T buffers change.  The
+  // buffers hold [W | W_lo] and [W^T | W^T_lo] (n_params floats each half).
+  int ensure_weight_maps(const float* w, const float* wt) {
+    const bool new_w = w && w != map_w, new_wt = wt && wt != map_wt;
+    if (!maps_dev || (!new_w && !new_wt)) return RGB_OK;
+    const size_t nb = bufs.size();
+    for (size_t cid = 0; cid < wts.size(); ++cid) {
+      const WDesc& d = wts[cid];
+      char* ok = &map_ok[nb + 4 * cid];
+      CUtensorMap* m = &maps[nb + 4 * cid];
+      if (d.rows == 0) continue;
+      if (new_w) {
+        ok[0] = encode_map(&m[0], w + d.off, d.rows, d.cols, 32);
+        ok[1] = encode_map(&m[1], w + n_params + d.off, d.rows, d.cols, 32);
+      }
+      if (new_wt) {
+        ok[2] = encode_map(&m[2], wt + d.off, d.cols, d.rows, 32);
+        ok[3] = encode_map(&m[3], wt + n_params + d.off, d.cols, d.rows, 32);
+      }
+    }
+    // synchronous: the host mirror may be rewritten on the next change
+    if (cudaMemcpy(maps_dev + nb, maps.data() + nb, 4 * wts.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return fail(RGB_ERR_CUDA, "weight tensor-map upload failed");
+    if (new_w) map_w = w;
+    if (new_wt) map_wt = wt;
+    return RGB_OK;
+  }
 
   // scratch layout inside the workspace (float offsets)
   int64_t tgt_off() const { return scratch_off; }
@@ -240,7 +328,7 @@ struct rgb_plan {
     return RGB_OK;
   }
 
-  int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) const {
+  int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) {
     Reader rd{p, n};
     while (rd.i < n) {
       const int kind = rd.next();
@@ -268,6 +356,8 @@ struct rgb_plan {
         G.rows = c.frames * S;
         G.ring = ring_for(c);
         G.tile_start[0] = 0;
+        if ((rc = ensure_weight_maps(c.w, c.wt))) return rc;
+        bool all_tma = !maps.empty();
         for (int j = 0; j < G.njobs; ++j) {
           GemmJob& jb = G.job[j];
           jb.nseg = rd.next();
@@ -283,6 +373,15 @@ struct rgb_plan {
             jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
             jb.seg[s].k = trans ? wd.rows : wd.cols;
             if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
+            const int mi = (int)bufs.size() + 4 * cid + (trans ? 2 : 0);
+            if (all_tma && map_ok[ab] && map_ok[mi] && map_ok[mi + 1]) {
+              jb.seg[s].ta = maps_dev + ab;
+              jb.seg[s].tb = maps_dev + mi;
+              jb.seg[s].tblo = maps_dev + mi + 1;
+              jb.seg[s].arow = (int)((a - (ws + bufs[ab].off)) / bufs[ab].width);
+            } else {
+              all_tma = false;
+            }
           }
           if ((rc = parse_chain(rd, c, true, jb.epi))) return rc;
           jb.n = jb.epi.width;
@@ -290,6 +389,7 @@ struct rgb_plan {
           G.tiles_n[j] = tn;
           G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
         }
+        G.tma = all_tma ? 1 : 0;
         double flops = 0, bytes = 0;
         for (int j = 0; j < G.njobs; ++j) {
           int64_t ksum = 0;
@@ -383,6 +483,8 @@ int cuda_rc(cudaError_t e, const char* what) {
 
 }  // namespace
 
+static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* stream);
+
 extern "C" {
 
 int rgb_abi_version(void) { return RGB_ABI_VERSION; }
@@ -401,7 +503,7 @@ int rgb_gemm_nt(const float* a, const float* b, float* c, int m, int n, int k, i
   G.rows = m;
   GemmJob& jb = G.job[0];
   jb.nseg = 1;
-  jb.seg[0] = Seg{a, b, k, 0};
+  jb.seg[0] = Seg{a, b, nullptr, nullptr, nullptr, 0, k};
   jb.n = n;
   jb.epi.width = n;
   jb.epi.nops = 1;
@@ -496,6 +598,7 @@ int rgb_plan_bind(rgb_plan* p, void* ws) {
   if (!p || !ws) return fail(RGB_ERR_KERNEL, "null argument");
   if (reinterpret_cast<uintptr_t>(ws) % 16) return fail(RGB_ERR_KERNEL, "workspace must be 16-byte aligned");
   p->ws = static_cast<float*>(ws);
+  return p->build_buffer_maps();
   return RGB_OK;
 }
 
@@ -616,16 +719,28 @@ int rgb_sgd_update(rgb_plan* p, float* w, float* wt, const float* g, float lr, v
   if (!(lr > 0.0f)) return fail(RGB_ERR_ENGINE, "learning rate must be positive, got %g", (double)lr);
   cudaStream_t st = as_stream(stream);
   const int slot = prof_start(st);
-  launch_sgd(w, g, lr, p->n_params, st);
+  launch_sgd(w, w + p->n_params, g, lr, p->n_params, st);
   note_launch();
-  prof_stop(slot, st, PROF_SGD, 2.0 * p->n_params, 12.0 * p->n_params);
+  prof_stop(slot, st, PROF_SGD, 2.0 * p->n_params, 16.0 * p->n_params);
   int rc = cuda_rc(cudaGetLastError(), "sgd launch");
   if (rc) return rc;
-  return rgb_refresh_transpose(p, w, wt, stream);
+  return transpose_weights(p, w, wt, stream);
 }
 
 int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) {
   if (!p || !w || !wt) return fail(RGB_ERR_KERNEL, "null argument");
+  launch_sgd(const_cast<float*>(w), const_cast<float*>(w) + p->n_params, nullptr, 0.0f, p->n_params,
+             as_stream(stream));
+  note_launch();
+  int rc = cuda_rc(cudaGetLastError(), "residual launch");
+  if (rc) return rc;
+  return transpose_weights(p, w, wt, stream);
+}
+
+}  // extern "C"
+
+// W^T and its tf32 residual for every dense connection (grouped launches).
+static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* stream) {
   TransposeGroup T;
   std::memset(&T, 0, sizeof T);
   for (size_t cid = 0; cid < p->wts.size(); ++cid) {
@@ -637,7 +752,7 @@ int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) 
       std::memset(&T, 0, sizeof T);
     }
     const int j = T.njobs++;
-    T.job[j] = TransposeJob{w + d.off, wt + d.off, d.rows, d.cols};
+    T.job[j] = TransposeJob{w + d.off, wt + d.off, wt + p->n_params + d.off, d.rows, d.cols};
     T.tiles_c[j] = (d.cols + 31) / 32;
     T.tile_start[j + 1] = T.tile_start[j] + ((d.rows + 31) / 32) * T.tiles_c[j];
   }
@@ -651,6 +766,8 @@ int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) 
   }
   return cuda_rc(cudaGetLastError(), "transpose launch");
 }
+
+extern "C" {
 
 int rgb_reset_stream(rgb_plan* p, int s, void* stream) {
   if (!p || !p->ws) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");

@@ -112,6 +112,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// 2-D tiled TMA load (box {32 fp32 along the row, R rows}, SWIZZLE_128B) into
+// smem, completing `bytes` on the mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// tf32 residual of an fp32 value: kind::tf32 consumes only the top 19 bits
+// (it truncates -- measured, tools/tc_probe.cu), so x itself acts as "hi" and
+// lo = x - trunc13(x) is exact in fp32.
+__device__ __forceinline__ float tf32_residual(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
 // One operand tile source: `rows` is the valid extent along M (or N), `kv` the
 // valid extent along K, ld the global leading dimension (elements).
 struct Src {
@@ -183,7 +204,7 @@ struct TileLoad {
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 2 : (BN == 128 ? 3 : 4);
+  static constexpr int STAGES = BN == 256 ? 2 : (BN == 128 ? 3 : (BN == 64 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
@@ -196,6 +217,60 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
   job = 0;
   while (job + 1 < njobs && bid >= tile_start[job + 1]) ++job;
   tile = bid - tile_start[job];
+}
+
+// Epilogue, run by 256 threads after the accumulator is complete:
+// (1) tcgen05.ld the TMEM tile into a padded smem tile (warp w reads lane
+//     quarter w%4, column half w/4);
+// (2) walk the tile with consecutive threads on consecutive columns and apply
+//     the job's elementwise chain (or the dW store) to U elements per thread
+//     at a time, gathering every operand of an op for all U before storing.
+template <int BN, bool IS_DW, class P>
+__device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, int M, int N, uint32_t tmem,
+                                         float* tile_s, int tid) {
+  using C = Cfg<BN>;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int r_loc = quarter * 32 + lane;
+  for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
+    if (n0 + cc >= N) break;  // warp-uniform
+    float v[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+    float4* dst = reinterpret_cast<float4*>(tile_s + r_loc * C::EPI_LD + cc);
+    dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+    dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+    dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+    dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  const int ncols = (N - n0) < BN ? (N - n0) : BN;
+  const int nrows = (M - m0) < BM ? (M - m0) : BM;
+  const int total = ncols * nrows;
+  constexpr int U = 8;
+#pragma unroll 1
+  for (int base = 0; base < total; base += 256 * U) {
+    int64_t rr[U];
+    int cc[U];
+    bool ok[U];
+    float acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + tid + 256 * u;
+      ok[u] = idx < total;
+      const int rl = ok[u] ? idx / ncols : 0, cl = ok[u] ? idx - (idx / ncols) * ncols : 0;
+      rr[u] = m0 + rl;
+      cc[u] = n0 + cl;
+      acc[u] = tile_s[rl * C::EPI_LD + cl];
+    }
+    if constexpr (IS_DW) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) p.job[jid].g[rr[u] * N + cc[u]] = p.alpha * acc[u];
+    } else {
+      const auto& epi = p.job[jid].epi;
+      for (int k = 0; k < epi.nops; ++k) ew_apply_batch<U>(epi.op[k], N, rr, cc, ok, p.ring, k == 0, acc);
+    }
+  }
 }
 
 // IS_DW = false: C[r, n] = sum_seg A_seg[r, :] . B_seg[n, :] (both K-major), EW-chain epilogue.
@@ -313,42 +388,144 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     mbar_wait(done, 0);
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // 1) TMEM -> padded smem tile (all MMAs are complete: the pipeline smem is free)
-    float* tile_s = reinterpret_cast<float*>(smem);
-    const int quarter = warp & 3, half = warp >> 2;
-    const int r_loc = quarter * 32 + lane;
-    for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
-      if (n0 + cc >= N) break;  // warp-uniform
-      float v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
-      float4* dst = reinterpret_cast<float4*>(tile_s + r_loc * C::EPI_LD + cc);
-      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-      dst[2] = make_float4(v[8], v[9], v[10], v[11]);
-      dst[3] = make_float4(v[12], v[13], v[14], v[15]);
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    // 2) rows across warps, columns across lanes: coalesced operand traffic
-    const int ncols = (N - n0) < BN ? (N - n0) : BN;
-    const int nrows = (M - m0) < BM ? (M - m0) : BM;
-#pragma unroll 1
-    for (int r = warp; r < nrows; r += 8) {
-#pragma unroll 1
-      for (int c = lane; c < ncols; c += 32) {
-        const float acc = tile_s[r * C::EPI_LD + c];
-        if constexpr (IS_DW) {
-          p.job[jid].g[(int64_t)(m0 + r) * N + n0 + c] = p.alpha * acc;
-        } else {
-          const auto& epi = p.job[jid].epi;
-          for (int k = 0; k < epi.nops; ++k) ew_apply(epi.op[k], N, m0 + r, n0 + c, p.ring, k == 0, acc);
-        }
-      }
-    }
+    // all MMAs are complete: the pipeline smem is free for the staging tile
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 8) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed NT GEMM.  Per stage, one thread (warp 8) issues the TMA loads of the
+// raw fp32 A tile (activations; the tensor core truncates it to its tf32 "hi"
+// part) and of the pre-split weight tiles B = W and B_lo = W - trunc(W) (kept
+// by the SGD / W^T-refresh kernels), all with SWIZZLE_128B straight into the
+// UMMA K-major layout; the 8 converter warps only form A_lo = A - trunc(A) in
+// place-aligned smem (same byte offsets, no swizzle arithmetic); one thread of
+// warp 9 issues the three tcgen05.mma per 8-deep k-step.  Three mbarriers per
+// stage: TMA landed -> residual written -> MMAs done (tcgen05.commit).
+constexpr int kTmaThreads = 320;  // warps 0-7 convert + epilogue, 8 TMA, 9 MMA
+constexpr int kBoxB = 32;         // weight maps are cut in 32-row boxes (BN / 32 loads per operand)
+
+template <int BN>
+__global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ GemmGroup p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* conv_full = tma_full + C::STAGES;
+  uint64_t* empty = conv_full + C::STAGES;
+  uint64_t* done = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int jid, tile;
+  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  const GemmJob& job = p.job[jid];
+  const int tiles_n = p.tiles_n[jid];
+  const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+  const int M = p.rows, N = job.n;
+  int nstages = 0;
+  for (int s = 0; s < job.nseg; ++s) nstages += (job.seg[s].k + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&tma_full[s], 1);
+      mbar_init(&conv_full[s], kProducers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int seg = 0, k0 = 0;
+      for (int it = 0; it < nstages; ++it) {
+        const int s = it % C::STAGES;
+        mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+        uint8_t* base = smem + s * C::STAGE_BYTES;
+        const Seg& sg = job.seg[seg];
+        mbar_expect_tx(&tma_full[s], C::A_BYTES + 2 * C::B_BYTES);
+        tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
+#pragma unroll
+        for (int b = 0; b < BN / kBoxB; ++b) {
+          tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * 128, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
+          tma_load_2d(base + 2 * C::A_BYTES + C::B_BYTES + b * kBoxB * 128, sg.tblo, k0, n0 + b * kBoxB,
+                      &tma_full[s]);
+        }
+        k0 += BK;
+        if (k0 >= sg.k) {
+          k0 = 0;
+          ++seg;
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
+      const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);
+      for (int it = 0; it < nstages; ++it) {
+        const int s = it % C::STAGES;
+        mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+        const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
+        const uint32_t b_hi = base + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint32_t off = j * 32;
+          const uint64_t dah = smem_desc(a_hi + off, 16, 1024), dal = smem_desc(a_lo + off, 16, 1024);
+          const uint64_t dbh = smem_desc(b_hi + off, 16, 1024), dbl = smem_desc(b_lo + off, 16, 1024);
+          const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+          mma_tf32(tmem, dal, dbh, idesc, acc0);
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+          mma_tf32(tmem, dah, dbh, idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+  } else {
+    // ---------------- converters: A_lo = A - trunc(A) ----------------
+    for (int it = 0; it < nstages; ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait(&tma_full[s], (it / C::STAGES) & 1);
+      const float4* a_hi = reinterpret_cast<const float4*>(smem + s * C::STAGE_BYTES);
+      float4* a_lo = reinterpret_cast<float4*>(smem + s * C::STAGE_BYTES + C::A_BYTES);
+#pragma unroll
+      for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
+        const int q = threadIdx.x + i * kProducers;
+        const float4 x = a_hi[q];
+        a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&conv_full[s]);
+    }
+    // ---------------- epilogue ----------------
+    mbar_wait(done, 0);
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    epilogue<BN, false>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 9) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
   }
 }
 
@@ -363,12 +540,23 @@ void launch_one(P p, int tiles, cudaStream_t s) {
   k<<<tiles, kThreads, Cfg<BN>::SMEM, s>>>(p);
 }
 
-// Widest N tile that still gives most SMs a tile.
+template <int BN>
+void launch_tma(const GemmGroup& p, int tiles, cudaStream_t s) {
+  static bool configured = false;
+  auto k = tma_gemm_kernel<BN>;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+    configured = true;
+  }
+  k<<<tiles, kTmaThreads, Cfg<BN>::SMEM, s>>>(p);
+}
+
+// Widest N tile that still gives most of the 148 SMs a tile.
 template <class F>
 int pick_bn(F tiles_for) {
-  if (tiles_for(256) >= 120) return 256;
-  if (tiles_for(128) >= 120) return 128;
-  return 64;
+  for (int bn : {256, 128, 64})
+    if (tiles_for(bn) >= 120) return bn;
+  return 32;
 }
 
 }  // namespace tc
@@ -387,9 +575,17 @@ void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   }
   const int tiles = p.tile_start[p.njobs];
   if (tiles == 0) return;
-  if (bn == 256) tc::launch_one<256, false>(p, tiles, s);
-  else if (bn == 128) tc::launch_one<128, false>(p, tiles, s);
-  else tc::launch_one<64, false>(p, tiles, s);
+  if (p.tma) {
+    if (bn == 256) tc::launch_tma<256>(p, tiles, s);
+    else if (bn == 128) tc::launch_tma<128>(p, tiles, s);
+    else if (bn == 64) tc::launch_tma<64>(p, tiles, s);
+    else tc::launch_tma<32>(p, tiles, s);
+  } else {
+    if (bn == 256) tc::launch_one<256, false>(p, tiles, s);
+    else if (bn == 128) tc::launch_one<128, false>(p, tiles, s);
+    else if (bn == 64) tc::launch_one<64, false>(p, tiles, s);
+    else tc::launch_one<32, false>(p, tiles, s);
+  }
 }
 
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
@@ -408,7 +604,8 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   if (tiles == 0) return;
   if (bn == 256) tc::launch_one<256, true>(p, tiles, s);
   else if (bn == 128) tc::launch_one<128, true>(p, tiles, s);
-  else tc::launch_one<64, true>(p, tiles, s);
+  else if (bn == 64) tc::launch_one<64, true>(p, tiles, s);
+  else tc::launch_one<32, true>(p, tiles, s);
 }
 
 }  // namespace rgb

@@ -62,7 +62,11 @@ struct RingWrite {
 struct Seg {
   const float* a;      // [rows x K] row-major (K-major A)
   const float* b;      // [N x K] row-major (K-major B): W (forward) or W^T (backward)
-  int k, pad;
+  const void* ta;      // TMA tensor map of A's whole buffer (device memory), or null
+  const void* tb;      // TMA tensor maps of B and of its tf32 residual B_lo
+  const void* tblo;
+  int arow;            // row of `a` inside A's buffer (TMA coordinate)
+  int k;
 };
 
 struct GemmJob {
@@ -73,6 +77,7 @@ struct GemmJob {
 
 struct GemmGroup {
   int njobs, rows;
+  int tma, pad;                  // 1: every segment has TMA maps (TMA-fed tcgen05 kernel)
   int tile_start[kMaxJobs + 1];  // prefix sum of tiles per job
   int tiles_n[kMaxJobs];         // tiles along N per job
   RingWrite ring;

@@ -172,7 +172,10 @@ class Weights:
         self.net = net
         self.offsets, self.n_params = weight_offsets(net)
         dev = _device()
-        self.flat = _flat if _flat is not None else torch.zeros(max(self.n_params, 4), dtype=DTYPE, device=dev)
+        # [W | W_lo] and [W^T | W^T_lo]: the second halves hold the tf32 residuals
+        # the tensor-core GEMMs consume (refreshed by every update)
+        n2 = 2 * max(self.n_params, 4)
+        self.flat = _flat if _flat is not None else torch.zeros(n2, dtype=DTYPE, device=dev)
         self.flat_t = _flat_t if _flat_t is not None else torch.zeros_like(self.flat)
         self._plan = _Plan(weights_program(net))
         self.w, self.wt = {}, {}
