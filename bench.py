@@ -354,7 +354,9 @@ def run_ours(args, cfg):
                    "schedule": "hoisted (paper §3.1)"},
         "algorithmic_tflops": F_iter / (ms / 1000.0) / 1e12,
         "roofline": roof,
-        "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps}
+        "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                        "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
+                        "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
                     for k, v in prof.items()},
         "e2e": e2e,
         "clocks": clocks.summary(),

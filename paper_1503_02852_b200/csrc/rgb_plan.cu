@@ -104,7 +104,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // Row-major fp32 [rows x width] matrix, boxes of {32 fp32, box_rows} with the
 // 128-byte swizzle the UMMA K-major descriptors expect; out-of-range boxes fill 0.
-bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t box_rows) {
+// mn_major = true: the same boxes with the 32-byte-atom 128B swizzle that the
+// UMMA SWIZZLE_128B_BASE32B MN-major layout (kind::tf32) expects -- the dW
+// operands, whose contiguous dimension is M or N (tools/tc_probe_mn.cu).
+bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t box_rows,
+                bool mn_major = false) {
   auto enc = tensor_map_encoder();
   if (!enc || width % 4 || reinterpret_cast<uintptr_t>(base) % 16 || rows == 0) return false;
   cuuint64_t dims[2] = {width, rows};
@@ -112,8 +116,8 @@ bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width
   cuuint32_t box[2] = {32, box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -128,9 +132,10 @@ struct rgb_plan {
   float* ws = nullptr;
   int64_t cursor = 0;
 
-  // TMA tensor maps (device copy + host mirror): one per workspace buffer
-  // (box 128 rows, the GEMM A operand) at [0, nbufs), then four per dense
-  // connection (W, W_lo, W^T, W^T_lo; box 32 rows) at nbufs + 4 * cid.
+  // TMA tensor maps (device copy + host mirror): per workspace buffer one
+  // K-major map (box 32 x 128 rows, NT GEMM A operand) at [0, nb) and one
+  // MN-major map (box 32 x 32 rows, dW operand) at [nb, 2nb); then four per
+  // dense connection (W, W_lo, W^T, W^T_lo; box 32 rows) at 2nb + 4 * cid.
   std::vector<CUtensorMap> maps;
   std::vector<char> map_ok;
   CUtensorMap* maps_dev = nullptr;
@@ -143,12 +148,17 @@ struct rgb_plan {
 
   int frames_of(int kind) const { return kind == BUF_RING ? 2 * cap : (kind == BUF_WIN ? hmax + maxd : hmax); }
 
+  size_t wmap0() const { return 2 * bufs.size(); }
+
   int build_buffer_maps() {
-    const size_t nb = bufs.size(), total = nb + 4 * wts.size();
+    const size_t nb = bufs.size(), total = wmap0() + 4 * wts.size();
     maps.assign(total, CUtensorMap{});
     map_ok.assign(total, 0);
-    for (size_t i = 0; i < nb; ++i)
-      map_ok[i] = encode_map(&maps[i], ws + bufs[i].off, (uint64_t)frames_of(bufs[i].kind) * S, bufs[i].width, 128);
+    for (size_t i = 0; i < nb; ++i) {
+      const uint64_t rows = (uint64_t)frames_of(bufs[i].kind) * S;
+      map_ok[i] = encode_map(&maps[i], ws + bufs[i].off, rows, bufs[i].width, 128);
+      map_ok[nb + i] = encode_map(&maps[nb + i], ws + bufs[i].off, rows, bufs[i].width, 32, true);
+    }
     if (!maps_dev && cudaMalloc(&maps_dev, total * sizeof(CUtensorMap)) != cudaSuccess)
       return fail(RGB_ERR_CUDA, "tensor-map table allocation failed");
     map_w = map_wt = nullptr;
@@ -162,7 +172,7 @@ struct rgb_plan {
   int ensure_weight_maps(const float* w, const float* wt) {
     const bool new_w = w && w != map_w, new_wt = wt && wt != map_wt;
     if (!maps_dev || (!new_w && !new_wt)) return RGB_OK;
-    const size_t nb = bufs.size();
+    const size_t nb = wmap0();
     for (size_t cid = 0; cid < wts.size(); ++cid) {
       const WDesc& d = wts[cid];
       char* ok = &map_ok[nb + 4 * cid];
@@ -373,7 +383,7 @@ struct rgb_plan {
             jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
             jb.seg[s].k = trans ? wd.rows : wd.cols;
             if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
-            const int mi = (int)bufs.size() + 4 * cid + (trans ? 2 : 0);
+            const int mi = (int)wmap0() + 4 * cid + (trans ? 2 : 0);
             if (all_tma && map_ok[ab] && map_ok[mi] && map_ok[mi + 1]) {
               jb.seg[s].ta = maps_dev + ab;
               jb.seg[s].tb = maps_dev + mi;
@@ -437,20 +447,56 @@ struct rgb_plan {
           const WDesc& wd = wts[cid];
           if (bufs[eb].width != wd.rows || bufs[yb].width != wd.cols)
             return fail(RGB_ERR_KERNEL, "dW shape mismatch (cid %d)", cid);
-          D.job[j] = DwJob{e, y, c.g + wd.off, wd.rows, wd.cols};
-          const int tm = (wd.rows + 63) / 64, tn = (wd.cols + 63) / 64;
-          D.tiles_n[j] = tn;
-          D.tile_start[j + 1] = D.tile_start[j] + tm * tn;
+          D.job[j] = DwJob{e, y, c.g + wd.off, wd.rows, wd.cols, nullptr, nullptr, 0, 0};
+          const size_t nb = bufs.size();
+          if (!maps.empty() && map_ok[nb + eb] && map_ok[nb + yb]) {
+            D.job[j].te = maps_dev + nb + eb;
+            D.job[j].ty = maps_dev + nb + yb;
+            D.job[j].erow = (int)((e - (ws + bufs[eb].off)) / bufs[eb].width);
+            D.job[j].yrow = (int)((y - (ws + bufs[yb].off)) / bufs[yb].width);
+          }
         }
         double flops = 0, bytes = 0;
         for (int j = 0; j < D.njobs; ++j) {
           flops += 2.0 * D.k * (double)D.job[j].m * D.job[j].n;
           bytes += 4.0 * ((double)D.k * (D.job[j].m + D.job[j].n) + (double)D.job[j].m * D.job[j].n);
         }
+        // jobs with TMA maps -> TMA-fed tcgen05 launch; the rest (e.g. width-1
+        // bias sources) -> one SIMT / register-fed launch
+        DwGroup T = D, R = D;
+        T.njobs = R.njobs = 0;
+        T.tma = 1;
+        R.tma = 0;
+        double rflops = 0;
+        for (int j = 0; j < D.njobs; ++j) {
+          const DwJob& jb = D.job[j];
+          const double f = 2.0 * D.k * (double)jb.m * jb.n;
+          if (jb.te && use_tc(flops)) {
+            T.job[T.njobs++] = jb;
+          } else {
+            R.job[R.njobs++] = jb;
+            rflops += f;
+          }
+        }
+        auto tiles64 = [](DwGroup& G) {
+          G.tile_start[0] = 0;
+          for (int j = 0; j < G.njobs; ++j) {
+            G.tiles_n[j] = (G.job[j].n + 63) / 64;
+            G.tile_start[j + 1] = G.tile_start[j] + ((G.job[j].m + 63) / 64) * G.tiles_n[j];
+          }
+        };
+        tiles64(T);
+        tiles64(R);
         const int slot = prof_start(st);
-        if (use_tc(flops)) launch_tc_gemm_dw(D, st);
-        else launch_gemm_dw(D, st);
-        note_launch();
+        if (T.njobs) {
+          launch_tc_gemm_dw(T, st);
+          note_launch();
+        }
+        if (R.njobs) {
+          if (use_tc(rflops)) launch_tc_gemm_dw(R, st);
+          else launch_gemm_dw(R, st);
+          note_launch();
+        }
         prof_stop(slot, st, PROF_DW, flops, bytes);
       } else {
         return fail(RGB_ERR_KERNEL, "unknown step %d", kind);
@@ -526,7 +572,7 @@ int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, f
   D.njobs = 1;
   D.k = k;
   D.alpha = alpha;
-  D.job[0] = DwJob{e, y, g, m, n};
+  D.job[0] = DwJob{e, y, g, m, n, nullptr, nullptr, 0, 0};
   D.tiles_n[0] = (n + 63) / 64;
   D.tile_start[1] = ((m + 63) / 64) * D.tiles_n[0];
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

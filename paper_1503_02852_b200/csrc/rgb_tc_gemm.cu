@@ -70,13 +70,15 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 // SM100 shared-memory matrix descriptor, SWIZZLE_128B, version 1.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout 2 = SWIZZLE_128B (K-major operands), 1 = SWIZZLE_128B_BASE32B (the
+// MN-major tf32 layout TMA's 128B_ATOM_32B swizzle produces).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
-  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
 }
 
@@ -410,8 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 constexpr int kTmaThreads = 320;  // warps 0-7 convert + epilogue, 8 TMA, 9 MMA
 constexpr int kBoxB = 32;         // weight maps are cut in 32-row boxes (BN / 32 loads per operand)
 
-template <int BN>
-__global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ GemmGroup p) {
+template <int BN, bool IS_DW, class P>
+__global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ P p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -424,12 +426,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int jid, tile;
   find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
-  const GemmJob& job = p.job[jid];
+  const auto& job = p.job[jid];
   const int tiles_n = p.tiles_n[jid];
   const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
-  const int M = p.rows, N = job.n;
-  int nstages = 0;
-  for (int s = 0; s < job.nseg; ++s) nstages += (job.seg[s].k + BK - 1) / BK;
+  int M, N, nstages;
+  if constexpr (IS_DW) {
+    M = job.m;
+    N = job.n;
+    nstages = (p.k + BK - 1) / BK;
+  } else {
+    M = p.rows;
+    N = job.n;
+    nstages = 0;
+    for (int s = 0; s < job.nseg; ++s) nstages += (job.seg[s].k + BK - 1) / BK;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -458,19 +468,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         const int s = it % C::STAGES;
         mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
         uint8_t* base = smem + s * C::STAGE_BYTES;
-        const Seg& sg = job.seg[seg];
-        mbar_expect_tx(&tma_full[s], C::A_BYTES + 2 * C::B_BYTES);
-        tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
+        if constexpr (IS_DW) {
+          // MN-contiguous E [K x M] and Y [K x N]: boxes {32 mn, 32 k}, 4 KB each
+          mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
 #pragma unroll
-        for (int b = 0; b < BN / kBoxB; ++b) {
-          tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * 128, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
-          tma_load_2d(base + 2 * C::A_BYTES + C::B_BYTES + b * kBoxB * 128, sg.tblo, k0, n0 + b * kBoxB,
-                      &tma_full[s]);
-        }
-        k0 += BK;
-        if (k0 >= sg.k) {
-          k0 = 0;
-          ++seg;
+          for (int b = 0; b < BM / 32; ++b)
+            tma_load_2d(base + b * 4096, job.te, m0 + 32 * b, job.erow + k0, &tma_full[s]);
+#pragma unroll
+          for (int b = 0; b < BN / 32; ++b)
+            tma_load_2d(base + 2 * C::A_BYTES + b * 4096, job.ty, n0 + 32 * b, job.yrow + k0, &tma_full[s]);
+          k0 += BK;
+        } else {
+          const Seg& sg = job.seg[seg];
+          mbar_expect_tx(&tma_full[s], C::A_BYTES + 2 * C::B_BYTES);
+          tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
+#pragma unroll
+          for (int b = 0; b < BN / kBoxB; ++b) {
+            tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * 128, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
+            tma_load_2d(base + 2 * C::A_BYTES + C::B_BYTES + b * kBoxB * 128, sg.tblo, k0, n0 + b * kBoxB,
+                        &tma_full[s]);
+          }
+          k0 += BK;
+          if (k0 >= sg.k) {
+            k0 = 0;
+            ++seg;
+          }
         }
       }
     }
@@ -478,7 +500,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
-      const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);
+      const uint32_t idesc = idesc_tf32(BM, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
@@ -488,9 +510,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         const uint32_t b_hi = base + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
-          const uint32_t off = j * 32;
-          const uint64_t dah = smem_desc(a_hi + off, 16, 1024), dal = smem_desc(a_lo + off, 16, 1024);
-          const uint64_t dbh = smem_desc(b_hi + off, 16, 1024), dbl = smem_desc(b_lo + off, 16, 1024);
+          uint64_t dah, dal, dbh, dbl;
+          if constexpr (IS_DW) {
+            // MN-major SWIZZLE_128B_BASE32B: 32-wide MN atoms 4 KB apart (LBO),
+            // 4-row K groups 512 B apart (SBO); an 8-deep k-step is 1 KB
+            const uint32_t off = j * 1024;
+            dah = smem_desc(a_hi + off, 4096, 512, 1);
+            dal = smem_desc(a_lo + off, 4096, 512, 1);
+            dbh = smem_desc(b_hi + off, 4096, 512, 1);
+            dbl = smem_desc(b_lo + off, 4096, 512, 1);
+          } else {
+            const uint32_t off = j * 32;
+            dah = smem_desc(a_hi + off, 16, 1024);
+            dal = smem_desc(a_lo + off, 16, 1024);
+            dbh = smem_desc(b_hi + off, 16, 1024);
+            dbl = smem_desc(b_lo + off, 16, 1024);
+          }
           const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
           mma_tf32(tmem, dal, dbh, idesc, acc0);
           mma_tf32(tmem, dah, dbl, idesc, 1u);
@@ -501,17 +536,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       mma_commit(done);
     }
   } else {
-    // ---------------- converters: A_lo = A - trunc(A) ----------------
+    // ---------------- converters: x_lo = x - trunc(x), same byte offsets ----------------
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
       mbar_wait(&tma_full[s], (it / C::STAGES) & 1);
-      const float4* a_hi = reinterpret_cast<const float4*>(smem + s * C::STAGE_BYTES);
-      float4* a_lo = reinterpret_cast<float4*>(smem + s * C::STAGE_BYTES + C::A_BYTES);
+      uint8_t* base = smem + s * C::STAGE_BYTES;
+      const float4* a_hi = reinterpret_cast<const float4*>(base);
+      float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
       for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
         const int q = threadIdx.x + i * kProducers;
         const float4 x = a_hi[q];
         a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+      }
+      if constexpr (IS_DW) {  // both dW operands are activations: split B too
+        const float4* b_hi = reinterpret_cast<const float4*>(base + 2 * C::A_BYTES);
+        float4* b_lo = reinterpret_cast<float4*>(base + 2 * C::A_BYTES + C::B_BYTES);
+        for (int q = threadIdx.x; q < C::B_BYTES / 16; q += kProducers) {
+          const float4 x = b_hi[q];
+          b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&conv_full[s]);
@@ -520,7 +564,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     mbar_wait(done, 0);
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue<BN, false>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -540,10 +584,10 @@ void launch_one(P p, int tiles, cudaStream_t s) {
   k<<<tiles, kThreads, Cfg<BN>::SMEM, s>>>(p);
 }
 
-template <int BN>
-void launch_tma(const GemmGroup& p, int tiles, cudaStream_t s) {
+template <int BN, bool IS_DW, class P>
+void launch_tma(const P& p, int tiles, cudaStream_t s) {
   static bool configured = false;
-  auto k = tma_gemm_kernel<BN>;
+  auto k = tma_gemm_kernel<BN, IS_DW, P>;
   if (!configured) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
     configured = true;
@@ -576,10 +620,10 @@ void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   const int tiles = p.tile_start[p.njobs];
   if (tiles == 0) return;
   if (p.tma) {
-    if (bn == 256) tc::launch_tma<256>(p, tiles, s);
-    else if (bn == 128) tc::launch_tma<128>(p, tiles, s);
-    else if (bn == 64) tc::launch_tma<64>(p, tiles, s);
-    else tc::launch_tma<32>(p, tiles, s);
+    if (bn == 256) tc::launch_tma<256, false>(p, tiles, s);
+    else if (bn == 128) tc::launch_tma<128, false>(p, tiles, s);
+    else if (bn == 64) tc::launch_tma<64, false>(p, tiles, s);
+    else tc::launch_tma<32, false>(p, tiles, s);
   } else {
     if (bn == 256) tc::launch_one<256, false>(p, tiles, s);
     else if (bn == 128) tc::launch_one<128, false>(p, tiles, s);
@@ -602,10 +646,17 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   }
   const int tiles = p.tile_start[p.njobs];
   if (tiles == 0) return;
-  if (bn == 256) tc::launch_one<256, true>(p, tiles, s);
-  else if (bn == 128) tc::launch_one<128, true>(p, tiles, s);
-  else if (bn == 64) tc::launch_one<64, true>(p, tiles, s);
-  else tc::launch_one<32, true>(p, tiles, s);
+  if (p.tma) {
+    if (bn == 256) tc::launch_tma<256, true>(p, tiles, s);
+    else if (bn == 128) tc::launch_tma<128, true>(p, tiles, s);
+    else if (bn == 64) tc::launch_tma<64, true>(p, tiles, s);
+    else tc::launch_tma<32, true>(p, tiles, s);
+  } else {
+    if (bn == 256) tc::launch_one<256, true>(p, tiles, s);
+    else if (bn == 128) tc::launch_one<128, true>(p, tiles, s);
+    else if (bn == 64) tc::launch_one<64, true>(p, tiles, s);
+    else tc::launch_one<32, true>(p, tiles, s);
+  }
 }
 
 }  // namespace rgb

@@ -96,11 +96,15 @@ struct DwJob {
   const float* y;      // [K x N] (N-major)
   float* g;            // [M x N] row-major
   int m, n;
+  const void* te;      // TMA maps (MN-major boxes) of E's and Y's buffers, or null
+  const void* ty;
+  int erow, yrow;      // first row of E / Y inside their buffers
 };
 
 struct DwGroup {
   int njobs, k;
-  float alpha, pad;
+  float alpha;
+  int tma;             // 1: every job has TMA maps
   int tile_start[kMaxDw + 1];
   int tiles_n[kMaxDw];
   DwJob job[kMaxDw];
