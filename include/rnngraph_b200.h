@@ -117,6 +117,11 @@ int rgb_count_nonfinite(rgb_plan* plan, int buffer, int64_t t_lo, int64_t t_hi, 
  * for latency-bound small products), 1 SIMT only, 2 tcgen05 only.  The
  * reference's deterministic k-ascending GEMMs are kernels.py:84-103. */
 int rgb_set_gemm_mode(int mode);
+/* Persistent recurrent-SCC kernel: 1 (default) runs every eligible
+ * frame-sequential loop (engine.py:405-413, 568-576) as one cooperative launch
+ * with W_rec resident in shared memory and a grid barrier per dense
+ * dependency; 0 launches the loop body once per frame. */
+int rgb_set_scc_mode(int on);
 /* Stand-alone GEMM forms (kernel-level parity tests): C[m,n] = A[m,k] . B[n,k]
  * (both row-major) and G[m,n] = alpha * sum_r E[r,m] Y[r,n]; mode 1 SIMT,
  * 2 tcgen05. */

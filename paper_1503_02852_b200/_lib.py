@@ -15,8 +15,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "librnngraph_b200.so")
-SOURCES = ["csrc/rgb_kernels.cu", "csrc/rgb_tc_gemm.cu", "csrc/rgb_plan.cu", "csrc/rgb_prof.cu"]
-HEADERS = ["csrc/rgb_types.cuh", "csrc/rgb_kernels.cuh", "csrc/rgb_ew.cuh", "csrc/rgb_prof.cuh",
+SOURCES = ["csrc/rgb_kernels.cu", "csrc/rgb_tc_gemm.cu", "csrc/rgb_scc.cu", "csrc/rgb_plan.cu", "csrc/rgb_prof.cu"]
+HEADERS = ["csrc/rgb_types.cuh", "csrc/rgb_kernels.cuh", "csrc/rgb_ew.cuh", "csrc/rgb_prof.cuh", "csrc/rgb_scc.cuh",
            "../include/rnngraph_b200.h"]
 PROF_CATEGORIES = ("ew", "gemm", "gemm_frame", "ew_frame", "dw", "softmax", "inject", "sgd", "transpose", "scc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -49,6 +49,7 @@ _SIGS = {
     "rgb_inject_rows": ([_P, _P, _I, _I, _P, _P, _P, _I, _I, _P], _I),
     "rgb_onehot_rows": ([_P, _I, _I, _P, _P], _I),
     "rgb_set_gemm_mode": ([_I], _I),
+    "rgb_set_scc_mode": ([_I], _I),
     "rgb_gemm_nt": ([_P, _P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_gemm_dw": ([_P, _P, _P, _I, _I, _I, ctypes.c_float, _I, _P], _I),
     "rgb_launch_count": ([ctypes.POINTER(_I64)], _I),

@@ -20,6 +20,9 @@
 #include "../../include/rnngraph_b200.h"
 #include "rgb_kernels.cuh"
 #include "rgb_prof.cuh"
+#include "rgb_scc.cuh"
+
+#include <map>
 
 using namespace rgb;
 
@@ -64,7 +67,12 @@ struct Ctx {
   const float* wt = nullptr;
   float* g = nullptr;
   bool in_loop = false;
+  int section = -1;                  // program section being run (fwd/bwd/...)
+  const int32_t* sec_base = nullptr; // its first word (to locate loop bodies)
 };
+
+// persistent SCC kernel switch (1 = use it for eligible loops)
+int g_scc_mode = 1;
 
 // algorithmic bytes of one elementwise chain over `rows` rows (reads + one
 // write per output; the ring mirror copy is an implementation cost, not counted)
@@ -142,8 +150,130 @@ struct rgb_plan {
   const float* map_w = nullptr;
   const float* map_wt = nullptr;
 
+  // device copies for the persistent SCC kernel: program sections, tables,
+  // grid-barrier state; plus the per-loop eligibility decisions
+  int32_t* prog_dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  SccBuf* bufs_dev = nullptr;
+  SccW* wts_dev = nullptr;
+  unsigned* bar_dev = nullptr;
+  struct SccPlan {
+    bool ok = false;
+    int width = 0, blocks = 0, use_cache = 0;
+    long long cache_floats = 0;
+    size_t smem = 0;
+    double flops_per_frame = 0;
+  };
+  std::map<std::pair<int, int64_t>, SccPlan> scc_plans;
+
   ~rgb_plan() {
     if (maps_dev) cudaFree(maps_dev);
+    for (auto* q : prog_dev)
+      if (q) cudaFree(q);
+    if (bufs_dev) cudaFree(bufs_dev);
+    if (wts_dev) cudaFree(wts_dev);
+    if (bar_dev) cudaFree(bar_dev);
+  }
+
+  int upload_scc_tables() {
+    for (int k = 0; k < 4; ++k) {
+      if (prog[k].empty() || prog_dev[k]) continue;
+      if (cudaMalloc(&prog_dev[k], prog[k].size() * 4) != cudaSuccess ||
+          cudaMemcpy(prog_dev[k], prog[k].data(), prog[k].size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(RGB_ERR_CUDA, "program upload failed");
+    }
+    if (!bufs_dev) {
+      std::vector<SccBuf> hb;
+      for (const BufDesc& b : bufs) hb.push_back(SccBuf{b.kind, b.width, (long long)b.off});
+      std::vector<SccW> hw;
+      for (const WDesc& d : wts) hw.push_back(SccW{d.rows, d.cols, (long long)d.off});
+      if (hb.empty()) hb.push_back(SccBuf{});
+      if (hw.empty()) hw.push_back(SccW{});
+      if (cudaMalloc(&bufs_dev, hb.size() * sizeof(SccBuf)) != cudaSuccess ||
+          cudaMalloc(&wts_dev, hw.size() * sizeof(SccW)) != cudaSuccess ||
+          cudaMalloc(&bar_dev, 2 * sizeof(unsigned)) != cudaSuccess)
+        return fail(RGB_ERR_CUDA, "SCC table allocation failed");
+      if (cudaMemcpy(bufs_dev, hb.data(), hb.size() * sizeof(SccBuf), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(wts_dev, hw.data(), hw.size() * sizeof(SccW), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemset(bar_dev, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+        return fail(RGB_ERR_CUDA, "SCC table upload failed");
+    }
+    return RGB_OK;
+  }
+
+  // Can this loop body run as one persistent launch?  Every GEMM job and
+  // elementwise chain must write one common width W (so a column partition is
+  // element-local for every op) and the per-frame work must be latency-sized.
+  SccPlan plan_scc(const int32_t* body, int64_t len) const {
+    SccPlan sp;
+    int64_t pos = 0;
+    int W = -1;
+    double macs = 0;
+    std::vector<int> ks;  // K of every GEMM segment, in walk order
+    auto width_ok = [&](int w) {
+      if (W < 0) W = w;
+      return W == w;
+    };
+    auto skip_op = [&](int64_t q) {
+      q += 3;
+      q += 1 + 2 * body[q];
+      q += 1 + 3 * body[q];
+      q += 1 + 2 * body[q];
+      q += 5;
+      q += 1 + body[q];
+      return q;
+    };
+    while (pos < len) {
+      const int kind = body[pos++];
+      if (kind == STEP_GEMM) {
+        const int njobs = body[pos++];
+        for (int j = 0; j < njobs; ++j) {
+          const int nseg = body[pos++];
+          int ksum = 0;
+          for (int s = 0; s < nseg; ++s, pos += 4) {
+            const WDesc& d = wts[body[pos + 2]];
+            const int K = body[pos + 3] ? d.rows : d.cols;
+            ks.push_back(K);
+            ksum += K;
+          }
+          const int width = body[pos], nops = body[pos + 1];
+          if (!width_ok(width)) return sp;
+          pos += 2;
+          for (int k = 0; k < nops; ++k) pos = skip_op(pos);
+          macs += (double)S * width * ksum;
+        }
+      } else if (kind == STEP_EW) {
+        const int nch = body[pos++];
+        for (int i = 0; i < nch; ++i) {
+          if (!width_ok(body[pos])) return sp;
+          const int nops = body[pos + 1];
+          pos += 2;
+          for (int k = 0; k < nops; ++k) pos = skip_op(pos);
+        }
+      } else {
+        return sp;  // softmax / nested loop / dW: not in a recurrent body
+      }
+    }
+    if (W <= 0 || macs > 64.0 * 1024 * 1024 || S > 256) return sp;
+    int blocks = W / 4 < 1 ? 1 : W / 4;
+    if (blocks > 148) blocks = 148;
+    const int ncol = (W + blocks - 1) / blocks;
+    long long cache = 0;
+    for (int K : ks) cache += (long long)ncol * K;
+    sp.use_cache = 1;
+    sp.smem = scc_smem_bytes((int)len, cache);
+    if (sp.smem > 200 * 1024) {
+      sp.use_cache = 0;
+      cache = 0;
+      sp.smem = scc_smem_bytes((int)len, 0);
+    }
+    const int maxb = scc_max_blocks(sp.smem);
+    if (maxb < blocks) return sp;  // all CTAs must be co-resident
+    sp.ok = true;
+    sp.width = W;
+    sp.blocks = blocks;
+    sp.cache_floats = cache;
+    sp.flops_per_frame = 2.0 * macs;
+    return sp;
   }
 
   int frames_of(int kind) const { return kind == BUF_RING ? 2 * cap : (kind == BUF_WIN ? hmax + maxd : hmax); }
@@ -424,6 +554,45 @@ struct rgb_plan {
         const int reverse = rd.next();
         const int len = rd.next();
         if (rd.i + len > n) return fail(RGB_ERR_KERNEL, "truncated loop body");
+        const int32_t* body = p + rd.i;
+        if (g_scc_mode && g_gemm_mode != 2 && c.section >= 0 && c.frames >= 2 && prog_dev[c.section]) {
+          const std::pair<int, int64_t> key{c.section, (int64_t)(body - c.sec_base)};
+          auto found = scc_plans.find(key);
+          if (found == scc_plans.end()) found = scc_plans.emplace(key, plan_scc(body, len)).first;
+          const SccPlan& sp = found->second;
+          if (sp.ok) {
+            SccCtx sc{};
+            sc.body = prog_dev[c.section] + key.second;
+            sc.body_len = len;
+            sc.width = sp.width;
+            sc.bufs = bufs_dev;
+            sc.wts = wts_dev;
+            sc.ws = ws;
+            sc.w = c.w;
+            sc.wt = c.wt;
+            sc.t_first = c.t_a;
+            sc.frames = c.frames;
+            sc.reverse = reverse;
+            sc.t1 = c.t1;
+            sc.t0 = c.t0;
+            sc.chunk_base = c.chunk_base;
+            sc.S = S;
+            sc.cap = cap;
+            sc.hmax = hmax;
+            sc.maxd = maxd;
+            sc.inj_buf = inj_buf;
+            sc.use_cache = sp.use_cache;
+            sc.wcache_floats = sp.cache_floats;
+            sc.bar = bar_dev;
+            const int slot = prof_start(st);
+            cudaError_t e = launch_scc(sc, sp.blocks, sp.smem, st);
+            note_launch();
+            prof_stop(slot, st, PROF_SCC, sp.flops_per_frame * c.frames, 0.0);
+            if (e != cudaSuccess) return fail(RGB_ERR_CUDA, "persistent SCC launch: %s", cudaGetErrorString(e));
+            rd.i += len;
+            continue;
+          }
+        }
         for (int f = 0; f < c.frames; ++f) {
           Ctx ci = c;
           ci.t_a = reverse ? c.t_a + c.frames - 1 - f : c.t_a + f;
@@ -535,6 +704,11 @@ extern "C" {
 
 int rgb_abi_version(void) { return RGB_ABI_VERSION; }
 
+int rgb_set_scc_mode(int on) {
+  g_scc_mode = on ? 1 : 0;
+  return RGB_OK;
+}
+
 int rgb_set_gemm_mode(int mode) {
   if (mode < 0 || mode > 2) return fail(RGB_ERR_KERNEL, "gemm mode must be 0 (auto), 1 (simt) or 2 (tcgen05)");
   g_gemm_mode = mode;
@@ -644,7 +818,9 @@ int rgb_plan_bind(rgb_plan* p, void* ws) {
   if (!p || !ws) return fail(RGB_ERR_KERNEL, "null argument");
   if (reinterpret_cast<uintptr_t>(ws) % 16) return fail(RGB_ERR_KERNEL, "workspace must be 16-byte aligned");
   p->ws = static_cast<float*>(ws);
-  return p->build_buffer_maps();
+  int rc = p->build_buffer_maps();
+  if (rc) return rc;
+  return p->upload_scc_tables();
   return RGB_OK;
 }
 
@@ -678,7 +854,9 @@ int rgb_forward_chunk(rgb_plan* p, const float* w, const float* x, int x_on_host
   c.t1 = p->cursor;
   c.t0 = p->cursor;
   c.w = w;
-  const auto& prog = p->prog[sequential ? 2 : 0];
+  c.section = sequential ? 2 : 0;
+  const auto& prog = p->prog[c.section];
+  c.sec_base = prog.data();
   return p->run(prog.data(), (int64_t)prog.size(), c, st);
 }
 
@@ -756,7 +934,9 @@ int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_pri
   c.chunk_base = c.t0 + 1;
   c.wt = wt;
   c.g = g;
-  const auto& prog = p->prog[sequential ? 3 : 1];
+  c.section = sequential ? 3 : 1;
+  const auto& prog = p->prog[c.section];
+  c.sec_base = prog.data();
   return p->run(prog.data(), (int64_t)prog.size(), c, as_stream(stream));
 }
 

@@ -1,0 +1,42 @@
+// Persistent recurrent-SCC kernel (rgb_scc.cu): launch descriptor.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rgb_types.cuh"
+
+namespace rgb {
+
+struct SccBuf {
+  int kind, width;
+  long long off;
+};
+struct SccW {
+  int rows, cols;
+  long long off;
+};
+
+struct SccCtx {
+  const int32_t* body;      // device copy of the loop-body step words
+  int body_len;
+  int width;                // common width W of every layer the body writes
+  const SccBuf* bufs;       // device copies of the plan's buffer / weight tables
+  const SccW* wts;
+  float* ws;
+  const float* w;
+  const float* wt;
+  long long t_first;        // first frame of the loop (ascending order)
+  int frames, reverse;
+  long long t1, t0, chunk_base;
+  int S, cap, hmax, maxd;
+  int inj_buf, use_cache;
+  long long wcache_floats;  // per-CTA shared-memory weight cache (0 = read W from global)
+  unsigned* bar;            // [count, generation] of the grid barrier
+};
+
+size_t scc_smem_bytes(int body_len, long long wcache_floats);
+int scc_max_blocks(size_t smem);  // co-resident CTAs for a cooperative launch
+cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s);
+
+}  // namespace rgb

@@ -282,7 +282,9 @@ template <int BN, bool IS_DW, class P>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ P p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SWIZZLE_128B); offset arithmetic keeps the pointer in the
+  // shared window so the compiler emits LDS/STS rather than generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* done = empty + C::STAGES;
@@ -416,7 +418,9 @@ template <int BN, bool IS_DW, class P>
 __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ P p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SWIZZLE_128B); offset arithmetic keeps the pointer in the
+  // shared window so the compiler emits LDS/STS rather than generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* conv_full = tma_full + C::STAGES;
   uint64_t* empty = conv_full + C::STAGES;

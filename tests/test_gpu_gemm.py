@@ -88,6 +88,26 @@ def test_engine_parity_simt_forced():
         _lib.check(L.rgb_set_gemm_mode(0))
 
 
+def test_engine_parity_without_persistent_scc():
+    """Per-frame launches instead of the persistent SCC kernel (the default)."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_scc_mode(0))
+    try:
+        assert run_pair(P.build_lstm(39, 128, 39), 1, 32, 16, 4, 1e-3, 0) < 1e-4
+        assert run_pair(P.build_custom_graph(), 2, 16, 8, 4, 1e-3, 1) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_scc_mode(1))
+
+
+def test_persistent_scc_matches_per_frame_launches():
+    """Same step with and without the persistent kernel (fp32 rounding only)."""
+    from test_gpu_engine import run_pair
+    net = P.build_stacked_lstm(48, [64, 64], 40)
+    assert run_pair(net, 3, 24, 8, 5, 1e-2, 7) < 1e-4
+    assert run_pair(P.build_custom_graph(16, 512, 16), 1, 32, 16, 3, 1e-3, 8) < 1e-4
+
+
 def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
