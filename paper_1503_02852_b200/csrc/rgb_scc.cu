@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   int32_t* words = reinterpret_cast<int32_t*>(sm);
   const int words_pad = (c.body_len + 3) & ~3;
   float* wcache = reinterpret_cast<float*>(words + words_pad);
-  SJob* jobs = reinterpret_cast<SJob*>(wcache + c.wcache_floats);
+  SJob* jobs = reinterpret_cast<SJob*>(wcache + ((c.wcache_floats + 3) & ~3LL));  // 16-B aligned
   EwChain* chains = reinterpret_cast<EwChain*>(jobs + kMaxJobs);
   __shared__ int s_nunits;
 
@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
 }  // namespace
 
 size_t scc_smem_bytes(int body_len, long long wcache_floats) {
-  return (size_t)((body_len + 3) & ~3) * 4 + (size_t)wcache_floats * 4 + sizeof(SJob) * kMaxJobs +
+  static_assert(sizeof(SJob) % 16 == 0 || sizeof(SJob) % 8 == 0, "SJob keeps 8-byte alignment");
+  return (size_t)((body_len + 3) & ~3) * 4 + (size_t)((wcache_floats + 3) & ~3LL) * 4 + sizeof(SJob) * kMaxJobs +
          sizeof(EwChain) * kMaxChains + 64;
 }
 
@@ -274,6 +275,9 @@ int scc_max_blocks(size_t smem) {
 }
 
 cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s) {
+  // the attribute is per function, not per launch: (re)set it for this size
+  cudaError_t e = cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   void* args[] = {const_cast<SccCtx*>(&c)};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scc_kernel), dim3(blocks), dim3(kSccThreads), args,
                                      smem, s);
