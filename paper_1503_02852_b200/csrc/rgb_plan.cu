@@ -158,8 +158,8 @@ struct rgb_plan {
   unsigned* bar_dev = nullptr;
   struct SccPlan {
     bool ok = false;
-    int width = 0, blocks = 0, use_cache = 0;
-    long long cache_floats = 0;
+    int width = 0, blocks = 0, use_cache = 0, cluster = 0;
+    long long cache_floats = 0, acc_floats = 0, stage_floats = 0, arena_bytes = 0;
     size_t smem = 0;
     double flops_per_frame = 0;
   };
@@ -206,28 +206,40 @@ struct rgb_plan {
   SccPlan plan_scc(const int32_t* body, int64_t len) const {
     SccPlan sp;
     int64_t pos = 0;
-    int W = -1;
+    int W = -1, max_jobs = 0, nsteps = 0, njobs_total = 0, nchains_total = 0, nslots = 0;
+    long long max_step_akf = 0;  // A floats per stream row read by one GEMM step
     double macs = 0;
     std::vector<int> ks;  // K of every GEMM segment, in walk order
     auto width_ok = [&](int w) {
       if (W < 0) W = w;
       return W == w;
     };
-    auto skip_op = [&](int64_t q) {
+    auto skip_op = [&](int64_t q) {  // also counts the op's pointer slots (device template)
       q += 3;
+      nslots += 1 + body[q];
       q += 1 + 2 * body[q];
+      nslots += body[q];
       q += 1 + 3 * body[q];
+      nslots += body[q];
       q += 1 + 2 * body[q];
+      nslots += (body[q] >= 0) + (body[q + 2] >= 0) + (body[q + 4] != 0);
       q += 5;
+      for (int i = 0; i < body[q]; ++i) nslots += body[q + 1 + i] >= 0;
       q += 1 + body[q];
       return q;
     };
     while (pos < len) {
       const int kind = body[pos++];
+      ++nsteps;
       if (kind == STEP_GEMM) {
         const int njobs = body[pos++];
+        if (njobs > max_jobs) max_jobs = njobs;
+        njobs_total += njobs;
+        nchains_total += njobs;
+        long long step_akf = 0;
         for (int j = 0; j < njobs; ++j) {
           const int nseg = body[pos++];
+          nslots += nseg;
           int ksum = 0;
           for (int s = 0; s < nseg; ++s, pos += 4) {
             const WDesc& d = wts[body[pos + 2]];
@@ -240,9 +252,12 @@ struct rgb_plan {
           pos += 2;
           for (int k = 0; k < nops; ++k) pos = skip_op(pos);
           macs += (double)S * width * ksum;
+          step_akf += ksum;
         }
+        if (step_akf > max_step_akf) max_step_akf = step_akf;
       } else if (kind == STEP_EW) {
         const int nch = body[pos++];
+        nchains_total += nch;
         for (int i = 0; i < nch; ++i) {
           if (!width_ok(body[pos])) return sp;
           const int nops = body[pos + 1];
@@ -253,25 +268,38 @@ struct rgb_plan {
         return sp;  // softmax / nested loop / dW: not in a recurrent body
       }
     }
-    if (W <= 0 || macs > 64.0 * 1024 * 1024 || S > 256) return sp;
-    int blocks = W / 4 < 1 ? 1 : W / 4;
+    if (W <= 0 || macs > 64.0 * 1024 * 1024 || S > 256 || nsteps > 8 || nslots > 512) return sp;
+    // small per-frame work: one cluster of <= 16 CTAs (hardware cluster barrier,
+    // ~0.2 us); otherwise up to 148 CTAs with the atomic grid barrier (~2.3 us)
+    const bool cluster = macs / 16.0 <= 1024.0 * 1024.0;
+    int blocks = cluster ? (W / 4 < 1 ? 1 : (W / 4 > 16 ? 16 : W / 4)) : (W / 4 < 1 ? 1 : W / 4);
     if (blocks > 148) blocks = 148;
     const int ncol = (W + blocks - 1) / blocks;
-    long long cache = 0;
-    for (int K : ks) cache += (long long)ncol * K;
+    SccCtx probe{};
+    probe.nbufs = (int)bufs.size();
+    probe.nwts = (int)wts.size();
+    probe.acc_floats = (long long)max_jobs * S * ncol;
+    probe.arena_bytes = (long long)scc_arena_bytes(njobs_total, nchains_total);
+    probe.wcache_floats = 0;
+    for (int K : ks) probe.wcache_floats += (long long)ncol * K;
+    probe.stage_floats = max_step_akf * S <= 16384 ? max_step_akf * S : 0;
     sp.use_cache = 1;
-    sp.smem = scc_smem_bytes((int)len, cache);
+    sp.smem = scc_smem_bytes(probe);
     if (sp.smem > 200 * 1024) {
       sp.use_cache = 0;
-      cache = 0;
-      sp.smem = scc_smem_bytes((int)len, 0);
+      probe.wcache_floats = 0;
+      sp.smem = scc_smem_bytes(probe);
+      if (sp.smem > 200 * 1024) return sp;
     }
-    const int maxb = scc_max_blocks(sp.smem);
-    if (maxb < blocks) return sp;  // all CTAs must be co-resident
+    if (!cluster && scc_max_blocks(sp.smem) < blocks) return sp;  // cooperative: all CTAs co-resident
     sp.ok = true;
+    sp.cluster = cluster ? 1 : 0;
     sp.width = W;
     sp.blocks = blocks;
-    sp.cache_floats = cache;
+    sp.cache_floats = probe.wcache_floats;
+    sp.acc_floats = probe.acc_floats;
+    sp.stage_floats = probe.stage_floats;
+    sp.arena_bytes = probe.arena_bytes;
     sp.flops_per_frame = 2.0 * macs;
     return sp;
   }
@@ -567,6 +595,8 @@ struct rgb_plan {
             sc.width = sp.width;
             sc.bufs = bufs_dev;
             sc.wts = wts_dev;
+            sc.nbufs = (int)bufs.size();
+            sc.nwts = (int)wts.size();
             sc.ws = ws;
             sc.w = c.w;
             sc.wt = c.wt;
@@ -582,7 +612,11 @@ struct rgb_plan {
             sc.maxd = maxd;
             sc.inj_buf = inj_buf;
             sc.use_cache = sp.use_cache;
+            sc.cluster = sp.cluster;
             sc.wcache_floats = sp.cache_floats;
+            sc.acc_floats = sp.acc_floats;
+            sc.stage_floats = sp.stage_floats;
+            sc.arena_bytes = sp.arena_bytes;
             sc.bar = bar_dev;
             const int slot = prof_start(st);
             cudaError_t e = launch_scc(sc, sp.blocks, sp.smem, st);

@@ -1,22 +1,29 @@
 // Persistent recurrent-SCC kernel (paper §3.1: the frame-sequential part).
 //
-// One cooperative launch runs a whole per-frame loop of one strongly connected
-// component -- forward (ascending) or backward (descending) -- instead of one or
-// two launches per frame.  The loop body is the same int32 step program the
-// host executor interprets (schedule.py), copied to shared memory and walked
-// by the device every frame:
+// One launch runs a whole per-frame loop of one strongly connected component
+// -- forward (ascending) or backward (descending) -- instead of one or two
+// launches per frame.  The loop body is the same int32 step program the host
+// executor interprets (schedule.py):
+//   * at kernel start the body is parsed ONCE into shared-memory templates
+//     (GEMM jobs, elementwise chains) plus a list of frame-dependent pointer
+//     "slots" (operand buffer + frame shift); per frame the CTA's threads
+//     re-resolve the slots in parallel -- no per-frame parsing;
 //   * GEMM step (the intra-SCC dense edges, e.g. cell(t-1) -> {in,forget}
 //     gates): CTA b owns output columns [b*W/G, (b+1)*W/G) of every job; the
 //     matching rows of the recurrent weights (W_rec) are loaded into shared
-//     memory ONCE at kernel start and stay resident for all frames; one warp
-//     per (stream, column) dot product, then the fused elementwise epilogue
-//     (activation, gates, cell update, f', eps) for that element;
+//     memory once and stay resident for all frames.  Phase 1: one warp per
+//     (job, stream row) reads the A row once and dots it with every owned
+//     weight row; phase 2: one thread per output element runs the fused
+//     elementwise chain (activation, gates, cell update, f', eps);
 //   * elementwise step: the CTA's own columns (element-local by construction);
-//   * a grid barrier precedes every GEMM step -- the only place a CTA reads
-//     columns other CTAs wrote (the delayed or zero-delay dense edges).
+//   * before every GEMM step the CTAs synchronise: the hardware cluster
+//     barrier (~0.2 us, measured) when the SCC is small enough for one cluster
+//     of <= 16 CTAs, else an atomic grid barrier (~2.3 us) over a cooperative
+//     launch (tools/barrier_probe.cu).
 // Reference semantics: engine.py:405-413 (forward), 568-576 (backward).
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "rgb_ew.cuh"
@@ -27,75 +34,113 @@ namespace rgb {
 namespace {
 
 constexpr int kSccThreads = 256;
+constexpr int kColChunk = 4;   // owned weight rows dotted per pass over an A row
+constexpr int kMaxSteps = 8;
+constexpr int kMaxSlots = 512;
 enum { S_EW = 1, S_GEMM = 2 };
 
 __device__ __forceinline__ long long pmod_d(long long a, long long m) { return ((a % m) + m) % m; }
 
-__device__ __forceinline__ float* resolve_d(const SccCtx& c, int buf, int shift, long long t) {
-  const SccBuf b = c.bufs[buf];
-  const long long tt = t + shift;
-  long long idx;
-  if (b.kind == 0) idx = pmod_d(tt, c.cap);
-  else if (b.kind == 1) idx = tt - c.t1 + c.hmax - 1;
-  else idx = tt - c.chunk_base;
-  return c.ws + b.off + idx * (long long)c.S * b.width;
-}
+struct SJob {
+  int nseg, n;
+  const float* a[kMaxSegs];   // A rows of the frame (slot-resolved)
+  const float* bs[kMaxSegs];  // this CTA's weight rows (shared or global)
+  const float* bsrc[kMaxSegs];  // the same rows in global memory (cache source)
+  int k[kMaxSegs];
+  int pad[kMaxSegs];
+};
 
-// Parse one op (same word layout as rgb_plan.cu parse_op) for frame t.
-__device__ int parse_op_d(const int32_t* w, int pos, const SccCtx& c, long long t, EwOp& op) {
-  op.kind = w[pos++];
-  op.act = w[pos++];
-  const int out_buf = w[pos++];
-  op.out = resolve_d(c, out_buf, 0, t);
-  op.out_is_ring = c.bufs[out_buf].kind == 0;
-  op.nterm = w[pos++];
-  for (int i = 0; i < op.nterm; ++i, pos += 2) op.term[i] = resolve_d(c, w[pos], w[pos + 1], t);
-  op.nrank1 = w[pos++];
-  for (int i = 0; i < op.nrank1; ++i, pos += 3) {
-    op.r1src[i] = resolve_d(c, w[pos], w[pos + 1], t);
-    op.r1w[i] = c.w + c.wts[w[pos + 2]].off;
+struct Slot {
+  int off;      // byte offset of the pointer field inside the template arena
+  short buf, shift;
+  int inj;      // 1: only valid on injected frames (t > t0)
+};
+
+struct Step {
+  int kind, n;          // S_GEMM: n jobs; S_EW: n chains
+  int jobs_off, chains_off;
+  int slot_begin, slot_end;
+};
+
+// Per-frame index bases: ring slot, window index, chunk index of frame t.
+struct FrameIdx {
+  int tmod, win, chunk, inj;
+};
+
+__device__ __forceinline__ float* resolve(const SccCtx& c, const SccBuf* bufs, const FrameIdx& f, int buf, int shift) {
+  const SccBuf b = bufs[buf];
+  int idx;
+  if (b.kind == 0) {
+    idx = f.tmod + shift;
+    while (idx < 0) idx += c.cap;
+    while (idx >= c.cap) idx -= c.cap;
+  } else {
+    idx = (b.kind == 1 ? f.win : f.chunk) + shift;
   }
-  op.nfac = w[pos++];
-  for (int i = 0; i < op.nfac; ++i, pos += 2) op.fac[i] = resolve_d(c, w[pos], w[pos + 1], t);
-  op.y = w[pos] >= 0 ? resolve_d(c, w[pos], w[pos + 1], t) : nullptr;
-  pos += 2;
-  op.base = w[pos] >= 0 ? resolve_d(c, w[pos], w[pos + 1], t) : nullptr;  // -2 (accumulator) -> null
-  pos += 2;
-  const int inj = w[pos++];
-  op.inj = nullptr;
-  op.inj_row0 = 0;
-  if (inj && t > c.t0) op.inj = resolve_d(c, c.inj_buf, 0, t);
-  const int neps = w[pos++];
-  for (int i = 0; i < kMaxFac; ++i) op.eps[i] = nullptr;
-  for (int i = 0; i < neps; ++i, ++pos) op.eps[i] = w[pos] >= 0 ? resolve_d(c, w[pos], 0, t) : nullptr;
-  return pos;
+  return c.ws + b.off + (long long)idx * c.S * b.width;
 }
 
-__device__ int parse_chain_d(const int32_t* w, int pos, const SccCtx& c, long long t, EwChain& ch) {
-  ch.width = w[pos++];
-  ch.nops = w[pos++];
-  for (int k = 0; k < ch.nops; ++k) pos = parse_op_d(w, pos, c, t, ch.op[k]);
-  return pos;
-}
+// ---- one-time template build (thread 0) ------------------------------------
 
-// Skip an op / chain without resolving (used by the weight preload walk).
-__device__ int skip_op(const int32_t* w, int pos) {
-  pos += 3;
-  pos += 1 + 2 * w[pos];
-  pos += 1 + 3 * w[pos];
-  pos += 1 + 2 * w[pos];
-  pos += 4;
-  pos += 1;
-  pos += 1 + w[pos];
-  return pos;
-}
+struct Builder {
+  const int32_t* w;
+  int pos;
+  unsigned char* arena;
+  int used;
+  Slot* slots;
+  int nslots;
+  bool ok;
 
-__device__ int skip_chain(const int32_t* w, int pos) {
-  const int nops = w[pos + 1];
-  pos += 2;
-  for (int k = 0; k < nops; ++k) pos = skip_op(w, pos);
-  return pos;
-}
+  template <class T>
+  __device__ T* alloc(int count, int& off) {
+    used = (used + 15) & ~15;
+    off = used;
+    used += count * (int)sizeof(T);
+    return reinterpret_cast<T*>(arena + off);
+  }
+  __device__ void slot(const void* field, int buf, int shift, int inj = 0) {
+    if (nslots >= kMaxSlots) {
+      ok = false;
+      return;
+    }
+    slots[nslots++] = Slot{(int)(reinterpret_cast<const unsigned char*>(field) - arena), (short)buf, (short)shift, inj};
+  }
+  __device__ void op(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwOp& o) {
+    o.kind = w[pos++];
+    o.act = w[pos++];
+    const int out = w[pos++];
+    o.out = nullptr;
+    slot(&o.out, out, 0);
+    o.out_is_ring = bufs[out].kind == 0;
+    o.nterm = w[pos++];
+    for (int i = 0; i < o.nterm; ++i, pos += 2) slot(&o.term[i], w[pos], w[pos + 1]);
+    o.nrank1 = w[pos++];
+    for (int i = 0; i < o.nrank1; ++i, pos += 3) {
+      slot(&o.r1src[i], w[pos], w[pos + 1]);
+      o.r1w[i] = c.w + wts[w[pos + 2]].off;  // frame-independent
+    }
+    o.nfac = w[pos++];
+    for (int i = 0; i < o.nfac; ++i, pos += 2) slot(&o.fac[i], w[pos], w[pos + 1]);
+    o.y = nullptr;
+    if (w[pos] >= 0) slot(&o.y, w[pos], w[pos + 1]);
+    pos += 2;
+    o.base = nullptr;  // -2 (accumulator) stays null
+    if (w[pos] >= 0) slot(&o.base, w[pos], w[pos + 1]);
+    pos += 2;
+    o.inj = nullptr;
+    o.inj_row0 = 0;
+    if (w[pos++]) slot(&o.inj, c.inj_buf, 0, 1);
+    const int neps = w[pos++];
+    for (int i = 0; i < kMaxFac; ++i) o.eps[i] = nullptr;
+    for (int i = 0; i < neps; ++i, ++pos)
+      if (w[pos] >= 0) slot(&o.eps[i], w[pos], 0);
+  }
+  __device__ void chain(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwChain& ch) {
+    ch.width = w[pos++];
+    ch.nops = w[pos++];
+    for (int k = 0; k < ch.nops; ++k) op(c, bufs, wts, ch.op[k]);
+  }
+};
 
 // Sense-reversing grid barrier over the co-resident CTAs of a cooperative launch.
 __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks, unsigned& my_gen) {
@@ -119,146 +164,211 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, uns
   __syncthreads();
 }
 
-struct SJob {
-  int nseg, n;
-  const float* a[kMaxSegs];
-  const float* bs[kMaxSegs];  // weight rows of this CTA's columns (shared or global)
-  int k[kMaxSegs];
-  int b_ld[kMaxSegs];         // leading dimension of bs (k when cached, k as well in global)
-};
+__device__ __forceinline__ void sync_ctas(const SccCtx& c, unsigned& my_gen) {
+  if (c.cluster) {
+    // release/acquire at cluster scope: global writes of every CTA in the
+    // cluster are visible after the barrier (the acquire invalidates L1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    grid_barrier(c.bar, c.bar + 1, gridDim.x, my_gen);
+  }
+}
 
 __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_constant__ SccCtx c) {
   extern __shared__ __align__(16) unsigned char sm[];
-  int32_t* words = reinterpret_cast<int32_t*>(sm);
-  const int words_pad = (c.body_len + 3) & ~3;
-  float* wcache = reinterpret_cast<float*>(words + words_pad);
-  SJob* jobs = reinterpret_cast<SJob*>(wcache + ((c.wcache_floats + 3) & ~3LL));  // 16-B aligned
-  EwChain* chains = reinterpret_cast<EwChain*>(jobs + kMaxJobs);
-  __shared__ int s_nunits;
+  // layout: [tables][weight cache][accumulators][template arena][slots]
+  SccBuf* sbufs = reinterpret_cast<SccBuf*>(sm);
+  SccW* swts = reinterpret_cast<SccW*>(sbufs + c.nbufs);
+  float* wcache = reinterpret_cast<float*>(
+      sm + ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)));
+  float* accs = wcache + ((c.wcache_floats + 3) & ~3LL);
+  float* astage = accs + ((c.acc_floats + 3) & ~3LL);
+  unsigned char* arena = reinterpret_cast<unsigned char*>(astage + ((c.stage_floats + 3) & ~3LL));
+  Slot* slots = reinterpret_cast<Slot*>(arena + c.arena_bytes);
+  __shared__ Step steps[kMaxSteps];
+  __shared__ int s_nsteps;
 
-  for (int i = threadIdx.x; i < c.body_len; i += blockDim.x) words[i] = c.body[i];
+  for (int i = threadIdx.x; i < c.nbufs; i += blockDim.x) sbufs[i] = c.bufs[i];
+  for (int i = threadIdx.x; i < c.nwts; i += blockDim.x) swts[i] = c.wts[i];
   const int W = c.width;
   const int j0 = (int)((long long)blockIdx.x * W / gridDim.x);
   const int j1 = (int)((long long)(blockIdx.x + 1) * W / gridDim.x);
   const int ncol = j1 - j0;
   __syncthreads();
 
-  // preload this CTA's weight rows of every GEMM step (identical walk in all threads)
-  if (c.use_cache) {
-    int pos = 0, off = 0;
-    while (pos < c.body_len) {
-      const int kind = words[pos++];
-      if (kind == S_GEMM) {
-        const int njobs = words[pos++];
-        for (int jb = 0; jb < njobs; ++jb) {
-          const int nseg = words[pos++];
-          for (int s = 0; s < nseg; ++s, pos += 4) {
-            const int cid = words[pos + 2], trans = words[pos + 3];
-            const SccW wd = c.wts[cid];
+  // ---- build the templates once (thread 0), preload W_rec rows (all threads)
+  if (threadIdx.x == 0) {
+    Builder B{c.body, 0, arena, 0, slots, 0, true};
+    int nsteps = 0, woff = 0;
+    while (B.pos < c.body_len && nsteps < kMaxSteps) {
+      Step& st = steps[nsteps++];
+      st.kind = B.w[B.pos++];
+      st.n = B.w[B.pos++];
+      st.slot_begin = B.nslots;
+      if (st.kind == S_GEMM) {
+        SJob* jobs = B.alloc<SJob>(st.n, st.jobs_off);
+        EwChain* chains = B.alloc<EwChain>(st.n, st.chains_off);
+        for (int jb = 0; jb < st.n; ++jb) {
+          SJob& J = jobs[jb];
+          J.nseg = B.w[B.pos++];
+          for (int s = 0; s < J.nseg; ++s, B.pos += 4) {
+            const int ab = B.w[B.pos], ash = B.w[B.pos + 1], cid = B.w[B.pos + 2], trans = B.w[B.pos + 3];
+            const SccW wd = swts[cid];
             const int K = trans ? wd.rows : wd.cols;
-            const float* src = (trans ? c.wt : c.w) + wd.off + (long long)j0 * K;
-            for (int i = threadIdx.x; i < ncol * K; i += blockDim.x) wcache[off + i] = src[i];
-            off += ncol * K;
+            J.k[s] = K;
+            J.a[s] = nullptr;
+            B.slot(&J.a[s], ab, ash);
+            J.bsrc[s] = (trans ? c.wt : c.w) + wd.off + (long long)j0 * K;
+            if (c.use_cache) {
+              J.bs[s] = wcache + woff;
+              woff += ncol * K;
+            } else {
+              J.bs[s] = J.bsrc[s];
+            }
           }
-          pos = skip_chain(words, pos);
+          B.chain(c, sbufs, swts, chains[jb]);
+          J.n = chains[jb].width;
         }
       } else {
-        const int nch = words[pos++];
-        for (int i = 0; i < nch; ++i) pos = skip_chain(words, pos);
+        st.jobs_off = 0;
+        EwChain* chains = B.alloc<EwChain>(st.n, st.chains_off);
+        for (int i = 0; i < st.n; ++i) B.chain(c, sbufs, swts, chains[i]);
       }
+      st.slot_end = B.nslots;
+    }
+    s_nsteps = nsteps;
+  }
+  __syncthreads();
+  if (c.use_cache) {
+    int off = 0;
+    for (int si = 0; si < s_nsteps; ++si) {
+      if (steps[si].kind != S_GEMM) continue;
+      const SJob* jobs = reinterpret_cast<const SJob*>(arena + steps[si].jobs_off);
+      for (int jb = 0; jb < steps[si].n; ++jb)
+        for (int s = 0; s < jobs[jb].nseg; ++s) {
+          const int K = jobs[jb].k[s];
+          const float* src = jobs[jb].bsrc[s];
+          for (int i = threadIdx.x; i < ncol * K; i += blockDim.x) wcache[off + i] = src[i];
+          off += ncol * K;
+        }
     }
   }
   unsigned my_gen = 0;
-  if (threadIdx.x == 0) my_gen = *reinterpret_cast<volatile unsigned*>(c.bar + 1);
+  if (!c.cluster && threadIdx.x == 0) my_gen = *reinterpret_cast<volatile unsigned*>(c.bar + 1);
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int f = 0; f < c.frames; ++f) {
     const long long t = c.reverse ? c.t_first + c.frames - 1 - f : c.t_first + f;
+    FrameIdx fi;
+    fi.tmod = (int)pmod_d(t, c.cap);
+    fi.win = (int)(t - c.t1 + c.hmax - 1);
+    fi.chunk = (int)(t - c.chunk_base);
+    fi.inj = t > c.t0;
     RingWrite ring;
-    ring.split = (long long)(c.cap - pmod_d(t, c.cap)) * c.S;
+    ring.split = (long long)(c.cap - fi.tmod) * c.S;
     ring.frame_rows = (long long)c.cap * c.S;
-    int pos = 0, woff = 0;
-    while (pos < c.body_len) {
-      const int kind = words[pos];
-      if (kind == S_GEMM) {
-        grid_barrier(c.bar, c.bar + 1, gridDim.x, my_gen);
-        const int njobs = words[pos + 1];
-        if (threadIdx.x == 0) {
-          int p = pos + 2;
-          for (int jb = 0; jb < njobs; ++jb) {
-            SJob& J = jobs[jb];
-            J.nseg = words[p++];
-            for (int s = 0; s < J.nseg; ++s, p += 4) {
-              const int ab = words[p], ash = words[p + 1], cid = words[p + 2], trans = words[p + 3];
-              const SccW wd = c.wts[cid];
-              const int K = trans ? wd.rows : wd.cols;
-              J.a[s] = resolve_d(c, ab, ash, t);
-              J.k[s] = K;
-              J.b_ld[s] = K;
-              if (c.use_cache) {
-                J.bs[s] = wcache + woff;
-                woff += ncol * K;
-              } else {
-                J.bs[s] = (trans ? c.wt : c.w) + wd.off + (long long)j0 * K;
-              }
+    for (int si = 0; si < s_nsteps; ++si) {
+      const Step st = steps[si];
+      // the CTAs only exchange data through the dense (GEMM) reads
+      if (st.kind == S_GEMM) sync_ctas(c, my_gen);
+      for (int i = st.slot_begin + threadIdx.x; i < st.slot_end; i += blockDim.x) {
+        const Slot sl = slots[i];
+        *reinterpret_cast<float**>(arena + sl.off) =
+            (sl.inj && !fi.inj) ? nullptr : resolve(c, sbufs, fi, sl.buf, sl.shift);
+      }
+      __syncthreads();
+      const EwChain* chains = reinterpret_cast<const EwChain*>(arena + st.chains_off);
+      if (st.kind == S_GEMM) {
+        const SJob* jobs = reinterpret_cast<const SJob*>(arena + st.jobs_off);
+        // stage the (small) A operands in shared memory once: every CTA reads
+        // the whole state vector(s) written by its peers in the previous phase
+        const float* a_src[kMaxJobs][kMaxSegs];
+        if (c.stage_floats > 0) {
+          int off = 0;
+          for (int jb = 0; jb < st.n; ++jb)
+            for (int s = 0; s < jobs[jb].nseg; ++s) {
+              const int n = c.S * jobs[jb].k[s];
+              const float* src = jobs[jb].a[s];
+              for (int i = threadIdx.x; i < n; i += blockDim.x) astage[off + i] = src[i];
+              a_src[jb][s] = astage + off;
+              off += n;
             }
-            p = parse_chain_d(words, p, c, t, chains[jb]);
-            J.n = chains[jb].width;
-          }
-          s_nunits = p;  // end of the step
+          __syncthreads();
+        } else {
+          for (int jb = 0; jb < st.n; ++jb)
+            for (int s = 0; s < jobs[jb].nseg; ++s) a_src[jb][s] = jobs[jb].a[s];
         }
-        __syncthreads();
-        pos = s_nunits;  // (woff is only meaningful in thread 0, which resolved the pointers)
-        // one warp per (job, stream, column): dot products over all segments
-        const int items = njobs * c.S * ncol;
-        for (int it = warp; it < items; it += nwarps) {
-          const int jb = it / (c.S * ncol), rem = it - jb * (c.S * ncol);
-          const int srow = rem / ncol, col = rem - srow * ncol;
+        // phase 1: one warp per (job, stream row, chunk of owned columns)
+        const int nchunks = (ncol + kColChunk - 1) / kColChunk;
+        const int items1 = st.n * c.S * nchunks;
+        for (int it = warp; it < items1; it += nwarps) {
+          const int jb = it / (c.S * nchunks), rem = it - jb * (c.S * nchunks);
+          const int srow = rem / nchunks, c0 = (rem - srow * nchunks) * kColChunk;
           const SJob& J = jobs[jb];
-          float acc = 0.f;
+          float part[kColChunk];
+#pragma unroll
+          for (int q = 0; q < kColChunk; ++q) part[q] = 0.f;
           for (int s = 0; s < J.nseg; ++s) {
-            const float* a = J.a[s] + (long long)srow * J.k[s];
-            const float* b = J.bs[s] + (long long)col * J.b_ld[s];
-            for (int k = lane; k < J.k[s]; k += 32) acc = fmaf(a[k], b[k], acc);
+            const float* a = a_src[jb][s] + (long long)srow * J.k[s];
+            const float* b = J.bs[s] + (long long)c0 * J.k[s];
+            const int K = J.k[s];
+#pragma unroll 4
+            for (int k = lane; k < K; k += 32) {
+              const float av = a[k];
+#pragma unroll
+              for (int q = 0; q < kColChunk; ++q)
+                if (c0 + q < ncol) part[q] = fmaf(av, b[(long long)q * K + k], part[q]);
+            }
           }
 #pragma unroll
-          for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          for (int q = 0; q < kColChunk; ++q) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+          }
           if (lane == 0) {
-            const EwChain& ch = chains[jb];
-            for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
+#pragma unroll
+            for (int q = 0; q < kColChunk; ++q)
+              if (c0 + q < ncol) accs[(jb * c.S + srow) * ncol + c0 + q] = part[q];
           }
         }
         __syncthreads();
-      } else {  // S_EW
-        const int nch = words[pos + 1];
-        if (threadIdx.x == 0) {
-          int p = pos + 2;
-          for (int i = 0; i < nch; ++i) p = parse_chain_d(words, p, c, t, chains[i]);
-          s_nunits = p;
+        const int items = st.n * c.S * ncol;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+          const int jb = it / (c.S * ncol), rem = it - jb * (c.S * ncol);
+          const int srow = rem / ncol, col = rem - srow * ncol;
+          const EwChain& ch = chains[jb];
+          const float acc = accs[it];
+          for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
         }
-        __syncthreads();
-        pos = s_nunits;
-        for (int i = 0; i < nch; ++i) {
+      } else {
+        const int items = c.S * ncol;
+        for (int i = 0; i < st.n; ++i) {
           const EwChain& ch = chains[i];
-          const int items = c.S * ncol;
           for (int e = threadIdx.x; e < items; e += blockDim.x) {
             const int srow = e / ncol, col = j0 + (e - (e / ncol) * ncol);
             for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, col, ring, false, 0.0f);
           }
         }
-        __syncthreads();
       }
+      __syncthreads();
     }
+  }
+  if (c.cluster) {  // no CTA may exit while a peer could still be inside a barrier phase
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 }
 
 }  // namespace
 
-size_t scc_smem_bytes(int body_len, long long wcache_floats) {
-  static_assert(sizeof(SJob) % 16 == 0 || sizeof(SJob) % 8 == 0, "SJob keeps 8-byte alignment");
-  return (size_t)((body_len + 3) & ~3) * 4 + (size_t)((wcache_floats + 3) & ~3LL) * 4 + sizeof(SJob) * kMaxJobs +
-         sizeof(EwChain) * kMaxChains + 64;
+size_t scc_smem_bytes(const SccCtx& c) {
+  return ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)) +
+         (size_t)((c.wcache_floats + 3) & ~3LL) * 4 + (size_t)((c.acc_floats + 3) & ~3LL) * 4 +
+         (size_t)((c.stage_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots + 64;
+}
+
+size_t scc_arena_bytes(int max_jobs_total, int max_chains_total) {
+  return (size_t)max_jobs_total * (sizeof(SJob) + 16) + (size_t)max_chains_total * (sizeof(EwChain) + 16) + 64;
 }
 
 int scc_max_blocks(size_t smem) {
@@ -278,6 +388,23 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
   // the attribute is per function, not per launch: (re)set it for this size
   cudaError_t e = cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (c.cluster) {
+    e = cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kSccThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = blocks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, scc_kernel, c);
+  }
   void* args[] = {const_cast<SccCtx*>(&c)};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scc_kernel), dim3(blocks), dim3(kSccThreads), args,
                                      smem, s);

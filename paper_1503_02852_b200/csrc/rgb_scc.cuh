@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "rgb_types.cuh"
@@ -23,6 +24,7 @@ struct SccCtx {
   int width;                // common width W of every layer the body writes
   const SccBuf* bufs;       // device copies of the plan's buffer / weight tables
   const SccW* wts;
+  int nbufs, nwts;
   float* ws;
   const float* w;
   const float* wt;
@@ -31,11 +33,16 @@ struct SccCtx {
   long long t1, t0, chunk_base;
   int S, cap, hmax, maxd;
   int inj_buf, use_cache;
+  int cluster;              // 1: one thread-block cluster, hardware cluster barrier
   long long wcache_floats;  // per-CTA shared-memory weight cache (0 = read W from global)
+  long long acc_floats;     // per-CTA accumulator staging
+  long long stage_floats;   // per-CTA A-operand staging (0 = read A from global)
+  long long arena_bytes;    // per-CTA template arena
   unsigned* bar;            // [count, generation] of the grid barrier
 };
 
-size_t scc_smem_bytes(int body_len, long long wcache_floats);
+size_t scc_smem_bytes(const SccCtx& c);
+size_t scc_arena_bytes(int max_jobs_total, int max_chains_total);
 int scc_max_blocks(size_t smem);  // co-resident CTAs for a cooperative launch
 cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s);
 
