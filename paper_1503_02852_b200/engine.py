@@ -616,6 +616,48 @@ class Trainer:
         _lib.check(self._lib.rgb_read_loss(self.state._plan.handle, ctypes.byref(v), self._stream()))
         return v.value
 
+    # ---- CUDA-graph replay of whole iterations --------------------------------
+    def enable_graphs(self, exchange=None) -> None:
+        """Capture the iteration once per ring phase and replay it.
+
+        Every kernel argument of an iteration depends on the cursor only
+        through (cursor mod ring capacity) and through differences of frame
+        numbers, so an iteration captured at cursor c is valid at every cursor
+        c + k*cap.  Inputs/targets come from static device buffers
+        (``graph_inputs``); the loss stays on the device (``loss()`` syncs)."""
+        hp = self.cfg.h_prime
+        n_in = self.net.input_layers()[0].size
+        dev = _device()
+        S = self.state.n
+        self.gx = torch.zeros((hp * S, n_in), dtype=DTYPE, device=dev)
+        self.gt = torch.zeros((hp * S,), dtype=torch.int64, device=dev)
+        self._graphs = {}
+        self._exchange = exchange
+        self._cap = self.state.program.layout.cap
+
+    def graph_inputs(self):
+        """(x, targets) device buffers the next graphed step reads."""
+        return self.gx, self.gt
+
+    def step_graphed(self) -> None:
+        """One iteration on (graph_inputs()), replayed from a captured graph."""
+        hp = self.cfg.h_prime
+        if not self._graphs and not getattr(self, "_graph_warm", False):
+            # first call runs eagerly: it builds the tensor maps and SCC plans
+            # (host-synchronous work that must not happen inside a capture)
+            self.step(self.gx, self.gt, self._exchange)
+            self._graph_warm = True
+            return
+        start = self.state.cursor
+        g = self._graphs.get(start % self._cap)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):  # records only; rewinds the host cursor below
+                self.step(self.gx, self.gt, self._exchange)
+            self._graphs[start % self._cap] = g
+        g.replay()
+        _lib.check(self._lib.rgb_plan_set_cursor(self.state._plan.handle, start + hp))
+
     @staticmethod
     def _stream():
         return _stream()

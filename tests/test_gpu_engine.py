@@ -250,6 +250,32 @@ def test_softmax_feeding_other_layers_cannot_backpropagate():
         P.backward_window(net, cg, w, st, P.BpttWindow(2, 2, 2), d)
 
 
+@pytest.mark.parametrize("net_fn,S", [(lambda: P.build_lstm(9, 32, 7), 4),
+                                      (lambda: P.build_stacked_lstm(64, [64, 64], 32), 128),
+                                      (lambda: P.build_custom_graph(8, 16, 6), 2)])
+def test_graph_replay_equals_eager(net_fn, S):
+    """CUDA-graph replay (one graph per ring phase) reproduces eager steps bit for bit."""
+    net = net_fn()
+    cfg = P.TrainConfig(h=8, h_prime=4, lr=0.02, iterations=1)
+    wa, wb = P.Weights.init(net, 3), P.Weights.init(net, 3)
+    ta, tb = P.Trainer(net, wa, S, cfg), P.Trainer(net, wb, S, cfg)
+    tb.enable_graphs()
+    gx, gt = tb.graph_inputs()
+    rng = np.random.default_rng(0)
+    n_in, n_out = net.input_layers()[0].size, net.output_layers()[0].size
+    for _ in range(9):
+        x = torch.tensor(rng.uniform(-1, 1, size=(4 * S, n_in)), dtype=torch.float32, device="cuda")
+        t = torch.tensor(rng.integers(0, n_out, size=4 * S), device="cuda")
+        ta.step(x, t)
+        gx.copy_(x)
+        gt.copy_(t)
+        tb.step_graphed()
+        assert ta.state.cursor == tb.state.cursor
+        assert abs(ta.loss() - tb.loss()) == 0.0
+    assert torch.equal(wa.flat, wb.flat)
+    assert len(tb._graphs) == tb._cap // 4
+
+
 def test_train_loop_matches_oracle_training():
     """train_loop (fused inject + lazy loss) tracks the oracle's SGD run."""
     net = P.build_lstm(6, 12, 6)
