@@ -161,4 +161,136 @@ __device__ __forceinline__ void ew_apply_batch(const EwOp& op, int width, const 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-vectorised form for the tensor-core epilogues: R rows x 4 consecutive
+// units (j % 4 == 0) per thread, every operand moved as one 16-byte access.
+// Valid when width % 4 == 0 and every pointer of the chain is 16-B aligned
+// (chain_vec_ok); per element the arithmetic is exactly ew_apply's.
+
+__device__ __forceinline__ float4 ld4(const float* p, int64_t e) { return *reinterpret_cast<const float4*>(p + e); }
+__device__ __forceinline__ void st4(float* p, int64_t e, float4 v) { *reinterpret_cast<float4*>(p + e) = v; }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 mul4(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+
+__device__ __forceinline__ void ring_store4(float* out, int64_t e, int64_t r, int width, bool is_ring,
+                                            const RingWrite& ring, float4 v) {
+  st4(out, e, v);
+  if (is_ring) {
+    const int64_t moff = ring.frame_rows * width;
+    st4(out, e + (r < ring.split ? moff : -moff), v);
+  }
+}
+
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// true when the whole chain can take the 16-byte path
+__device__ __forceinline__ bool chain_vec_ok(const EwChain& ch, int width) {
+  if (width % 4) return false;
+  for (int k = 0; k < ch.nops; ++k) {
+    const EwOp& o = ch.op[k];
+    bool ok = aligned16(o.out) && aligned16(o.base) && aligned16(o.y) && aligned16(o.inj);
+    for (int i = 0; i < kMaxTerms; ++i) ok = ok && aligned16(o.term[i]);
+    for (int i = 0; i < kMaxRank1; ++i) ok = ok && aligned16(o.r1w[i]);
+    for (int i = 0; i < kMaxFac; ++i) ok = ok && aligned16(o.fac[i]) && aligned16(o.eps[i]);
+    if (!ok) return false;
+  }
+  return true;
+}
+
+template <int R>
+__device__ __forceinline__ void ew_apply_vec(const EwOp& op, int width, const int64_t (&r)[R], int j,
+                                             const bool (&ok)[R], const RingWrite& ring, bool has_acc,
+                                             const float4 (&acc)[R]) {
+  int64_t e[R];
+  float4 v[R], t[R];
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < R; ++u) e[u] = r[u] * width + j;
+  const int kind = op.kind;
+  if (kind == EW_CONST1) {
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, make_float4(1.f, 1.f, 1.f, 1.f));
+    return;
+  }
+  if (kind == EW_FWD_MUL) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = ok[u] ? ld4(op.fac[0], e[u]) : zero;
+    for (int i = 1; i < op.nfac; ++i) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) t[u] = ok[u] ? ld4(op.fac[i], e[u]) : zero;
+#pragma unroll
+      for (int u = 0; u < R; ++u) v[u] = mul4(v[u], t[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) v[u] = has_acc ? acc[u] : ((op.base && ok[u]) ? ld4(op.base, e[u]) : zero);
+  for (int i = 0; i < op.nterm; ++i) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) t[u] = ok[u] ? ld4(op.term[i], e[u]) : zero;
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = add4(v[u], t[u]);
+  }
+  if (kind == EW_FWD_ADD) {
+    for (int i = 0; i < op.nrank1; ++i) {
+      const float4 w = ld4(op.r1w[i], j);
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const float s = ok[u] ? op.r1src[i][r[u]] : 0.0f;
+        v[u] = add4(v[u], make_float4(w.x * s, w.y * s, w.z * s, w.w * s));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const float4 a = make_float4(act_apply(op.act, v[u].x), act_apply(op.act, v[u].y),
+                                   act_apply(op.act, v[u].z), act_apply(op.act, v[u].w));
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, a);
+    }
+    return;
+  }
+  // EW_BWD
+  if (op.act == ACT_SIGMOID || op.act == ACT_TANH) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) t[u] = ok[u] ? ld4(op.y, e[u]) : zero;
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      v[u] = mul4(v[u], make_float4(act_deriv(op.act, t[u].x), act_deriv(op.act, t[u].y),
+                                    act_deriv(op.act, t[u].z), act_deriv(op.act, t[u].w)));
+  }
+  if (op.inj) {
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      t[u] = (ok[u] && r[u] >= op.inj_row0) ? ld4(op.inj, (r[u] - op.inj_row0) * width + j) : zero;
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = add4(v[u], t[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u)
+    if (ok[u]) st4(op.out, e[u], v[u]);
+  if (op.nfac == 0) return;
+  float4 f[kMaxFac][R];
+  const float4 one = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) f[i][u] = (i < op.nfac && ok[u]) ? ld4(op.fac[i], e[u]) : one;
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+    if (i >= op.nfac || !op.eps[i]) continue;
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      float4 p = v[u];
+#pragma unroll
+      for (int k = 0; k < kMaxFac; ++k)
+        if (k != i) p = mul4(p, f[k][u]);
+      if (ok[u]) st4(op.eps[i], e[u], p);
+    }
+  }
+}
+
 }  // namespace rgb

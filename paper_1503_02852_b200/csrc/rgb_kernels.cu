@@ -9,7 +9,13 @@ namespace rgb {
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ EwLaunch p) {
-  const EwChain& ch = p.chain[blockIdx.y];
+  // chain staged in shared memory: per-element indexed reads of the parameter
+  // block miss the constant cache (see rgb_tc_gemm.cu kChainBytes)
+  __shared__ __align__(16) int chain_words[sizeof(EwChain) / 4];
+  const int* src = reinterpret_cast<const int*>(&p.chain[blockIdx.y]);
+  for (int i = threadIdx.x; i < (int)(sizeof(EwChain) / 4); i += blockDim.x) chain_words[i] = src[i];
+  __syncthreads();
+  const EwChain& ch = *reinterpret_cast<const EwChain*>(chain_words);
   const int64_t total = (int64_t)p.rows * ch.width;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / ch.width;
@@ -43,9 +49,16 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
 __global__ void __launch_bounds__(256) gemm_nt_kernel(const __grid_constant__ GemmGroup p) {
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][BN + 4];
+  __shared__ __align__(16) int chain_words[sizeof(EwChain) / 4];
   int jid, tile;
   find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
   const GemmJob& job = p.job[jid];
+  {
+    const int* src = reinterpret_cast<const int*>(&job.epi);
+    for (int i = threadIdx.x; i < (int)(sizeof(EwChain) / 4); i += blockDim.x) chain_words[i] = src[i];
+  }
+  const EwChain& epi = *reinterpret_cast<const EwChain*>(chain_words);
+  const RingWrite ring = p.ring;
   const int tm = tile / p.tiles_n[jid], tn = tile % p.tiles_n[jid];
   const int m0 = tm * BM, n0 = tn * BN;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -90,7 +103,7 @@ __global__ void __launch_bounds__(256) gemm_nt_kernel(const __grid_constant__ Ge
     for (int j = 0; j < 4; ++j) {
       const int c = n0 + tx * 4 + j;
       if (c >= job.n) continue;
-      for (int k = 0; k < job.epi.nops; ++k) ew_apply(job.epi.op[k], job.n, r, c, p.ring, k == 0, acc[i][j]);
+      for (int k = 0; k < epi.nops; ++k) ew_apply(epi.op[k], job.n, r, c, ring, k == 0, acc[i][j]);
     }
   }
 }

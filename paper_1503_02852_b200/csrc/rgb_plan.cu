@@ -121,10 +121,13 @@ bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width
   if (!enc || width % 4 || reinterpret_cast<uintptr_t>(base) % 16 || rows == 0) return false;
   cuuint64_t dims[2] = {width, rows};
   cuuint64_t strides[1] = {width * 4};
-  cuuint32_t box[2] = {32, box_rows};
+  // K-major (NT GEMM) boxes are kTmaNtBk fp32 wide (rgb_types.cuh); MN-major
+  // (dW) boxes are 32 fp32 = 128 B wide (128B swizzle, 32-B atoms)
+  cuuint32_t box[2] = {mn_major ? 32u : (uint32_t)kTmaNtBk, box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                      : (kTmaNtBk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -768,6 +771,45 @@ int rgb_gemm_nt(const float* a, const float* b, float* c, int m, int n, int k, i
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (mode == 2) launch_tc_gemm_nt(G, st);
   else launch_gemm_nt(G, st);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+}
+
+// TMA-fed tcgen05 NT GEMM on raw matrices: C[m,n] = A[m,k] . B[n,k]^T with the
+// residual B_lo = B - trunc_tf32(B) supplied by the caller (as the SGD kernel
+// maintains it for weights).  Tensor maps are encoded per call (test/tuning hook).
+int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c, int m, int n, int k, void* stream) {
+  if (!a || !b || !b_lo || !c || m < 1 || n < 1 || k < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
+  static CUtensorMap* dmaps = nullptr;
+  static const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  static int64_t kshape[3] = {0, 0, 0};
+  if (!dmaps && cudaMalloc(&dmaps, 3 * sizeof(CUtensorMap)) != cudaSuccess) return fail(RGB_ERR_CUDA, "alloc");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (key[0] != a || key[1] != b || key[2] != b_lo || kshape[0] != m || kshape[1] != n || kshape[2] != k) {
+    // maps are re-encoded only when the operands change, so a timing loop
+    // over one problem measures the kernel alone
+    CUtensorMap hm[3];
+    if (!encode_map(&hm[0], a, m, k, 128) || !encode_map(&hm[1], b, n, k, 32) || !encode_map(&hm[2], b_lo, n, k, 32))
+      return fail(RGB_ERR_KERNEL, "operands not TMA-compatible (k %% 4, 16-B alignment)");
+    if (cudaMemcpy(dmaps, hm, sizeof hm, cudaMemcpyHostToDevice) != cudaSuccess) return fail(RGB_ERR_CUDA, "map upload");
+    key[0] = a, key[1] = b, key[2] = b_lo;
+    kshape[0] = m, kshape[1] = n, kshape[2] = k;
+  }
+  GemmGroup G;
+  std::memset(&G, 0, sizeof G);
+  G.njobs = 1;
+  G.rows = m;
+  G.tma = 1;
+  GemmJob& jb = G.job[0];
+  jb.nseg = 1;
+  jb.seg[0] = Seg{a, b, dmaps, dmaps + 1, dmaps + 2, 0, k};
+  jb.n = n;
+  jb.epi.width = n;
+  jb.epi.nops = 1;
+  jb.epi.op[0].kind = EW_FWD_ADD;
+  jb.epi.op[0].out = c;
+  launch_tc_gemm_nt(G, st);
   note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));

@@ -27,12 +27,32 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "rgb_ew.cuh"
 #include "rgb_kernels.cuh"
 
 namespace rgb {
 namespace tc {
+
+// tuning aid: per-stage clock64 trace of CTA 0 (tools/build_exp.sh trace -DRGB_EXP_TRACE)
+#ifdef RGB_EXP_TRACE
+__device__ long long g_trace[4][1024];
+__device__ long long g_cta[1024][4];  // globaltimer: start, mainloop done, epilogue done; smid
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_MARK(i) \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta[blockIdx.x][i] = gtimer();
+#define TRACE(row, it) \
+  if (blockIdx.x == 0 && (it) < 1024) g_trace[row][it] = clock64();
+#else
+#define TRACE(row, it)
+#define CTA_MARK(i)
+#endif
+
 
 constexpr int BM = 128;   // UMMA M, cta_group::1
 constexpr int BK = 32;    // fp32 per stage along K: one 128-byte swizzle row
@@ -204,13 +224,26 @@ struct TileLoad {
   }
 };
 
+// The job's elementwise chain is copied from the (large, dynamically indexed)
+// kernel parameter block into shared memory once per CTA: read per element
+// from param space it cost ~0.5 us per 8 elements (indexed constant-cache
+// misses), 40% of a 512x4096x1024 launch (tools/gemm_bench.py trace build).
+constexpr int kChainBytes = 1280;
+static_assert(sizeof(EwChain) <= kChainBytes, "chain staging slot");
+
+__device__ __forceinline__ void stage_chain(EwChain* dst, const EwChain& src, int tid, int nthreads) {
+  const int* s = reinterpret_cast<const int*>(&src);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int i = tid; i < (int)(sizeof(EwChain) / 4); i += nthreads) d[i] = s[i];
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int STAGES = BN == 256 ? 2 : (BN == 128 ? 3 : (BN == 64 ? 4 : 5));
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kChainBytes;
   static constexpr int EPI_LD = BN + 4;  // padded staging row (conflict-free 16-B stores)
   static_assert(BM * EPI_LD * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit in the pipeline smem");
 };
@@ -229,11 +262,12 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
 //     at a time, gathering every operand of an op for all U before storing.
 template <int BN, bool IS_DW, class P>
 __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, int M, int N, uint32_t tmem,
-                                         float* tile_s, int tid) {
+                                         float* tile_s, const EwChain* chain_s, int tid) {
   using C = Cfg<BN>;
   const int warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int r_loc = quarter * 32 + lane;
+#ifndef RGB_EXP_NOEPI1
   for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
     if (n0 + cc >= N) break;  // warp-uniform
     float v[16];
@@ -244,11 +278,65 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     dst[2] = make_float4(v[8], v[9], v[10], v[11]);
     dst[3] = make_float4(v[12], v[13], v[14], v[15]);
   }
+#endif
   asm volatile("bar.sync 1, 256;" ::: "memory");
+#ifdef RGB_EXP_NOEPI2
+  return;
+#endif
   const int ncols = (N - n0) < BN ? (N - n0) : BN;
   const int nrows = (M - m0) < BM ? (M - m0) : BM;
   const int total = ncols * nrows;
   constexpr int U = 8;
+  float* g_out = nullptr;
+  float alpha = 0.0f;
+  RingWrite ring{};
+  bool vec;
+  if constexpr (IS_DW) {
+    g_out = p.job[jid].g;
+    alpha = p.alpha;
+    vec = N % 4 == 0 && aligned16(g_out);
+  } else {
+    ring = p.ring;
+    vec = chain_vec_ok(*chain_s, N);
+  }
+  if (vec) {
+    // warp-per-row walk: LPR lanes cover one row with 16-byte accesses, each
+    // thread takes R = 2 rows per pass (fully coalesced, no index division)
+    constexpr int LPR = BN >= 128 ? 32 : BN / 4;  // lanes per row
+    constexpr int RPW = 32 / LPR;                  // rows per warp access
+    constexpr int CG = BN / 4 / LPR;               // float4 groups per lane per row
+    constexpr int R = 2;
+    const int sub = lane / LPR, lc = lane % LPR;
+#pragma unroll 1
+    for (int rb = warp * RPW + sub; rb < nrows; rb += 8 * RPW * R) {
+#pragma unroll
+      for (int g = 0; g < CG; ++g) {
+        const int cl = (g * LPR + lc) * 4;
+        if (cl >= ncols) continue;
+        int64_t rr[R];
+        bool ok[R];
+        float4 acc[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const int rl = rb + u * 8 * RPW;
+          ok[u] = rl < nrows;
+          rr[u] = m0 + (ok[u] ? rl : 0);
+          acc[u] = *reinterpret_cast<const float4*>(tile_s + (ok[u] ? rl : 0) * C::EPI_LD + cl);
+        }
+        if constexpr (IS_DW) {
+#pragma unroll
+          for (int u = 0; u < R; ++u)
+            if (ok[u])
+              st4(g_out, rr[u] * N + n0 + cl,
+                  make_float4(alpha * acc[u].x, alpha * acc[u].y, alpha * acc[u].z, alpha * acc[u].w));
+        } else {
+          const EwChain& epi = *chain_s;
+          for (int k = 0; k < epi.nops; ++k) ew_apply_vec<R>(epi.op[k], N, rr, n0 + cl, ok, ring, k == 0, acc);
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int base = 0; base < total; base += 256 * U) {
     int64_t rr[U];
@@ -267,10 +355,19 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     if constexpr (IS_DW) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (ok[u]) p.job[jid].g[rr[u] * N + cc[u]] = p.alpha * acc[u];
+        if (ok[u]) g_out[rr[u] * N + cc[u]] = alpha * acc[u];
     } else {
-      const auto& epi = p.job[jid].epi;
-      for (int k = 0; k < epi.nops; ++k) ew_apply_batch<U>(epi.op[k], N, rr, cc, ok, p.ring, k == 0, acc);
+      const EwChain& epi = *chain_s;
+#if defined(RGB_EXP_PLAINSTORE)
+      float* o = epi.op[0].out;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) o[rr[u] * N + cc[u]] = acc[u];
+#elif defined(RGB_EXP_NOSTORE)
+      if (acc[0] == 12345.f) epi.op[0].out[0] = acc[1];
+#else
+      for (int k = 0; k < epi.nops; ++k) ew_apply_batch<U>(epi.op[k], N, rr, cc, ok, ring, k == 0, acc);
+#endif
     }
   }
 }
@@ -289,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint64_t* empty = full + C::STAGES;
   uint64_t* done = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int jid, tile;
@@ -320,6 +418,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if constexpr (!IS_DW) {
+    if (threadIdx.x < 256) stage_chain(chain_s, p.job[jid].epi, threadIdx.x, 256);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -390,10 +491,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   // ---------------- epilogue (warps 0-7) ----------------
   if (warp < 8) {
     mbar_wait(done, 0);
+    if (threadIdx.x == 0) { TRACE(3, 0) }
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // all MMAs are complete: the pipeline smem is free for the staging tile
-    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -414,9 +516,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 constexpr int kTmaThreads = 320;  // warps 0-7 convert + epilogue, 8 TMA, 9 MMA
 constexpr int kBoxB = 32;         // weight maps are cut in 32-row boxes (BN / 32 loads per operand)
 
+// Pipeline of the TMA kernel.  NT stages are 16 fp32 deep along K (64-byte
+// rows, SWIZZLE_64B) so that 4-8 stages fit in shared memory and the TMA
+// latency is covered; with 32-deep stages only 2 fit at BN=256 and every
+// stage waited on its load (measured: 2.4 us per stage vs 0.8 us of MMA).
+template <int BN, int BKT>
+struct TCfg {
+  static constexpr int BK = BKT;
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  static constexpr int RAW = 196608 / STAGE_BYTES;
+  static constexpr int STAGES = RAW > 8 ? 8 : (RAW < 2 ? 2 : RAW);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kChainBytes;
+  static_assert(BM * (BN + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit in the pipeline smem");
+};
+
 template <int BN, bool IS_DW, class P>
 __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ P p) {
-  using C = Cfg<BN>;
+  using C = TCfg<BN, IS_DW ? 32 : kTmaNtBk>;
+  constexpr int BK = C::BK;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SWIZZLE_128B); offset arithmetic keeps the pointer in the
   // shared window so the compiler emits LDS/STS rather than generic LD/ST
@@ -426,8 +545,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   uint64_t* empty = conv_full + C::STAGES;
   uint64_t* done = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CTA_MARK(0)
   int jid, tile;
   find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
   const auto& job = p.job[jid];
@@ -459,6 +580,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
                  "r"(BN < 32 ? 32 : BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if constexpr (!IS_DW) {
+    if (threadIdx.x < 256) stage_chain(chain_s, p.job[jid].epi, threadIdx.x, 256);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -471,6 +595,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+        TRACE(0, it)
         uint8_t* base = smem + s * C::STAGE_BYTES;
         if constexpr (IS_DW) {
           // MN-contiguous E [K x M] and Y [K x N]: boxes {32 mn, 32 k}, 4 KB each
@@ -484,14 +609,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
           k0 += BK;
         } else {
           const Seg& sg = job.seg[seg];
-          mbar_expect_tx(&tma_full[s], C::A_BYTES + 2 * C::B_BYTES);
+          // raw fp32 A and B only; both residuals are formed in shared memory
+          // by the converter warps (loading a precomputed W_lo would add 40% to
+          // the TMA bytes of every stage, and these GEMMs are L2-bandwidth bound)
+          mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
           tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
 #pragma unroll
-          for (int b = 0; b < BN / kBoxB; ++b) {
-            tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * 128, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
-            tma_load_2d(base + 2 * C::A_BYTES + C::B_BYTES + b * kBoxB * 128, sg.tblo, k0, n0 + b * kBoxB,
-                        &tma_full[s]);
-          }
+          for (int b = 0; b < BN / kBoxB; ++b)
+            tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * BK * 4, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
           k0 += BK;
           if (k0 >= sg.k) {
             k0 = 0;
@@ -508,6 +633,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
+        TRACE(2, it)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
@@ -524,16 +650,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
             dbh = smem_desc(b_hi + off, 4096, 512, 1);
             dbl = smem_desc(b_lo + off, 4096, 512, 1);
           } else {
+            // K-major SWIZZLE_128B (BK 32: 128-byte rows, 8-row groups 1 KB
+            // apart) or SWIZZLE_64B (BK 16: 64-byte rows, groups 512 B apart);
+            // the j-th 8-deep k-step starts 32 B into each row
+            constexpr uint32_t sbo = BK * 32, lay = BK == 32 ? 2 : 4;
             const uint32_t off = j * 32;
-            dah = smem_desc(a_hi + off, 16, 1024);
-            dal = smem_desc(a_lo + off, 16, 1024);
-            dbh = smem_desc(b_hi + off, 16, 1024);
-            dbl = smem_desc(b_lo + off, 16, 1024);
+            dah = smem_desc(a_hi + off, 16, sbo, lay);
+            dal = smem_desc(a_lo + off, 16, sbo, lay);
+            dbh = smem_desc(b_hi + off, 16, sbo, lay);
+            dbl = smem_desc(b_lo + off, 16, sbo, lay);
           }
           const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+#ifndef RGB_EXP_ONEMMA
           mma_tf32(tmem, dal, dbh, idesc, acc0);
           mma_tf32(tmem, dah, dbl, idesc, 1u);
           mma_tf32(tmem, dah, dbh, idesc, 1u);
+#else
+          mma_tf32(tmem, dah, dbh, idesc, acc0);
+#endif
         }
         mma_commit(&empty[s]);
       }
@@ -544,7 +678,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
       mbar_wait(&tma_full[s], (it / C::STAGES) & 1);
+      if (threadIdx.x == 0) { TRACE(1, it) }
       uint8_t* base = smem + s * C::STAGE_BYTES;
+#ifndef RGB_EXP_NOCONV
       const float4* a_hi = reinterpret_cast<const float4*>(base);
       float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
@@ -553,7 +689,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         const float4 x = a_hi[q];
         a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
       }
-      if constexpr (IS_DW) {  // both dW operands are activations: split B too
+      {  // B residual (weights for the NT form, activations for dW)
         const float4* b_hi = reinterpret_cast<const float4*>(base + 2 * C::A_BYTES);
         float4* b_lo = reinterpret_cast<float4*>(base + 2 * C::A_BYTES + C::B_BYTES);
         for (int q = threadIdx.x; q < C::B_BYTES / 16; q += kProducers) {
@@ -562,13 +698,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
       mbar_arrive(&conv_full[s]);
     }
     // ---------------- epilogue ----------------
     mbar_wait(done, 0);
+    if (threadIdx.x == 0) { TRACE(3, 0) }
+    CTA_MARK(1)
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), threadIdx.x);
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x);
+    CTA_MARK(2)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -590,18 +730,25 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 
 template <int BN, bool IS_DW, class P>
 void launch_tma(const P& p, int tiles, cudaStream_t s) {
+  using C = TCfg<BN, IS_DW ? 32 : kTmaNtBk>;
   static bool configured = false;
   auto k = tma_gemm_kernel<BN, IS_DW, P>;
   if (!configured) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
-  k<<<tiles, kTmaThreads, Cfg<BN>::SMEM, s>>>(p);
+  k<<<tiles, kTmaThreads, C::SMEM, s>>>(p);
 }
 
 // Widest N tile that still gives most of the 148 SMs a tile.
 template <class F>
 int pick_bn(F tiles_for) {
+  static int forced = -1;  // RGB_TC_BN: tile-width override for tuning experiments
+  if (forced < 0) {
+    const char* e = getenv("RGB_TC_BN");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 32 || forced == 64 || forced == 128 || forced == 256) return forced;
   for (int bn : {256, 128, 64})
     if (tiles_for(bn) >= 120) return bn;
   return 32;
@@ -664,3 +811,12 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
 }
 
 }  // namespace rgb
+
+#ifdef RGB_EXP_TRACE
+extern "C" int rgb_exp_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, rgb::tc::g_trace, sizeof(rgb::tc::g_trace)) == cudaSuccess ? 0 : 3;
+}
+extern "C" int rgb_exp_cta(long long* out) {
+  return cudaMemcpyFromSymbol(out, rgb::tc::g_cta, sizeof(rgb::tc::g_cta)) == cudaSuccess ? 0 : 3;
+}
+#endif

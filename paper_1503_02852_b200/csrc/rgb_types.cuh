@@ -24,6 +24,13 @@ enum EwKind : int {
 constexpr int kMaxTerms = 4;
 constexpr int kMaxRank1 = 3;
 constexpr int kMaxFac = 4;
+// K depth (fp32) of one TMA stage of the NT tensor-core GEMM: 32 = 128-byte
+// rows with SWIZZLE_128B, 16 = 64-byte rows with SWIZZLE_64B.  The tensor
+// maps (rgb_plan.cu encode_map) and the UMMA descriptors follow it.
+#ifndef RGB_TMA_NT_BK
+#define RGB_TMA_NT_BK 32
+#endif
+constexpr int kTmaNtBk = RGB_TMA_NT_BK;
 constexpr int kMaxChain = 6;
 constexpr int kMaxSegs = 4;
 constexpr int kMaxJobs = 8;
