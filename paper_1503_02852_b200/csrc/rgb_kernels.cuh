@@ -32,7 +32,10 @@ void launch_gemm_nt(const GemmGroup& p, cudaStream_t s);
 void launch_gemm_dw(const DwGroup& p, cudaStream_t s);
 // tcgen05 (3xTF32, TMEM accumulator) versions of the two GEMM forms; same
 // descriptors, tiles recomputed for 128 x {64,128,256} (rgb_tc_gemm.cu).
-void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s);
+// returns the number of kernels launched (2 with split-K: GEMM + fixup/epilogue)
+int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s);
+// split-K scratch (floats) the TMA NT kernel would use for this group (0 = no split)
+long long tc_gemm_nt_scratch(const GemmGroup& p);
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s);
 void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.

@@ -168,7 +168,34 @@ struct rgb_plan {
   };
   std::map<std::pair<int, int64_t>, SccPlan> scc_plans;
 
+  // split-K scratch of the TMA GEMM (tc_gemm_nt_scratch): grown on demand
+  // outside stream capture; a captured launch that would need more falls back
+  // to the unsplit configuration (launch_tc_gemm_nt checks the capacity)
+  float* part = nullptr;
+  long long part_cap = 0;
+
+  int splitk_scratch(GemmGroup& G, cudaStream_t st) {
+    const long long need = tc_gemm_nt_scratch(G);
+    if (need > part_cap) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs == cudaStreamCaptureStatusNone) {
+        if (cudaStreamSynchronize(st) != cudaSuccess) return fail(RGB_ERR_CUDA, "split-K scratch sync");
+        if (part) cudaFree(part);
+        part = nullptr;
+        part_cap = 0;
+        if (cudaMalloc(&part, need * 4) != cudaSuccess)
+          return fail(RGB_ERR_CUDA, "split-K scratch allocation (%lld floats)", need);
+        part_cap = need;
+      }
+    }
+    G.part = part;
+    G.part_cap = part_cap;
+    return RGB_OK;
+  }
+
   ~rgb_plan() {
+    if (part) cudaFree(part);
     if (maps_dev) cudaFree(maps_dev);
     for (auto* q : prog_dev)
       if (q) cudaFree(q);
@@ -568,10 +595,13 @@ struct rgb_plan {
           flops += 2.0 * G.rows * G.job[j].n * (double)ksum;
           bytes += 4.0 * ((double)G.rows * ksum + (double)G.job[j].n * ksum) + ew_bytes(G.job[j].epi, G.rows);
         }
+        const bool tc = use_tc(flops);
+        if (tc && G.tma && (rc = splitk_scratch(G, st))) return rc;
         const int slot = prof_start(st);
-        if (use_tc(flops)) launch_tc_gemm_nt(G, st);
+        int nl = 1;
+        if (tc) nl = launch_tc_gemm_nt(G, st);
         else launch_gemm_nt(G, st);
-        note_launch();
+        for (int q = 0; q < nl; ++q) note_launch();
         prof_stop(slot, st, c.in_loop ? PROF_GEMM_FRAME : PROF_GEMM, flops, bytes);
       } else if (kind == STEP_SOFTMAX) {
         const int b = rd.next();
@@ -809,8 +839,19 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
   jb.epi.nops = 1;
   jb.epi.op[0].kind = EW_FWD_ADD;
   jb.epi.op[0].out = c;
-  launch_tc_gemm_nt(G, st);
-  note_launch();
+  static float* part = nullptr;
+  static long long part_cap = 0;
+  const long long need = tc_gemm_nt_scratch(G);
+  if (need > part_cap) {
+    cudaStreamSynchronize(st);
+    if (part) cudaFree(part);
+    if (cudaMalloc(&part, need * 4) != cudaSuccess) return fail(RGB_ERR_CUDA, "split-K scratch");
+    part_cap = need;
+  }
+  G.part = part;
+  G.part_cap = part_cap;
+  const int nl = launch_tc_gemm_nt(G, st);
+  for (int q = 0; q < nl; ++q) note_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
 }

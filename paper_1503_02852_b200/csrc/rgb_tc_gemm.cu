@@ -26,6 +26,7 @@
 // hand-written.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -262,7 +263,8 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
 //     at a time, gathering every operand of an op for all U before storing.
 template <int BN, bool IS_DW, class P>
 __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, int M, int N, uint32_t tmem,
-                                         float* tile_s, const EwChain* chain_s, int tid) {
+                                         float* tile_s, const EwChain* chain_s, int tid, int tile_lin, int split,
+                                         int splits) {
   using C = Cfg<BN>;
   const int warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
@@ -283,6 +285,20 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
 #ifdef RGB_EXP_NOEPI2
   return;
 #endif
+  if constexpr (!IS_DW) {
+    if (splits > 1) {
+      // split-K: publish this partial tile and stop; splitk_epilogue_kernel
+      // sums the partials in split order (deterministic) and runs the chain
+      // with every SM taking part
+      constexpr int Q = BM * BN / 4;
+      float* part = p.part + ((size_t)tile_lin * splits + split) * (BM * BN);
+      for (int q = tid; q < Q; q += 256) {
+        const int r = q / (BN / 4), c = (q % (BN / 4)) * 4;
+        st4(part, r * BN + c, *reinterpret_cast<const float4*>(tile_s + r * C::EPI_LD + c));
+      }
+      return;
+    }
+  }
   const int ncols = (N - n0) < BN ? (N - n0) : BN;
   const int nrows = (M - m0) < BM ? (M - m0) : BM;
   const int total = ncols * nrows;
@@ -495,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // all MMAs are complete: the pipeline smem is free for the staging tile
-    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x);
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x, 0, 0, 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -550,7 +566,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CTA_MARK(0)
   int jid, tile;
-  find_job(p.tile_start, p.njobs, blockIdx.x, jid, tile);
+  // split-K (NT only): the splits of one output tile are adjacent blocks
+  int splits = 1, split = 0, tile_lin = blockIdx.x;
+  if constexpr (!IS_DW) {
+    splits = p.splits > 1 ? p.splits : 1;
+    split = blockIdx.x % splits;
+    tile_lin = blockIdx.x / splits;
+  }
+  find_job(p.tile_start, p.njobs, tile_lin, jid, tile);
   const auto& job = p.job[jid];
   const int tiles_n = p.tiles_n[jid];
   const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
@@ -565,6 +588,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     nstages = 0;
     for (int s = 0; s < job.nseg; ++s) nstages += (job.seg[s].k + BK - 1) / BK;
   }
+  // this block's K-stage range [s_begin, s_begin + nstages)
+  const int s_begin = (int)((long long)split * nstages / splits);
+  nstages = (int)((long long)(split + 1) * nstages / splits) - s_begin;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -592,6 +618,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int seg = 0, k0 = 0;
+      if constexpr (!IS_DW) {
+        for (int skip = s_begin; skip > 0;) {  // locate the first stage of this split
+          const int ns = (job.seg[seg].k + BK - 1) / BK;
+          if (skip >= ns) {
+            skip -= ns;
+            ++seg;
+          } else {
+            k0 = skip * BK;
+            skip = 0;
+          }
+        }
+      }
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
@@ -707,7 +745,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     CTA_MARK(1)
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x);
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x, tile_lin,
+                        split, splits);
     CTA_MARK(2)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -740,6 +779,47 @@ void launch_tma(const P& p, int tiles, cudaStream_t s) {
   k<<<tiles, kTmaThreads, C::SMEM, s>>>(p);
 }
 
+// Split-K fixup + epilogue: acc = sum of the partial tiles in split order,
+// then the job's chain; one thread per 4 consecutive units of a row
+// (blockIdx.y = job).
+template <int BN>
+__global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_constant__ GemmGroup p) {
+  __shared__ __align__(16) int chain_words[sizeof(EwChain) / 4];
+  const int j = blockIdx.y;
+  stage_chain(reinterpret_cast<EwChain*>(chain_words), p.job[j].epi, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const EwChain& ch = *reinterpret_cast<const EwChain*>(chain_words);
+  const int N = p.job[j].n, M = p.rows, splits = p.splits, tiles_n = p.tiles_n[j], t0 = p.tile_start[j];
+  const RingWrite ring = p.ring;
+  const size_t tile_floats = (size_t)BM * BN;
+  if (chain_vec_ok(ch, N)) {
+    const int64_t nq = (int64_t)M * (N / 4);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = q / (N / 4);
+      const int c = (int)(q - r * (N / 4)) * 4;
+      const int tl = t0 + (int)(r / BM) * tiles_n + c / BN;
+      const float* src = p.part + (size_t)tl * splits * tile_floats + (r % BM) * BN + (c % BN);
+      float4 a = __ldcg(reinterpret_cast<const float4*>(src));
+      for (int sp = 1; sp < splits; ++sp) a = add4(a, __ldcg(reinterpret_cast<const float4*>(src + sp * tile_floats)));
+      const int64_t rr[1] = {r};
+      const bool ok[1] = {true};
+      const float4 acc[1] = {a};
+      for (int k = 0; k < ch.nops; ++k) ew_apply_vec<1>(ch.op[k], N, rr, c, ok, ring, k == 0, acc);
+    }
+  } else {
+    const int64_t ne = (int64_t)M * N;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = e / N;
+      const int c = (int)(e - r * N);
+      const int tl = t0 + (int)(r / BM) * tiles_n + c / BN;
+      const float* src = p.part + (size_t)tl * splits * tile_floats + (r % BM) * BN + (c % BN);
+      float a = __ldcg(src);
+      for (int sp = 1; sp < splits; ++sp) a += __ldcg(src + sp * tile_floats);
+      for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], N, r, c, ring, k == 0, a);
+    }
+  }
+}
+
 // Widest N tile that still gives most of the 148 SMs a tile.
 template <class F>
 int pick_bn(F tiles_for) {
@@ -756,20 +836,68 @@ int pick_bn(F tiles_for) {
 
 }  // namespace tc
 
-void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
-  auto tiles_for = [&](int bn) {
-    int t = 0;
-    for (int j = 0; j < p.njobs; ++j) t += ((p.rows + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
-    return t;
-  };
-  const int bn = tc::pick_bn(tiles_for);
+namespace {
+
+int nt_tiles(const GemmGroup& p, int bn) {
+  int t = 0;
+  for (int j = 0; j < p.njobs; ++j) t += ((p.rows + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
+  return t;
+}
+
+// Tile width and split-K factor of a TMA NT launch.  Narrow tiles (BN <= 64,
+// chosen because there are few output tiles) re-read the A operand once per
+// tile column and convert it again each time; when K is deep, 128-wide tiles
+// split along K over up to 4 blocks keep every SM busy with half the
+// operand traffic per flop (512x1024x4096: 76 -> ~35 us).
+void nt_config(const GemmGroup& p, int& bn, int& splits) {
+  bn = tc::pick_bn([&](int b) { return nt_tiles(p, b); });
+  splits = 1;
+  static int split_env = -2;  // RGB_TC_SPLIT=0 disables split-K (tuning experiments)
+  if (split_env == -2) {
+    const char* e = getenv("RGB_TC_SPLIT");
+    split_env = e ? atoi(e) : -1;
+  }
+  if (!p.tma || bn >= 128 || getenv("RGB_TC_BN") || split_env == 0) return;
+  int kst = 1 << 30;
+  for (int j = 0; j < p.njobs; ++j) {
+    int st = 0;
+    for (int s = 0; s < p.job[j].nseg; ++s) st += (p.job[j].seg[s].k + kTmaNtBk - 1) / kTmaNtBk;
+    kst = st < kst ? st : kst;
+  }
+  const int t128 = nt_tiles(p, 128);
+  int sp = 148 / (t128 > 0 ? t128 : 1);
+  sp = sp > 4 ? 4 : sp;
+  while (sp > 1 && kst / sp < 8) --sp;  // at least 8 K-stages per split
+  if (sp > 1) {
+    bn = 128;
+    splits = sp;
+  }
+}
+
+}  // namespace
+
+long long tc_gemm_nt_scratch(const GemmGroup& p) {
+  int bn, splits;
+  nt_config(p, bn, splits);
+  return splits > 1 ? (long long)nt_tiles(p, bn) * splits * tc::BM * bn : 0;
+}
+
+int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
+  int bn, splits;
+  nt_config(p, bn, splits);
+  if (splits > 1 && (!p.part || (long long)nt_tiles(p, bn) * splits * tc::BM * bn > p.part_cap)) {
+    // no (or too small a) scratch: fall back to the unsplit configuration
+    bn = tc::pick_bn([&](int b) { return nt_tiles(p, b); });
+    splits = 1;
+  }
+  p.splits = splits;
   p.tile_start[0] = 0;
   for (int j = 0; j < p.njobs; ++j) {
     p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
     p.tile_start[j + 1] = p.tile_start[j] + ((p.rows + tc::BM - 1) / tc::BM) * p.tiles_n[j];
   }
-  const int tiles = p.tile_start[p.njobs];
-  if (tiles == 0) return;
+  const int tiles = p.tile_start[p.njobs] * splits;
+  if (tiles == 0) return 0;
   if (p.tma) {
     if (bn == 256) tc::launch_tma<256, false>(p, tiles, s);
     else if (bn == 128) tc::launch_tma<128, false>(p, tiles, s);
@@ -781,6 +909,15 @@ void launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
     else if (bn == 64) tc::launch_one<64, false>(p, tiles, s);
     else tc::launch_one<32, false>(p, tiles, s);
   }
+  if (splits == 1) return 1;
+  int64_t maxq = 0;
+  for (int j = 0; j < p.njobs; ++j) maxq = std::max<int64_t>(maxq, (int64_t)p.rows * p.job[j].n);
+  maxq = (maxq + 3) / 4;
+  int blocks = (int)std::min<int64_t>((maxq + 255) / 256, 148 * 8);
+  blocks = blocks < 1 ? 1 : blocks;
+  // bn == 128 whenever splits > 1 (nt_config)
+  tc::splitk_epilogue_kernel<128><<<dim3(blocks, p.njobs), 256, 0, s>>>(p);
+  return 2;
 }
 
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {

@@ -89,6 +89,11 @@ struct GemmGroup {
   int tiles_n[kMaxJobs];         // tiles along N per job
   RingWrite ring;
   GemmJob job[kMaxJobs];
+  // split-K scratch of the TMA tensor-core kernel (owned by the plan): one
+  // partial tile per (output tile, split).  part == nullptr: no split.
+  float* part;
+  long long part_cap;  // floats
+  int splits;          // set by launch_tc_gemm_nt
 };
 
 struct EwLaunch {

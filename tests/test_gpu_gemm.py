@@ -112,3 +112,32 @@ def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
     assert run_pair(P.build_stacked_lstm(512, [512, 512], 512), 64, 32, 16, 3, 1e-3, 5) < 1e-4
+
+
+TMA_SHAPES = [(512, 4096, 1024),   # 128 tiles of 128, no split
+              (512, 1024, 4096),   # few tiles, deep K: split-K over 4 blocks
+              (384, 512, 2080),    # split-K with a ragged last stage
+              (100, 256, 520),     # partial M tile
+              (256, 96, 64)]       # K too shallow to split
+
+
+@pytest.mark.parametrize("m,n,k", TMA_SHAPES)
+def test_gemm_nt_tma_split(m, n, k):
+    """TMA-fed kernel incl. the split-K path: parity with float64 and bitwise
+    reproducibility (the partial tiles are summed in split order)."""
+    rng = np.random.default_rng(m + 5 * n + 11 * k)
+    a = rng.uniform(-1, 1, size=(m, k))
+    b = rng.uniform(-1, 1, size=(n, k))
+    ta = torch.tensor(a, dtype=torch.float32, device="cuda")
+    tb = torch.tensor(b, dtype=torch.float32, device="cuda")
+    tbl = tb - (tb.view(torch.int32) & ~0x1FFF).view(torch.float32)
+    outs = []
+    for _ in range(3):
+        tc = torch.full((m, n), float("nan"), device="cuda")
+        _lib.check(_lib.lib().rgb_gemm_nt_tma(ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()),
+                                              ctypes.c_void_p(tbl.data_ptr()), ctypes.c_void_p(tc.data_ptr()),
+                                              m, n, k, _stream()))
+        outs.append(tc.cpu().numpy())
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    assert normwise(outs[0], ref) < 1e-5
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
