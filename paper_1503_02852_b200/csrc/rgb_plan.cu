@@ -115,20 +115,35 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // mn_major = true: the same boxes with the 32-byte-atom 128B swizzle that the
 // UMMA SWIZZLE_128B_BASE32B MN-major layout (kind::tf32) expects -- the dW
 // operands, whose contiguous dimension is M or N (tools/tc_probe_mn.cu).
-bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t box_rows,
-                bool mn_major = false) {
+bool encode_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t box_rows) {
   auto enc = tensor_map_encoder();
   if (!enc || width % 4 || reinterpret_cast<uintptr_t>(base) % 16 || rows == 0) return false;
   cuuint64_t dims[2] = {width, rows};
   cuuint64_t strides[1] = {width * 4};
-  // K-major (NT GEMM) boxes are kTmaNtBk fp32 wide (rgb_types.cuh); MN-major
-  // (dW) boxes are 32 fp32 = 128 B wide (128B swizzle, 32-B atoms)
-  cuuint32_t box[2] = {mn_major ? 32u : (uint32_t)kTmaNtBk, box_rows};
+  // K-major boxes are kTmaNtBk fp32 wide (rgb_types.cuh)
+  cuuint32_t box[2] = {(uint32_t)kTmaNtBk, box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                      : (kTmaNtBk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
+             CU_TENSOR_MAP_INTERLEAVE_NONE, kTmaNtBk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// MN-major operand of the dW GEMM (rows = K frames*streams, width = M or N,
+// contiguous): a 3-D view {32 units, K rows, width/32 unit blocks} with
+// boxes {32, 32, blocks} lands `blocks` 4-KB atoms [32 k x 128 B] back to back
+// -- the UMMA SWIZZLE_128B_BASE32B MN-major layout (kind::tf32, LBO 4 KB,
+// tools/tc_probe_mn.cu) -- with ONE TMA instruction per operand and stage.
+// width % 32 == 0 (a partial unit block would read into the next row).
+bool encode_map_mn(CUtensorMap* m, const float* base, uint64_t rows, uint64_t width, uint32_t blocks) {
+  auto enc = tensor_map_encoder();
+  if (!enc || width % 32 || reinterpret_cast<uintptr_t>(base) % 16 || rows == 0) return false;
+  cuuint64_t dims[3] = {32, rows, width / 32};
+  cuuint64_t strides[2] = {width * 4, 128};
+  cuuint32_t box[3] = {32, 32, blocks};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -336,16 +351,22 @@ struct rgb_plan {
 
   int frames_of(int kind) const { return kind == BUF_RING ? 2 * cap : (kind == BUF_WIN ? hmax + maxd : hmax); }
 
-  size_t wmap0() const { return 2 * bufs.size(); }
+  // map table: per buffer one K-major map (NT A operand, 128-row boxes) at
+  // [0, nb) and four MN-major dW maps (1, 2, 4, 8 unit blocks per box) at
+  // nb + 4 b; per dense connection eight K-major weight maps at
+  // wmap0() + 8 cid: W then W^T, each with 32/64/128/256-row boxes (one TMA
+  // instruction loads a whole BN-row operand tile)
+  size_t wmap0() const { return 5 * bufs.size(); }
 
   int build_buffer_maps() {
-    const size_t nb = bufs.size(), total = wmap0() + 4 * wts.size();
+    const size_t nb = bufs.size(), total = wmap0() + 8 * wts.size();
     maps.assign(total, CUtensorMap{});
     map_ok.assign(total, 0);
     for (size_t i = 0; i < nb; ++i) {
       const uint64_t rows = (uint64_t)frames_of(bufs[i].kind) * S;
       map_ok[i] = encode_map(&maps[i], ws + bufs[i].off, rows, bufs[i].width, 128);
-      map_ok[nb + i] = encode_map(&maps[nb + i], ws + bufs[i].off, rows, bufs[i].width, 32, true);
+      for (int q = 0; q < 4; ++q)
+        map_ok[nb + 4 * i + q] = encode_map_mn(&maps[nb + 4 * i + q], ws + bufs[i].off, rows, bufs[i].width, 1u << q);
     }
     if (!maps_dev && cudaMalloc(&maps_dev, total * sizeof(CUtensorMap)) != cudaSuccess)
       return fail(RGB_ERR_CUDA, "tensor-map table allocation failed");
@@ -355,28 +376,32 @@ struct rgb_plan {
     return RGB_OK;
   }
 
-  // (Re)build the weight maps when the caller's W / W^T buffers change.  The
-  // buffers hold [W | W_lo] and [W^T | W^T_lo] (n_params floats each half).
+  bool mn_maps_ok(int b) const {
+    const size_t i = bufs.size() + 4 * (size_t)b;
+    return map_ok[i] && map_ok[i + 1] && map_ok[i + 2] && map_ok[i + 3];
+  }
+  bool w_maps_ok(int cid, bool trans) const {
+    const size_t i = wmap0() + 8 * (size_t)cid + (trans ? 4 : 0);
+    return map_ok[i] && map_ok[i + 1] && map_ok[i + 2] && map_ok[i + 3];
+  }
+
+  // (Re)build the weight maps when the caller's W / W^T buffers change.
   int ensure_weight_maps(const float* w, const float* wt) {
     const bool new_w = w && w != map_w, new_wt = wt && wt != map_wt;
     if (!maps_dev || (!new_w && !new_wt)) return RGB_OK;
     const size_t nb = wmap0();
     for (size_t cid = 0; cid < wts.size(); ++cid) {
       const WDesc& d = wts[cid];
-      char* ok = &map_ok[nb + 4 * cid];
-      CUtensorMap* m = &maps[nb + 4 * cid];
+      char* ok = &map_ok[nb + 8 * cid];
+      CUtensorMap* m = &maps[nb + 8 * cid];
       if (d.rows == 0) continue;
-      if (new_w) {
-        ok[0] = encode_map(&m[0], w + d.off, d.rows, d.cols, 32);
-        ok[1] = encode_map(&m[1], w + n_params + d.off, d.rows, d.cols, 32);
-      }
-      if (new_wt) {
-        ok[2] = encode_map(&m[2], wt + d.off, d.cols, d.rows, 32);
-        ok[3] = encode_map(&m[3], wt + n_params + d.off, d.cols, d.rows, 32);
+      for (int q = 0; q < 4; ++q) {
+        if (new_w) ok[q] = encode_map(&m[q], w + d.off, d.rows, d.cols, 32u << q);
+        if (new_wt) ok[4 + q] = encode_map(&m[4 + q], wt + d.off, d.cols, d.rows, 32u << q);
       }
     }
     // synchronous: the host mirror may be rewritten on the next change
-    if (cudaMemcpy(maps_dev + nb, maps.data() + nb, 4 * wts.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) !=
+    if (cudaMemcpy(maps_dev + nb, maps.data() + nb, 8 * wts.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) !=
         cudaSuccess)
       return fail(RGB_ERR_CUDA, "weight tensor-map upload failed");
     if (new_w) map_w = w;
@@ -571,11 +596,11 @@ struct rgb_plan {
             jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
             jb.seg[s].k = trans ? wd.rows : wd.cols;
             if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
-            const int mi = (int)wmap0() + 4 * cid + (trans ? 2 : 0);
-            if (all_tma && map_ok[ab] && map_ok[mi] && map_ok[mi + 1]) {
+            const int mi = (int)wmap0() + 8 * cid + (trans ? 4 : 0);
+            if (all_tma && map_ok[ab] && w_maps_ok(cid, trans)) {
               jb.seg[s].ta = maps_dev + ab;
               jb.seg[s].tb = maps_dev + mi;
-              jb.seg[s].tblo = maps_dev + mi + 1;
+              jb.seg[s].tblo = nullptr;
               jb.seg[s].arow = (int)((a - (ws + bufs[ab].off)) / bufs[ab].width);
             } else {
               all_tma = false;
@@ -685,9 +710,9 @@ struct rgb_plan {
             return fail(RGB_ERR_KERNEL, "dW shape mismatch (cid %d)", cid);
           D.job[j] = DwJob{e, y, c.g + wd.off, wd.rows, wd.cols, nullptr, nullptr, 0, 0};
           const size_t nb = bufs.size();
-          if (!maps.empty() && map_ok[nb + eb] && map_ok[nb + yb]) {
-            D.job[j].te = maps_dev + nb + eb;
-            D.job[j].ty = maps_dev + nb + yb;
+          if (!maps.empty() && mn_maps_ok(eb) && mn_maps_ok(yb)) {
+            D.job[j].te = maps_dev + nb + 4 * eb;
+            D.job[j].ty = maps_dev + nb + 4 * yb;
             D.job[j].erow = (int)((e - (ws + bufs[eb].off)) / bufs[eb].width);
             D.job[j].yrow = (int)((y - (ws + bufs[yb].off)) / bufs[yb].width);
           }
@@ -814,14 +839,16 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
   static CUtensorMap* dmaps = nullptr;
   static const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
   static int64_t kshape[3] = {0, 0, 0};
-  if (!dmaps && cudaMalloc(&dmaps, 3 * sizeof(CUtensorMap)) != cudaSuccess) return fail(RGB_ERR_CUDA, "alloc");
+  if (!dmaps && cudaMalloc(&dmaps, 5 * sizeof(CUtensorMap)) != cudaSuccess) return fail(RGB_ERR_CUDA, "alloc");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (key[0] != a || key[1] != b || key[2] != b_lo || kshape[0] != m || kshape[1] != n || kshape[2] != k) {
     // maps are re-encoded only when the operands change, so a timing loop
-    // over one problem measures the kernel alone
-    CUtensorMap hm[3];
-    if (!encode_map(&hm[0], a, m, k, 128) || !encode_map(&hm[1], b, n, k, 32) || !encode_map(&hm[2], b_lo, n, k, 32))
-      return fail(RGB_ERR_KERNEL, "operands not TMA-compatible (k %% 4, 16-B alignment)");
+    // over one problem measures the kernel alone (b_lo: kept for the ABI; the
+    // kernel forms the residual in shared memory)
+    CUtensorMap hm[5];
+    bool ok = encode_map(&hm[0], a, m, k, 128);
+    for (int q = 0; q < 4; ++q) ok = ok && encode_map(&hm[1 + q], b, n, k, 32u << q);
+    if (!ok) return fail(RGB_ERR_KERNEL, "operands not TMA-compatible (k %% 4, 16-B alignment)");
     if (cudaMemcpy(dmaps, hm, sizeof hm, cudaMemcpyHostToDevice) != cudaSuccess) return fail(RGB_ERR_CUDA, "map upload");
     key[0] = a, key[1] = b, key[2] = b_lo;
     kshape[0] = m, kshape[1] = n, kshape[2] = k;
@@ -833,7 +860,7 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
   G.tma = 1;
   GemmJob& jb = G.job[0];
   jb.nseg = 1;
-  jb.seg[0] = Seg{a, b, dmaps, dmaps + 1, dmaps + 2, 0, k};
+  jb.seg[0] = Seg{a, b, dmaps, dmaps + 1, nullptr, 0, k};
   jb.n = n;
   jb.epi.width = n;
   jb.epi.nops = 1;

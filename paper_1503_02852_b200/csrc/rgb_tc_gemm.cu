@@ -149,6 +149,20 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, in
       : "memory");
 }
 
+// i-th tensor map of a table (CUtensorMap is 128 bytes; the tables hold plain
+// void pointers so this file does not depend on cuda.h)
+__device__ __forceinline__ const void* map_at(const void* table, int i) {
+  return static_cast<const uint8_t*>(table) + 128 * i;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // tf32 residual of an fp32 value: kind::tf32 consumes only the top 19 bits
 // (it truncates -- measured, tools/tc_probe.cu), so x itself acts as "hi" and
 // lo = x - trunc13(x) is exact in fp32.
@@ -521,26 +535,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------
-// TMA-fed NT GEMM.  Per stage, one thread (warp 8) issues the TMA loads of the
-// raw fp32 A tile (activations; the tensor core truncates it to its tf32 "hi"
-// part) and of the pre-split weight tiles B = W and B_lo = W - trunc(W) (kept
-// by the SGD / W^T-refresh kernels), all with SWIZZLE_128B straight into the
-// UMMA K-major layout; the 8 converter warps only form A_lo = A - trunc(A) in
-// place-aligned smem (same byte offsets, no swizzle arithmetic); one thread of
-// warp 9 issues the three tcgen05.mma per 8-deep k-step.  Three mbarriers per
-// stage: TMA landed -> residual written -> MMAs done (tcgen05.commit).
+// TMA-fed tensor-core GEMM (NT form with the elementwise-chain epilogue, and
+// the dW form).  Warp roles: warp 8 lane 0 issues one TMA load per operand and
+// stage (raw fp32; the tensor core truncates it to its tf32 "hi" part), the 8
+// converter warps form x_lo = x - trunc(x) for both operands at the same byte
+// offsets (the swizzle is position-independent), warp 9 lane 0 issues the
+// three tcgen05.mma per 8-deep k-step.  Three mbarriers per stage: TMA landed
+// -> residuals written -> MMAs done (tcgen05.commit frees the slot).
+//
+// PAIR = true runs a CTA pair (cluster of 2 on one TPC, tcgen05 cta_group::2):
+// the pair computes a 256 x BN tile; each CTA loads and converts its own 128
+// rows of A and HALF of B (BN/2 rows) and holds its 128 accumulator rows in its
+// own TMEM, the leader (rank 0) issues M=256 MMAs that read both CTAs' shared
+// memory.  Per CTA this halves the B bytes written by TMA, converted and read
+// by the tensor core -- the kernel is shared-memory-bandwidth bound
+// (tools/gemm_bench.py trace build: 288 KB of smem traffic per 32-deep stage at
+// 128x256 vs 1536 MMA cycles).
 constexpr int kTmaThreads = 320;  // warps 0-7 convert + epilogue, 8 TMA, 9 MMA
-constexpr int kBoxB = 32;         // weight maps are cut in 32-row boxes (BN / 32 loads per operand)
 
-// Pipeline of the TMA kernel.  NT stages are 16 fp32 deep along K (64-byte
-// rows, SWIZZLE_64B) so that 4-8 stages fit in shared memory and the TMA
-// latency is covered; with 32-deep stages only 2 fit at BN=256 and every
-// stage waited on its load (measured: 2.4 us per stage vs 0.8 us of MMA).
-template <int BN, int BKT>
+template <int BN, int BNL, int BKT>
 struct TCfg {
   static constexpr int BK = BKT;
   static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int B_BYTES = BNL * BK * 4;  // this CTA's B rows
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
   static constexpr int RAW = 196608 / STAGE_BYTES;
   static constexpr int STAGES = RAW > 8 ? 8 : (RAW < 2 ? 2 : RAW);
@@ -548,13 +565,71 @@ struct TCfg {
   static_assert(BM * (BN + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit in the pipeline smem");
 };
 
-template <int BN, bool IS_DW, class P>
+template <int ROWS>
+__host__ __device__ constexpr int box_idx() {  // 32/64/128/256-row map variant
+  return ROWS == 32 ? 0 : (ROWS == 64 ? 1 : (ROWS == 128 ? 2 : 3));
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// arrive on the mbarrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// wait with cluster-scope acquire (arrivals from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// commit to the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN, bool IS_DW, bool PAIR, class P>
 __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ P p) {
-  using C = TCfg<BN, IS_DW ? 32 : kTmaNtBk>;
+  constexpr int NCTA = PAIR ? 2 : 1;
+  constexpr int BNL = BN / NCTA;  // B rows held by this CTA
+  using C = TCfg<BN, BNL, IS_DW ? 32 : kTmaNtBk>;
   constexpr int BK = C::BK;
+  constexpr int kBoxIdx = box_idx<BNL>();
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SWIZZLE_128B); offset arithmetic keeps the pointer in the
-  // shared window so the compiler emits LDS/STS rather than generic LD/ST
+  // shared window so the compiler emits LDS/STS rather than generic LD/ST.
+  // Both CTAs of a pair get the same layout (the leader's MMA descriptors
+  // address the peer's operands at the same offsets).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* conv_full = tma_full + C::STAGES;
@@ -564,19 +639,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
   CTA_MARK(0)
   int jid, tile;
-  // split-K (NT only): the splits of one output tile are adjacent blocks
-  int splits = 1, split = 0, tile_lin = blockIdx.x;
+  // block -> (output tile, split, pair rank); the splits of one tile are adjacent
+  const int blk = blockIdx.x / NCTA;
+  int splits = 1, split = 0, tile_lin = blk;
   if constexpr (!IS_DW) {
     splits = p.splits > 1 ? p.splits : 1;
-    split = blockIdx.x % splits;
-    tile_lin = blockIdx.x / splits;
+    split = blk % splits;
+    tile_lin = blk / splits;
   }
   find_job(p.tile_start, p.njobs, tile_lin, jid, tile);
   const auto& job = p.job[jid];
   const int tiles_n = p.tiles_n[jid];
-  const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+  const int m0 = (tile / tiles_n) * (BM * NCTA) + (int)rank * BM;  // this CTA's accumulator rows
+  const int n0 = (tile % tiles_n) * BN;
+  const int nb0 = n0 + (int)rank * BNL;                             // this CTA's B rows
   int M, N, nstages;
   if constexpr (IS_DW) {
     M = job.m;
@@ -595,22 +674,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&tma_full[s], 1);
-      mbar_init(&conv_full[s], kProducers);
+      // pair: one arrival per converter warp of both CTAs (on the leader's copy)
+      mbar_init(&conv_full[s], PAIR ? 2 : kProducers);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN < 32 ? 32 : BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if constexpr (!IS_DW) {
     if (threadIdx.x < 256) stage_chain(chain_s, p.job[jid].epi, threadIdx.x, 256);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) {
+    cluster_sync();  // peer barriers initialised before any remote arrive
+  } else {
+    __syncthreads();
+  }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -635,26 +725,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
         TRACE(0, it)
         uint8_t* base = smem + s * C::STAGE_BYTES;
+        mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
         if constexpr (IS_DW) {
-          // MN-contiguous E [K x M] and Y [K x N]: boxes {32 mn, 32 k}, 4 KB each
-          mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
-#pragma unroll
-          for (int b = 0; b < BM / 32; ++b)
-            tma_load_2d(base + b * 4096, job.te, m0 + 32 * b, job.erow + k0, &tma_full[s]);
-#pragma unroll
-          for (int b = 0; b < BN / 32; ++b)
-            tma_load_2d(base + 2 * C::A_BYTES + b * 4096, job.ty, n0 + 32 * b, job.yrow + k0, &tma_full[s]);
+          // MN-contiguous E [K x M] and Y [K x N]: one 3-D box of 4 (BNL/32)
+          // 4-KB atoms {32 mn, 32 k} per operand (rgb_plan.cu encode_map_mn)
+          tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, m0 / 32, &tma_full[s]);
+          tma_load_3d(base + 2 * C::A_BYTES, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, nb0 / 32, &tma_full[s]);
           k0 += BK;
         } else {
           const Seg& sg = job.seg[seg];
-          // raw fp32 A and B only; both residuals are formed in shared memory
-          // by the converter warps (loading a precomputed W_lo would add 40% to
-          // the TMA bytes of every stage, and these GEMMs are L2-bandwidth bound)
-          mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
           tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
-#pragma unroll
-          for (int b = 0; b < BN / kBoxB; ++b)
-            tma_load_2d(base + 2 * C::A_BYTES + b * kBoxB * BK * 4, sg.tb, k0, n0 + b * kBoxB, &tma_full[s]);
+          // weight maps come in 32/64/128/256-row box variants: one load per stage
+          tma_load_2d(base + 2 * C::A_BYTES, map_at(sg.tb, kBoxIdx), k0, nb0, &tma_full[s]);
           k0 += BK;
           if (k0 >= sg.k) {
             k0 = 0;
@@ -664,13 +746,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
-      const uint32_t idesc = idesc_tf32(BM, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (the leader of a pair) ----------------
+      // pair: always the full BN (B rows past N are zero-filled by TMA, the
+      // epilogue skips those columns) so that each CTA's half is BN/2 rows
+      const int n_inst = (PAIR || (N - n0) >= BN) ? BN : (((N - n0) + 15) / 16) * 16;
+      const uint32_t idesc = idesc_tf32(BM * NCTA, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
-        mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
+        if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (it / C::STAGES) & 1);
+        else mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
         TRACE(2, it)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
@@ -699,17 +784,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
             dbl = smem_desc(b_lo + off, 16, sbo, lay);
           }
           const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+          if constexpr (PAIR) {
+            mma_tf32_pair(tmem, dal, dbh, idesc, acc0);
+            mma_tf32_pair(tmem, dah, dbl, idesc, 1u);
+            mma_tf32_pair(tmem, dah, dbh, idesc, 1u);
+          } else {
 #ifndef RGB_EXP_ONEMMA
-          mma_tf32(tmem, dal, dbh, idesc, acc0);
-          mma_tf32(tmem, dah, dbl, idesc, 1u);
-          mma_tf32(tmem, dah, dbh, idesc, 1u);
+            mma_tf32(tmem, dal, dbh, idesc, acc0);
+            mma_tf32(tmem, dah, dbl, idesc, 1u);
+            mma_tf32(tmem, dah, dbh, idesc, 1u);
 #else
-          mma_tf32(tmem, dah, dbh, idesc, acc0);
+            mma_tf32(tmem, dah, dbh, idesc, acc0);
 #endif
+          }
         }
-        mma_commit(&empty[s]);
+        if constexpr (PAIR) mma_commit_pair(&empty[s]);
+        else mma_commit(&empty[s]);
       }
-      mma_commit(done);
+      if constexpr (PAIR) mma_commit_pair(done);
+      else mma_commit(done);
     }
   } else {
     // ---------------- converters: x_lo = x - trunc(x), same byte offsets ----------------
@@ -737,7 +830,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
-      mbar_arrive(&conv_full[s]);
+      if constexpr (PAIR) {
+        // one arrival per CTA: a cluster-scope release costs a GPU-scope
+        // MEMBAR (ncu: 20% of converter stall cycles when every warp arrived)
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (threadIdx.x == 0) {
+          if (rank == 0) mbar_arrive(&conv_full[s]);
+          else mbar_arrive_cluster(&conv_full[s], 0);
+        }
+      } else {
+        mbar_arrive(&conv_full[s]);
+      }
     }
     // ---------------- epilogue ----------------
     mbar_wait(done, 0);
@@ -745,14 +848,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     CTA_MARK(1)
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x, tile_lin,
-                        split, splits);
+    // split-K partial tiles are indexed by 128-row tile: pair tile * 2 + rank
+    epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x,
+                        tile_lin * NCTA + (int)rank, split, splits);
     CTA_MARK(2)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) {
+    cluster_sync();  // the pair's MMAs and remote arrivals are complete before teardown
+  } else {
+    __syncthreads();
+  }
   if (warp == 9) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    }
   }
 }
 
@@ -767,16 +879,40 @@ void launch_one(P p, int tiles, cudaStream_t s) {
   k<<<tiles, kThreads, Cfg<BN>::SMEM, s>>>(p);
 }
 
-template <int BN, bool IS_DW, class P>
-void launch_tma(const P& p, int tiles, cudaStream_t s) {
-  using C = TCfg<BN, IS_DW ? 32 : kTmaNtBk>;
+// blocks = CTAs (2 per pair tile when PAIR)
+template <int BN, bool IS_DW, bool PAIR, class P>
+void launch_tma(const P& p, int blocks, cudaStream_t s) {
+  using C = TCfg<BN, BN / (PAIR ? 2 : 1), IS_DW ? 32 : kTmaNtBk>;
   static bool configured = false;
-  auto k = tma_gemm_kernel<BN, IS_DW, P>;
+  auto k = tma_gemm_kernel<BN, IS_DW, PAIR, P>;
   if (!configured) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
-  k<<<tiles, kTmaThreads, C::SMEM, s>>>(p);
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, p);
+  } else {
+    k<<<blocks, kTmaThreads, C::SMEM, s>>>(p);
+  }
+}
+
+// 128-row tile index of output row r, tile column tn (pair launches number
+// their 256-row tiles; each CTA of the pair owns tile * 2 + rank)
+__device__ __forceinline__ int cta_tile(bool pair, int t0, int tiles_n, int64_t r, int tn) {
+  if (!pair) return t0 + (int)(r / BM) * tiles_n + tn;
+  return (t0 + (int)(r / (2 * BM)) * tiles_n + tn) * 2 + (int)((r / BM) & 1);
 }
 
 // Split-K fixup + epilogue: acc = sum of the partial tiles in split order,
@@ -797,7 +933,7 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_const
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
       const int64_t r = q / (N / 4);
       const int c = (int)(q - r * (N / 4)) * 4;
-      const int tl = t0 + (int)(r / BM) * tiles_n + c / BN;
+      const int tl = cta_tile(p.pair != 0, t0, tiles_n, r, c / BN);
       const float* src = p.part + (size_t)tl * splits * tile_floats + (r % BM) * BN + (c % BN);
       float4 a = __ldcg(reinterpret_cast<const float4*>(src));
       for (int sp = 1; sp < splits; ++sp) a = add4(a, __ldcg(reinterpret_cast<const float4*>(src + sp * tile_floats)));
@@ -811,7 +947,7 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_const
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
       const int64_t r = e / N;
       const int c = (int)(e - r * N);
-      const int tl = t0 + (int)(r / BM) * tiles_n + c / BN;
+      const int tl = cta_tile(p.pair != 0, t0, tiles_n, r, c / BN);
       const float* src = p.part + (size_t)tl * splits * tile_floats + (r % BM) * BN + (c % BN);
       float a = __ldcg(src);
       for (int sp = 1; sp < splits; ++sp) a += __ldcg(src + sp * tile_floats);
@@ -838,112 +974,163 @@ int pick_bn(F tiles_for) {
 
 namespace {
 
-int nt_tiles(const GemmGroup& p, int bn) {
+bool pair_enabled() {  // RGB_TC_PAIR=0 disables the CTA-pair kernels (tuning experiments)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RGB_TC_PAIR");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
+// output tiles of a launch: 128-row tiles, or 256-row pair tiles
+int nt_tiles(const GemmGroup& p, int bn, bool pair) {
+  const int bm = tc::BM * (pair ? 2 : 1);
   int t = 0;
-  for (int j = 0; j < p.njobs; ++j) t += ((p.rows + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
+  for (int j = 0; j < p.njobs; ++j) t += ((p.rows + bm - 1) / bm) * ((p.job[j].n + bn - 1) / bn);
   return t;
 }
 
-// Tile width and split-K factor of a TMA NT launch.  Narrow tiles (BN <= 64,
-// chosen because there are few output tiles) re-read the A operand once per
-// tile column and convert it again each time; when K is deep, 128-wide tiles
-// split along K over up to 4 blocks keep every SM busy with half the
-// operand traffic per flop (512x1024x4096: 76 -> ~35 us).
-void nt_config(const GemmGroup& p, int& bn, int& splits) {
-  bn = tc::pick_bn([&](int b) { return nt_tiles(p, b); });
-  splits = 1;
-  static int split_env = -2;  // RGB_TC_SPLIT=0 disables split-K (tuning experiments)
-  if (split_env == -2) {
-    const char* e = getenv("RGB_TC_SPLIT");
-    split_env = e ? atoi(e) : -1;
-  }
-  if (!p.tma || bn >= 128 || getenv("RGB_TC_BN") || split_env == 0) return;
+int nt_min_stages(const GemmGroup& p) {
   int kst = 1 << 30;
   for (int j = 0; j < p.njobs; ++j) {
     int st = 0;
     for (int s = 0; s < p.job[j].nseg; ++s) st += (p.job[j].seg[s].k + kTmaNtBk - 1) / kTmaNtBk;
     kst = st < kst ? st : kst;
   }
-  const int t128 = nt_tiles(p, 128);
-  int sp = 148 / (t128 > 0 ? t128 : 1);
-  sp = sp > 4 ? 4 : sp;
-  while (sp > 1 && kst / sp < 8) --sp;  // at least 8 K-stages per split
+  return kst;
+}
+
+struct NtConfig {
+  int bn = 32, splits = 1;
+  bool pair = false;
+};
+
+// Tile shape of a launch.  TMA launches prefer CTA pairs (256 x BN tiles,
+// half of B per CTA); when there are too few tiles to cover the SMs and K is
+// deep, the K range is split over up to 4 tiles' worth of blocks (narrow
+// tiles instead re-read and re-convert A once per tile column).
+NtConfig nt_config(const GemmGroup& p) {
+  NtConfig c;
+  c.bn = tc::pick_bn([&](int b) { return nt_tiles(p, b, false); });
+  static int split_env = -2;  // RGB_TC_SPLIT=0 disables split-K (tuning experiments)
+  if (split_env == -2) {
+    const char* e = getenv("RGB_TC_SPLIT");
+    split_env = e ? atoi(e) : -1;
+  }
+  if (!p.tma || getenv("RGB_TC_BN")) return c;
+  const int kst = nt_min_stages(p);
+  auto split_for = [&](int ctas) {
+    int sp = 148 / (ctas > 0 ? ctas : 1);
+    sp = sp > 4 ? 4 : sp;
+    while (sp > 1 && kst / sp < 8) --sp;  // at least 8 K-stages per split
+    return split_env == 0 ? 1 : (sp < 1 ? 1 : sp);
+  };
+  if (pair_enabled()) {
+    // pairs only when they fill the machine without split-K: small (per-frame)
+    // products with a short K range lose more to the pair's longer pipeline
+    // start than they gain (cfg4 per-frame GEMMs: 5.2 -> 6.0 ms per step)
+    for (int bn : {256, 128}) {
+      if (2 * nt_tiles(p, bn, true) >= 120) {
+        c.bn = bn;
+        c.pair = true;
+        return c;
+      }
+    }
+  }
+  if (c.bn >= 128) return c;
+  const int sp = split_for(nt_tiles(p, 128, false));
   if (sp > 1) {
-    bn = 128;
-    splits = sp;
+    c.bn = 128;
+    c.splits = sp;
+  }
+  return c;
+}
+
+long long nt_scratch(const GemmGroup& p, const NtConfig& c) {
+  return c.splits > 1 ? (long long)nt_tiles(p, c.bn, c.pair) * (c.pair ? 2 : 1) * c.splits * tc::BM * c.bn : 0;
+}
+
+template <bool PAIR>
+void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s) {
+  if (bn == 256) tc::launch_tma<256, false, PAIR>(p, blocks, s);
+  else if (bn == 128) tc::launch_tma<128, false, PAIR>(p, blocks, s);
+  else if constexpr (!PAIR) {
+    if (bn == 64) tc::launch_tma<64, false, false>(p, blocks, s);
+    else tc::launch_tma<32, false, false>(p, blocks, s);
   }
 }
 
 }  // namespace
 
-long long tc_gemm_nt_scratch(const GemmGroup& p) {
-  int bn, splits;
-  nt_config(p, bn, splits);
-  return splits > 1 ? (long long)nt_tiles(p, bn) * splits * tc::BM * bn : 0;
-}
+long long tc_gemm_nt_scratch(const GemmGroup& p) { return nt_scratch(p, nt_config(p)); }
 
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
-  int bn, splits;
-  nt_config(p, bn, splits);
-  if (splits > 1 && (!p.part || (long long)nt_tiles(p, bn) * splits * tc::BM * bn > p.part_cap)) {
-    // no (or too small a) scratch: fall back to the unsplit configuration
-    bn = tc::pick_bn([&](int b) { return nt_tiles(p, b); });
-    splits = 1;
-  }
-  p.splits = splits;
+  NtConfig c = nt_config(p);
+  if (c.splits > 1 && (!p.part || nt_scratch(p, c) > p.part_cap)) c.splits = 1;  // no (or too small a) scratch
+  if (!p.tma) c = NtConfig{tc::pick_bn([&](int b) { return nt_tiles(p, b, false); }), 1, false};
+  p.splits = c.splits;
+  p.pair = c.pair ? 1 : 0;
+  const int bm = tc::BM * (c.pair ? 2 : 1);
   p.tile_start[0] = 0;
   for (int j = 0; j < p.njobs; ++j) {
-    p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
-    p.tile_start[j + 1] = p.tile_start[j] + ((p.rows + tc::BM - 1) / tc::BM) * p.tiles_n[j];
+    p.tiles_n[j] = (p.job[j].n + c.bn - 1) / c.bn;
+    p.tile_start[j + 1] = p.tile_start[j] + ((p.rows + bm - 1) / bm) * p.tiles_n[j];
   }
-  const int tiles = p.tile_start[p.njobs] * splits;
-  if (tiles == 0) return 0;
+  const int blocks = p.tile_start[p.njobs] * c.splits * (c.pair ? 2 : 1);
+  if (blocks == 0) return 0;
   if (p.tma) {
-    if (bn == 256) tc::launch_tma<256, false>(p, tiles, s);
-    else if (bn == 128) tc::launch_tma<128, false>(p, tiles, s);
-    else if (bn == 64) tc::launch_tma<64, false>(p, tiles, s);
-    else tc::launch_tma<32, false>(p, tiles, s);
+    if (c.pair) launch_nt_bn<true>(p, c.bn, blocks, s);
+    else launch_nt_bn<false>(p, c.bn, blocks, s);
   } else {
-    if (bn == 256) tc::launch_one<256, false>(p, tiles, s);
-    else if (bn == 128) tc::launch_one<128, false>(p, tiles, s);
-    else if (bn == 64) tc::launch_one<64, false>(p, tiles, s);
-    else tc::launch_one<32, false>(p, tiles, s);
+    if (c.bn == 256) tc::launch_one<256, false>(p, blocks, s);
+    else if (c.bn == 128) tc::launch_one<128, false>(p, blocks, s);
+    else if (c.bn == 64) tc::launch_one<64, false>(p, blocks, s);
+    else tc::launch_one<32, false>(p, blocks, s);
   }
-  if (splits == 1) return 1;
+  if (c.splits == 1) return 1;
   int64_t maxq = 0;
   for (int j = 0; j < p.njobs; ++j) maxq = std::max<int64_t>(maxq, (int64_t)p.rows * p.job[j].n);
   maxq = (maxq + 3) / 4;
-  int blocks = (int)std::min<int64_t>((maxq + 255) / 256, 148 * 8);
-  blocks = blocks < 1 ? 1 : blocks;
-  // bn == 128 whenever splits > 1 (nt_config)
-  tc::splitk_epilogue_kernel<128><<<dim3(blocks, p.njobs), 256, 0, s>>>(p);
+  int eblocks = (int)std::min<int64_t>((maxq + 255) / 256, 148 * 8);
+  eblocks = eblocks < 1 ? 1 : eblocks;
+  if (c.bn == 256) tc::splitk_epilogue_kernel<256><<<dim3(eblocks, p.njobs), 256, 0, s>>>(p);
+  else tc::splitk_epilogue_kernel<128><<<dim3(eblocks, p.njobs), 256, 0, s>>>(p);
   return 2;
 }
 
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
+  const bool pair = p.tma && pair_enabled() && !getenv("RGB_TC_BN");
+  const int bm = tc::BM * (pair ? 2 : 1);
   auto tiles_for = [&](int bn) {
     int t = 0;
-    for (int j = 0; j < p.njobs; ++j) t += ((p.job[j].m + tc::BM - 1) / tc::BM) * ((p.job[j].n + bn - 1) / bn);
-    return t;
+    for (int j = 0; j < p.njobs; ++j) t += ((p.job[j].m + bm - 1) / bm) * ((p.job[j].n + bn - 1) / bn);
+    return t * (pair ? 2 : 1);
   };
-  const int bn = tc::pick_bn(tiles_for);
+  int bn = tc::pick_bn(tiles_for);
+  if (pair && bn < 128) bn = 128;
   p.tile_start[0] = 0;
   for (int j = 0; j < p.njobs; ++j) {
     p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
-    p.tile_start[j + 1] = p.tile_start[j] + ((p.job[j].m + tc::BM - 1) / tc::BM) * p.tiles_n[j];
+    p.tile_start[j + 1] = p.tile_start[j] + ((p.job[j].m + bm - 1) / bm) * p.tiles_n[j];
   }
-  const int tiles = p.tile_start[p.njobs];
-  if (tiles == 0) return;
+  const int blocks = p.tile_start[p.njobs] * (pair ? 2 : 1);
+  if (blocks == 0) return;
   if (p.tma) {
-    if (bn == 256) tc::launch_tma<256, true>(p, tiles, s);
-    else if (bn == 128) tc::launch_tma<128, true>(p, tiles, s);
-    else if (bn == 64) tc::launch_tma<64, true>(p, tiles, s);
-    else tc::launch_tma<32, true>(p, tiles, s);
+    if (pair) {
+      if (bn == 256) tc::launch_tma<256, true, true>(p, blocks, s);
+      else tc::launch_tma<128, true, true>(p, blocks, s);
+    } else {
+      if (bn == 256) tc::launch_tma<256, true, false>(p, blocks, s);
+      else if (bn == 128) tc::launch_tma<128, true, false>(p, blocks, s);
+      else if (bn == 64) tc::launch_tma<64, true, false>(p, blocks, s);
+      else tc::launch_tma<32, true, false>(p, blocks, s);
+    }
   } else {
-    if (bn == 256) tc::launch_one<256, true>(p, tiles, s);
-    else if (bn == 128) tc::launch_one<128, true>(p, tiles, s);
-    else if (bn == 64) tc::launch_one<64, true>(p, tiles, s);
-    else tc::launch_one<32, true>(p, tiles, s);
+    if (bn == 256) tc::launch_one<256, true>(p, blocks, s);
+    else if (bn == 128) tc::launch_one<128, true>(p, blocks, s);
+    else if (bn == 64) tc::launch_one<64, true>(p, blocks, s);
+    else tc::launch_one<32, true>(p, blocks, s);
   }
 }
 

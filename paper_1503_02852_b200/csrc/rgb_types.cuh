@@ -94,6 +94,7 @@ struct GemmGroup {
   float* part;
   long long part_cap;  // floats
   int splits;          // set by launch_tc_gemm_nt
+  int pair;            // 1: CTA-pair (cta_group::2) tiles of 256 rows
 };
 
 struct EwLaunch {

@@ -18,13 +18,30 @@
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <bool PARAM>
-__global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensorMap pm, const CUtensorMap* gm,
+__global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensorMap pm, const CUtensorMap* gm,
                                                 int iters, int stages, int stage_bytes, int box_w, int box_h,
-                                                int rows, int cols, long long* out, int prefetch) {
+                                                int rows, int cols, long long* out, int prefetch, int stream_warps) {
   extern __shared__ __align__(1024) uint8_t sm_base[];
   uint8_t* sm = sm_base;
-  const int nw = blockDim.x / 32, w = threadIdx.x / 32;
+  const int nw = blockDim.x / 32 - stream_warps, w = threadIdx.x / 32;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm_base + nw * stages * stage_bytes) + w * stages;
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (w >= nw) {
+    // converter-like smem traffic over a 64 KB region after the barriers
+    float4* s4 = reinterpret_cast<float4*>(sm_base + nw * stages * stage_bytes + 1024);
+    float acc = 0.f;
+    while (!stop) {
+      for (int q = threadIdx.x - nw * 32; q < 2048; q += stream_warps * 32) {
+        float4 v = s4[q];
+        acc += v.x;
+        s4[q + 2048] = v;
+      }
+    }
+    if (acc == 1234.f) out[0] = 0;
+    return;
+  }
   if ((threadIdx.x & 31) != 0) return;
   sm += w * stages * stage_bytes;
   const CUtensorMap* map = PARAM ? &pm : gm;
@@ -69,6 +86,7 @@ __global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensor
                    : "=r"(done) : "r"(su32(&bar[last % stages])), "r"(par) : "memory");
   }
   if (w == 0) {
+    stop = 1;
     out[blockIdx.x] = clock64() - t0;
     out[148 + blockIdx.x] = tw;
     out[296 + blockIdx.x] = ti;
@@ -89,12 +107,11 @@ int main() {
   long long* out;
   cudaMalloc(&out, 3 * 148 * 8);
   int sms = 148;
-  struct Case { int box_w, box_h, stages, stage_kb; bool param; int prefetch; int warps = 1; };
+  struct Case { int box_w, box_h, stages, stage_kb; bool param; int prefetch; int warps = 1; int stream = 0; };
   Case cases[] = {
-      {32, 128, 6, 16, true, 0, 1}, {32, 128, 3, 16, true, 0, 2}, {32, 128, 2, 16, true, 0, 4},
-      {32, 128, 1, 16, true, 0, 8}, {32, 32, 3, 16, true, 0, 2}, {32, 32, 1, 16, true, 0, 8},
-      {16, 128, 6, 16, true, 0, 1}, {16, 128, 3, 16, true, 0, 2}, {16, 128, 2, 16, true, 0, 4},
-      {32, 256, 4, 32, true, 0, 1}, {32, 256, 2, 32, true, 0, 2},
+      {32, 128, 3, 32, true, 0, 1, 0}, {32, 128, 3, 32, true, 0, 1, 8},
+      {32, 256, 3, 32, true, 0, 1, 0}, {32, 256, 3, 32, true, 0, 1, 8},
+      {32, 128, 6, 16, true, 0, 1, 0}, {32, 128, 6, 16, true, 0, 1, 8},
   };
   for (const Case& c : cases) {
     CUtensorMap m;
@@ -107,12 +124,12 @@ int main() {
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); continue; }
     cudaMemcpy(gm, &m, sizeof m, cudaMemcpyHostToDevice);
-    const int sb = c.stage_kb * 1024, smem = c.warps * c.stages * sb + 1024;
+    const int sb = c.stage_kb * 1024, smem = c.warps * c.stages * sb + 1024 + (c.stream ? 65536 + 1024 : 0);
     auto k = c.param ? probe<true> : probe<false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 2000;
     for (int rep = 0; rep < 2; ++rep)
-      k<<<sms, 32 * c.warps, smem>>>(m, gm, iters, c.stages, sb, c.box_w, c.box_h, rows, cols, out, c.prefetch);
+      k<<<sms, 32 * (c.warps + c.stream), smem>>>(m, gm, iters, c.stages, sb, c.box_w, c.box_h, rows, cols, out, c.prefetch, c.stream);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     long long h[3 * 148];
@@ -124,6 +141,7 @@ int main() {
       mw += h[148 + i] / (double)sms / iters;
       mi += h[296 + i] / (double)sms / iters;
     }
+    printf("stream %d ", c.stream);
     printf("box {%2d,%3d} %s%s %d warps x stages %2d x %2d KB: %6.1f B/clk/SM (mean cyc/stage %.0f)\n", c.box_w,
            c.box_h, c.param ? "param " : "global", c.prefetch ? "+pf" : "   ", c.warps, c.stages, c.stage_kb,
            (double)iters * sb * c.warps / mean, mean / iters);
