@@ -16,6 +16,20 @@ __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ E
   for (int i = threadIdx.x; i < (int)(sizeof(EwChain) / 4); i += blockDim.x) chain_words[i] = src[i];
   __syncthreads();
   const EwChain& ch = *reinterpret_cast<const EwChain*>(chain_words);
+  if (chain_vec_ok(ch, ch.width)) {
+    // 16-byte path: one thread per 4 consecutive units of a row
+    const int w4 = ch.width / 4;
+    const int64_t nq = (int64_t)p.rows * w4;
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t rr[1] = {q / w4};
+      const int j = (int)(q - rr[0] * w4) * 4;
+      const bool ok[1] = {true};
+      const float4 acc[1] = {zero};
+      for (int k = 0; k < ch.nops; ++k) ew_apply_vec<1>(ch.op[k], ch.width, rr, j, ok, p.ring, false, acc);
+    }
+    return;
+  }
   const int64_t total = (int64_t)p.rows * ch.width;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / ch.width;
@@ -163,6 +177,113 @@ __global__ void __launch_bounds__(256) gemm_dw_kernel(const __grid_constant__ Dw
 void launch_gemm_dw(const DwGroup& p, cudaStream_t s) {
   const int tiles = p.tile_start[p.njobs];
   if (tiles > 0) gemm_dw_kernel<<<tiles, 256, 0, s>>>(p);
+}
+
+// ---------------------------------------------------------------------------
+// Narrow dW (n <= 4, e.g. the bias edge from the constant-one layer):
+// G[m, j] = alpha * sum_r E[r, m] * Y[r, j].  A tensor-core tile would be
+// 97% padding; this is a GEMV-shaped HBM stream of E instead.  Pass 1: block
+// (job, 128-unit group, K chunk), lane = 4 consecutive units (16-byte loads),
+// warp w takes rows w, w+8, ...; warps reduced in fixed order into part[].
+// Pass 2 sums the chunks in order: bitwise reproducible.
+constexpr int kNarrowChunk = 1024;  // rows per K chunk
+
+__device__ __forceinline__ void narrow_locate(const DwGroup& p, int b, int nchunks, int& job, int& grp, int& chunk) {
+  job = 0;
+  int base = 0;
+  for (;;) {
+    const int groups = (p.job[job].m + 127) / 128;
+    if (b < base + groups * nchunks || job + 1 == p.njobs) break;
+    base += groups * nchunks;
+    ++job;
+  }
+  const int local = b - base;
+  grp = local / nchunks;
+  chunk = local % nchunks;
+}
+
+__global__ void __launch_bounds__(256) dw_narrow_kernel(const __grid_constant__ DwGroup p, float* part,
+                                                        int nchunks) {
+  __shared__ float red[8][128][4];
+  int job, grp, chunk;
+  narrow_locate(p, blockIdx.x, nchunks, job, grp, chunk);
+  const DwJob& jb = p.job[job];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m = jb.m, n = jb.n;
+  const int u0 = grp * 128 + lane * 4;
+  const int r0 = chunk * kNarrowChunk, r1 = min(p.k, r0 + kNarrowChunk);
+  float acc[4][4] = {};
+  for (int r = r0 + warp; r < r1; r += 8) {
+    float e[4];
+    if (u0 + 3 < m && (m & 3) == 0) {
+      const float4 v = *reinterpret_cast<const float4*>(jb.e + (int64_t)r * m + u0);
+      e[0] = v.x, e[1] = v.y, e[2] = v.z, e[3] = v.w;
+    } else {
+      for (int t = 0; t < 4; ++t) e[t] = u0 + t < m ? jb.e[(int64_t)r * m + u0 + t] : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= n) break;
+      const float y = jb.y[(int64_t)r * n + j];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[j][t] = fmaf(e[t], y, acc[j][t]);
+    }
+  }
+  for (int t = 0; t < 4; ++t)
+    for (int j = 0; j < 4; ++j) red[warp][lane * 4 + t][j] = acc[j][t];
+  __syncthreads();
+  // fixed-order reduction over the 8 warps; thread = (unit, j)
+  for (int q = threadIdx.x; q < 128 * 4; q += 256) {
+    const int u = q / 4, j = q % 4;
+    if (j >= n || grp * 128 + u >= m) continue;
+    float s = 0.0f;
+    for (int w = 0; w < 8; ++w) s += red[w][u][j];
+    part[((size_t)blockIdx.x) * 512 + q] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) dw_narrow_sum_kernel(const __grid_constant__ DwGroup p, const float* part,
+                                                            int nchunks) {
+  // one thread per (job, unit, j); blocks of pass 1 are laid out job-major,
+  // then unit group, then chunk
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  int base_blocks = 0;
+  for (int job = 0; job < p.njobs; ++job) {
+    const DwJob& jb = p.job[job];
+    const int groups = (jb.m + 127) / 128;
+    const int cnt = jb.m * jb.n;
+    if (q < cnt) {
+      const int u = q / jb.n, j = q % jb.n;
+      const int grp = u / 128, ul = u % 128;
+      const float* src = part + ((size_t)(base_blocks + grp * nchunks)) * 512 + ul * 4 + j;
+      float s = 0.0f;
+      for (int c = 0; c < nchunks; ++c) s += src[(size_t)c * 512];
+      jb.g[(int64_t)u * jb.n + j] = p.alpha * s;
+      return;
+    }
+    q -= cnt;
+    base_blocks += groups * nchunks;
+  }
+}
+
+long long dw_narrow_scratch(const DwGroup& p) {
+  const int nchunks = (p.k + kNarrowChunk - 1) / kNarrowChunk;
+  long long blocks = 0;
+  for (int j = 0; j < p.njobs; ++j) blocks += (long long)((p.job[j].m + 127) / 128) * nchunks;
+  return blocks * 512;
+}
+
+int launch_dw_narrow(const DwGroup& p, float* part, cudaStream_t s) {
+  const int nchunks = (p.k + kNarrowChunk - 1) / kNarrowChunk;
+  int blocks = 0, outs = 0;
+  for (int j = 0; j < p.njobs; ++j) {
+    blocks += ((p.job[j].m + 127) / 128) * nchunks;
+    outs += p.job[j].m * p.job[j].n;
+  }
+  if (blocks == 0) return 0;
+  dw_narrow_kernel<<<blocks, 256, 0, s>>>(p, part, nchunks);
+  dw_narrow_sum_kernel<<<(outs + 255) / 256, 256, 0, s>>>(p, part, nchunks);
+  return 2;
 }
 
 // ---------------------------------------------------------------------------

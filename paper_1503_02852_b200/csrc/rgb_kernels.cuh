@@ -30,6 +30,10 @@ struct TransposeGroup {
 void launch_ew(const EwLaunch& p, cudaStream_t s);
 void launch_gemm_nt(const GemmGroup& p, cudaStream_t s);
 void launch_gemm_dw(const DwGroup& p, cudaStream_t s);
+// dW of narrow sources (n <= 4, bias edges): two deterministic GEMV passes
+// through `part` (dw_narrow_scratch floats); returns the launch count
+long long dw_narrow_scratch(const DwGroup& p);
+int launch_dw_narrow(const DwGroup& p, float* part, cudaStream_t s);
 // tcgen05 (3xTF32, TMEM accumulator) versions of the two GEMM forms; same
 // descriptors, tiles recomputed for 128 x {64,128,256} (rgb_tc_gemm.cu).
 // returns the number of kernels launched (2 with split-K: GEMM + fixup/epilogue)

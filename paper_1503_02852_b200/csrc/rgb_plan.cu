@@ -189,21 +189,26 @@ struct rgb_plan {
   float* part = nullptr;
   long long part_cap = 0;
 
+  // required: the caller has no fallback when the scratch is short (a CUDA
+  // graph capture cannot allocate; graphs are captured after an eager step)
+  int grow_scratch(long long need, cudaStream_t st, bool required) {
+    if (need <= part_cap) return RGB_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return required ? fail(RGB_ERR_CUDA, "scratch must be sized by an eager step before graph capture") : RGB_OK;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(RGB_ERR_CUDA, "scratch sync");
+    if (part) cudaFree(part);
+    part = nullptr;
+    part_cap = 0;
+    if (cudaMalloc(&part, need * 4) != cudaSuccess) return fail(RGB_ERR_CUDA, "scratch allocation (%lld floats)", need);
+    part_cap = need;
+    return RGB_OK;
+  }
+
   int splitk_scratch(GemmGroup& G, cudaStream_t st) {
-    const long long need = tc_gemm_nt_scratch(G);
-    if (need > part_cap) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cs);
-      if (cs == cudaStreamCaptureStatusNone) {
-        if (cudaStreamSynchronize(st) != cudaSuccess) return fail(RGB_ERR_CUDA, "split-K scratch sync");
-        if (part) cudaFree(part);
-        part = nullptr;
-        part_cap = 0;
-        if (cudaMalloc(&part, need * 4) != cudaSuccess)
-          return fail(RGB_ERR_CUDA, "split-K scratch allocation (%lld floats)", need);
-        part_cap = need;
-      }
-    }
+    int rc = grow_scratch(tc_gemm_nt_scratch(G), st, false);
+    if (rc) return rc;
     G.part = part;
     G.part_cap = part_cap;
     return RGB_OK;
@@ -724,21 +729,27 @@ struct rgb_plan {
         }
         // jobs with TMA maps -> TMA-fed tcgen05 launch; the rest (e.g. width-1
         // bias sources) -> one SIMT / register-fed launch
-        DwGroup T = D, R = D;
-        T.njobs = R.njobs = 0;
+        // narrow sources (bias edges, n <= 4) -> GEMV-shaped stream (V) when the
+        // step is large enough for the tensor cores; the rest of the TC-eligible
+        // jobs -> TMA launch (T); remainder -> SIMT / register-fed launch (R)
+        DwGroup T = D, R = D, V = D;
+        T.njobs = R.njobs = V.njobs = 0;
         T.tma = 1;
-        R.tma = 0;
+        R.tma = V.tma = 0;
         double rflops = 0;
         for (int j = 0; j < D.njobs; ++j) {
           const DwJob& jb = D.job[j];
           const double f = 2.0 * D.k * (double)jb.m * jb.n;
           if (jb.te && use_tc(flops)) {
             T.job[T.njobs++] = jb;
+          } else if (jb.n <= 4 && use_tc(flops)) {
+            V.job[V.njobs++] = jb;
           } else {
             R.job[R.njobs++] = jb;
             rflops += f;
           }
         }
+        if (V.njobs && (rc = grow_scratch(dw_narrow_scratch(V), st, true))) return rc;
         auto tiles64 = [](DwGroup& G) {
           G.tile_start[0] = 0;
           for (int j = 0; j < G.njobs; ++j) {
@@ -757,6 +768,10 @@ struct rgb_plan {
           if (use_tc(rflops)) launch_tc_gemm_dw(R, st);
           else launch_gemm_dw(R, st);
           note_launch();
+        }
+        if (V.njobs) {
+          const int nl = launch_dw_narrow(V, part, st);
+          for (int q = 0; q < nl; ++q) note_launch();
         }
         prof_stop(slot, st, PROF_DW, flops, bytes);
       } else {
