@@ -21,9 +21,12 @@ __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ E
     const int w4 = ch.width / 4;
     const int64_t nq = (int64_t)p.rows * w4;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t rr[1] = {q / w4};
-      const int j = (int)(q - rr[0] * w4) * 4;
+    // 32-bit index arithmetic (a 64-bit division is a long subroutine call)
+    if (nq >= (int64_t)UINT32_MAX) __trap();
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)nq; q += gridDim.x * blockDim.x) {
+      const uint32_t r32 = q / (uint32_t)w4;
+      const int64_t rr[1] = {(int64_t)r32};
+      const int j = (int)(q - r32 * (uint32_t)w4) * 4;
       const bool ok[1] = {true};
       const float4 acc[1] = {zero};
       for (int k = 0; k < ch.nops; ++k) ew_apply_vec<1>(ch.op[k], ch.width, rr, j, ok, p.ring, false, acc);

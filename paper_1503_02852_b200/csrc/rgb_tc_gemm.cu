@@ -38,7 +38,7 @@ namespace tc {
 
 // tuning aid: per-stage clock64 trace of CTA 0 (tools/build_exp.sh trace -DRGB_EXP_TRACE)
 #ifdef RGB_EXP_TRACE
-__device__ long long g_trace[4][1024];
+__device__ long long g_trace[6][1024];
 __device__ long long g_cta[1024][4];  // globaltimer: start, mainloop done, epilogue done; smid
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -551,19 +551,57 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 // by the tensor core -- the kernel is shared-memory-bandwidth bound
 // (tools/gemm_bench.py trace build: 288 KB of smem traffic per 32-deep stage at
 // 128x256 vs 1536 MMA cycles).
-constexpr int kTmaThreads = 320;  // warps 0-7 convert + epilogue, 8 TMA, 9 MMA
+constexpr int kTmaThreads = 352;  // warps 0-7 convert + epilogue, 8 and 10 TMA, 9 MMA
 
-template <int BN, int BNL, int BKT>
+// TA: the A operand's tf32 hi/lo halves live in tensor memory (converter
+// warps tcgen05.st them), so the tensor core reads only B from shared memory.
+// Shared memory per stage: [A raw][B][B_lo] (TA) or [A][A_lo][B][B_lo].
+template <int BN, int BNL, int BKT, bool TA>
 struct TCfg {
   static constexpr int BK = BKT;
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BNL * BK * 4;  // this CTA's B rows
-  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  static constexpr int B_OFF = TA ? A_BYTES : 2 * A_BYTES;
+  static constexpr int STAGE_BYTES = B_OFF + 2 * B_BYTES;
   static constexpr int RAW = 196608 / STAGE_BYTES;
-  static constexpr int STAGES = RAW > 8 ? 8 : (RAW < 2 ? 2 : RAW);
+  static constexpr int TMEM_CAP = TA ? (512 - BN) / 64 : 8;  // A stages of 64 TMEM columns
+  static constexpr int CAP = TMEM_CAP < 8 ? TMEM_CAP : 8;
+  static constexpr int STAGES = RAW > CAP ? CAP : (RAW < 2 ? 2 : RAW);
+  static constexpr int TMEM_COLS = TA ? 512 : (BN < 32 ? 32 : BN);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kChainBytes;
   static_assert(BM * (BN + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit in the pipeline smem");
+  static_assert(!TA || BK == 32, "TMEM A path reads the SWIZZLE_128B K-major layout");
 };
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_tf32_ta_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
 
 template <int ROWS>
 __host__ __device__ constexpr int box_idx() {  // 32/64/128/256-row map variant
@@ -622,7 +660,12 @@ template <int BN, bool IS_DW, bool PAIR, class P>
 __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_constant__ P p) {
   constexpr int NCTA = PAIR ? 2 : 1;
   constexpr int BNL = BN / NCTA;  // B rows held by this CTA
-  using C = TCfg<BN, BNL, IS_DW ? 32 : kTmaNtBk>;
+#ifdef RGB_EXP_NO_TMEM_A
+  constexpr bool TA = false;
+#else
+  constexpr bool TA = !IS_DW && kTmaNtBk == 32;
+#endif
+  using C = TCfg<BN, BNL, IS_DW ? 32 : kTmaNtBk, TA>;
   constexpr int BK = C::BK;
   constexpr int kBoxIdx = box_idx<BNL>();
   extern __shared__ uint8_t smem_raw[];
@@ -673,7 +716,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&tma_full[s], 1);
+      mbar_init(&tma_full[s], 2);  // one expect_tx arrival per producer warp
       // pair: one arrival per converter warp of both CTAs (on the leader's copy)
       mbar_init(&conv_full[s], PAIR ? 2 : kProducers);
       mbar_init(&empty[s], 1);
@@ -684,11 +727,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   if (warp == 9) {
     if constexpr (PAIR) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(BN < 32 ? 32 : BN));
+                   "r"(C::TMEM_COLS));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(BN < 32 ? 32 : BN));
+                   "r"(C::TMEM_COLS));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -704,9 +747,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 8 || warp == 10) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producers: warp 8 loads A, warp 10 loads B ----------------
+      // (two issuing warps: a single thread's TMA instructions complete one
+      // after another at ~25-55 B/clk per SM -- tools/tma_probe.cu)
+      const bool load_a = warp == 8;
       int seg = 0, k0 = 0;
       if constexpr (!IS_DW) {
         for (int skip = s_begin; skip > 0;) {  // locate the first stage of this split
@@ -723,20 +769,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-        TRACE(0, it)
+        if (load_a) { TRACE(0, it) }
         uint8_t* base = smem + s * C::STAGE_BYTES;
-        mbar_expect_tx(&tma_full[s], C::A_BYTES + C::B_BYTES);
+        mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
         if constexpr (IS_DW) {
           // MN-contiguous E [K x M] and Y [K x N]: one 3-D box of 4 (BNL/32)
           // 4-KB atoms {32 mn, 32 k} per operand (rgb_plan.cu encode_map_mn)
-          tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, m0 / 32, &tma_full[s]);
-          tma_load_3d(base + 2 * C::A_BYTES, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, nb0 / 32, &tma_full[s]);
+          if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, m0 / 32, &tma_full[s]);
+          else tma_load_3d(base + C::B_OFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, nb0 / 32, &tma_full[s]);
           k0 += BK;
         } else {
           const Seg& sg = job.seg[seg];
-          tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
+          if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
           // weight maps come in 32/64/128/256-row box variants: one load per stage
-          tma_load_2d(base + 2 * C::A_BYTES, map_at(sg.tb, kBoxIdx), k0, nb0, &tma_full[s]);
+          else tma_load_2d(base + C::B_OFF, map_at(sg.tb, kBoxIdx), k0, nb0, &tma_full[s]);
           k0 += BK;
           if (k0 >= sg.k) {
             k0 = 0;
@@ -760,7 +806,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
-        const uint32_t b_hi = base + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
+        const uint32_t b_hi = base + C::B_OFF, b_lo = b_hi + C::B_BYTES;
+        const uint32_t ta_hi = tmem + BN + 64 * s, ta_lo = ta_hi + 32;  // TA: A stage in TMEM
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           uint64_t dah, dal, dbh, dbl;
@@ -784,7 +831,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
             dbl = smem_desc(b_lo + off, 16, sbo, lay);
           }
           const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
-          if constexpr (PAIR) {
+          if constexpr (TA) {
+            // A hi/lo from tensor memory: 8 columns per k-step
+            if constexpr (PAIR) {
+              mma_tf32_ta_pair(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
+              mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
+              mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbh, idesc, 1u);
+            } else {
+              mma_tf32_ta(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
+              mma_tf32_ta(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
+              mma_tf32_ta(tmem, ta_hi + 8 * j, dbh, idesc, 1u);
+            }
+          } else if constexpr (PAIR) {
             mma_tf32_pair(tmem, dal, dbh, idesc, acc0);
             mma_tf32_pair(tmem, dah, dbl, idesc, 1u);
             mma_tf32_pair(tmem, dah, dbh, idesc, 1u);
@@ -812,23 +870,47 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       if (threadIdx.x == 0) { TRACE(1, it) }
       uint8_t* base = smem + s * C::STAGE_BYTES;
 #ifndef RGB_EXP_NOCONV
-      const float4* a_hi = reinterpret_cast<const float4*>(base);
-      float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
+      if constexpr (TA) {
+        // A row r = 32*(warp%4) + lane (the TMEM lane quarter this warp may
+        // access), K half (warp/4): 16-B chunk c of row r sits at (c ^ (r%8))
+        // in the SWIZZLE_128B layout; hi = raw (the MMA truncates), lo = residual
+        const int quarter = warp & 3, kh = warp >> 2, r = quarter * 32 + lane;
+        const uint8_t* arow = base + r * 128;
+        float hi[16], lo[16];
 #pragma unroll
-      for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
-        const int q = threadIdx.x + i * kProducers;
-        const float4 x = a_hi[q];
-        a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = kh * 4 + cc;
+          const float4 x = *reinterpret_cast<const float4*>(arow + ((c ^ (r & 7)) * 16));
+          hi[4 * cc] = x.x, hi[4 * cc + 1] = x.y, hi[4 * cc + 2] = x.z, hi[4 * cc + 3] = x.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
+        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + 64 * s + 16 * kh;
+        tmem_st16(ta, hi);
+        tmem_st16(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      } else {
+        const float4* a_hi = reinterpret_cast<const float4*>(base);
+        float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
+#pragma unroll
+        for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
+          const int q = threadIdx.x + i * kProducers;
+          const float4 x = a_hi[q];
+          a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        }
       }
       {  // B residual (weights for the NT form, activations for dW)
-        const float4* b_hi = reinterpret_cast<const float4*>(base + 2 * C::A_BYTES);
-        float4* b_lo = reinterpret_cast<float4*>(base + 2 * C::A_BYTES + C::B_BYTES);
+        const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
+        float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
         for (int q = threadIdx.x; q < C::B_BYTES / 16; q += kProducers) {
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
       }
+      if (threadIdx.x == 0) { TRACE(4, it) }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (threadIdx.x == 0) { TRACE(5, it) }
 #endif
       if constexpr (PAIR) {
         // one arrival per CTA: a cluster-scope release costs a GPU-scope
@@ -861,9 +943,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   }
   if (warp == 9) {
     if constexpr (PAIR) {
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
     } else {
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
     }
   }
 }
@@ -882,7 +964,12 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // blocks = CTAs (2 per pair tile when PAIR)
 template <int BN, bool IS_DW, bool PAIR, class P>
 void launch_tma(const P& p, int blocks, cudaStream_t s) {
-  using C = TCfg<BN, BN / (PAIR ? 2 : 1), IS_DW ? 32 : kTmaNtBk>;
+#ifdef RGB_EXP_NO_TMEM_A
+  constexpr bool TA = false;
+#else
+  constexpr bool TA = !IS_DW && kTmaNtBk == 32;
+#endif
+  using C = TCfg<BN, BN / (PAIR ? 2 : 1), IS_DW ? 32 : kTmaNtBk, TA>;
   static bool configured = false;
   auto k = tma_gemm_kernel<BN, IS_DW, PAIR, P>;
   if (!configured) {
@@ -930,9 +1017,12 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_const
   const size_t tile_floats = (size_t)BM * BN;
   if (chain_vec_ok(ch, N)) {
     const int64_t nq = (int64_t)M * (N / 4);
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t r = q / (N / 4);
-      const int c = (int)(q - r * (N / 4)) * 4;
+    if (nq >= (int64_t)UINT32_MAX) __trap();
+    const uint32_t w4 = (uint32_t)(N / 4);
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)nq; q += gridDim.x * blockDim.x) {
+      const uint32_t r32 = q / w4;
+      const int64_t r = r32;
+      const int c = (int)(q - r32 * w4) * 4;
       const int tl = cta_tile(p.pair != 0, t0, tiles_n, r, c / BN);
       const float* src = p.part + (size_t)tl * splits * tile_floats + (r % BM) * BN + (c % BN);
       float4 a = __ldcg(reinterpret_cast<const float4*>(src));
@@ -1138,7 +1228,7 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
 
 #ifdef RGB_EXP_TRACE
 extern "C" int rgb_exp_trace(long long* out) {
-  return cudaMemcpyFromSymbol(out, rgb::tc::g_trace, sizeof(rgb::tc::g_trace)) == cudaSuccess ? 0 : 3;
+  return cudaMemcpyFromSymbol(out, rgb::tc::g_trace, sizeof(rgb::tc::g_trace)) == cudaSuccess ? 0 : 3;  // [6][1024]
 }
 extern "C" int rgb_exp_cta(long long* out) {
   return cudaMemcpyFromSymbol(out, rgb::tc::g_cta, sizeof(rgb::tc::g_cta)) == cudaSuccess ? 0 : 3;

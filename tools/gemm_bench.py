@@ -52,14 +52,15 @@ def main():
         print(f"{shape}: {us:8.1f} us  {2 * m * n * k / us / 1e6:7.1f} TFLOP/s  err {err:.1e}")
         if hasattr(L, "rgb_exp_trace"):  # per-stage clock64 trace of CTA 0 (RGB_EXP_TRACE build)
             import numpy as np
-            buf = np.zeros((4, 1024), dtype=np.int64)
+            buf = np.zeros((6, 1024), dtype=np.int64)
             L.rgb_exp_trace(buf.ctypes.data_as(ctypes.c_void_p))
             nst = int((buf[0] != 0).sum())
             t0 = buf[0, 0]
             rel = (buf[:, :nst] - t0)
             print("  stages", nst, "done at", buf[3, 0] - t0)
             for it in list(range(0, min(nst, 12))) + list(range(max(12, nst - 4), nst)):
-                print(f"  it {it:4d} issue {rel[0, it]:8d} landed {rel[1, it]:8d} mma {rel[2, it]:8d}")
+                print(f"  it {it:4d} issue {rel[0, it]:8d} landed {rel[1, it]:8d} converted {rel[4, it]:8d} "
+                      f"fenced {rel[5, it]:8d} mma {rel[2, it]:8d}")
             cta = np.zeros((1024, 4), dtype=np.int64)
             L.rgb_exp_cta(cta.ctypes.data_as(ctypes.c_void_p))
             nc = int((cta[:, 0] != 0).sum())
