@@ -293,4 +293,15 @@ __device__ __forceinline__ void ew_apply_vec(const EwOp& op, int width, const in
   }
 }
 
+// the whole chain on R rows x 4 units; op 0 takes `acc` (GEMM epilogues).
+// Latency note: every op waits for its own operand loads, so the callers
+// give each thread as many rows (R) as registers allow -- one memory latency
+// per op covers all of them.
+template <int R>
+__device__ __forceinline__ void ew_chain_vec(const EwChain& ch, int width, const int64_t (&r)[R], int j,
+                                             const bool (&ok)[R], const RingWrite& ring, bool has_acc,
+                                             const float4 (&acc)[R]) {
+  for (int k = 0; k < ch.nops; ++k) ew_apply_vec<R>(ch.op[k], width, r, j, ok, ring, has_acc && k == 0, acc);
+}
+
 }  // namespace rgb

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ E
       const int j = (int)(q - r32 * (uint32_t)w4) * 4;
       const bool ok[1] = {true};
       const float4 acc[1] = {zero};
-      for (int k = 0; k < ch.nops; ++k) ew_apply_vec<1>(ch.op[k], ch.width, rr, j, ok, p.ring, false, acc);
+      ew_chain_vec<1>(ch, ch.width, rr, j, ok, p.ring, false, acc);
     }
     return;
   }

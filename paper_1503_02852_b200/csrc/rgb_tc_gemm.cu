@@ -39,16 +39,20 @@ namespace tc {
 // tuning aid: per-stage clock64 trace of CTA 0 (tools/build_exp.sh trace -DRGB_EXP_TRACE)
 #ifdef RGB_EXP_TRACE
 __device__ long long g_trace[6][1024];
-__device__ long long g_cta[1024][4];  // globaltimer: start, mainloop done, epilogue done; smid
+__device__ long long g_cta[1024][6];  // globaltimer: start, mainloop done, epilogue done; smid
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifndef RGB_EXP_TRACE_GRID
+#define RGB_EXP_TRACE_GRID 0  // trace only launches of this grid size (0: all)
+#endif
+#define TRACE_ON (RGB_EXP_TRACE_GRID == 0 || gridDim.x == RGB_EXP_TRACE_GRID)
 #define CTA_MARK(i) \
-  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta[blockIdx.x][i] = gtimer();
+  if (TRACE_ON && threadIdx.x == 0 && blockIdx.x < 1024) g_cta[blockIdx.x][i] = gtimer();
 #define TRACE(row, it) \
-  if (blockIdx.x == 0 && (it) < 1024) g_trace[row][it] = clock64();
+  if (TRACE_ON && blockIdx.x == 0 && (it) < 1024) g_trace[row][it] = clock64();
 #else
 #define TRACE(row, it)
 #define CTA_MARK(i)
@@ -278,13 +282,12 @@ __device__ __forceinline__ void find_job(const int* tile_start, int njobs, int b
 template <int BN, bool IS_DW, class P>
 __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, int M, int N, uint32_t tmem,
                                          float* tile_s, const EwChain* chain_s, int tid, int tile_lin, int split,
-                                         int splits) {
+                                         int splits, int r_lo = 0, int r_hi = BM, int phases = 3) {
   using C = Cfg<BN>;
   const int warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int r_loc = quarter * 32 + lane;
-#ifndef RGB_EXP_NOEPI1
-  for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
+  for (int cc = half * (BN / 2); (phases & 1) && cc < (half + 1) * (BN / 2); cc += 16) {
     if (n0 + cc >= N) break;  // warp-uniform
     float v[16];
     tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
@@ -294,11 +297,8 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     dst[2] = make_float4(v[8], v[9], v[10], v[11]);
     dst[3] = make_float4(v[12], v[13], v[14], v[15]);
   }
-#endif
-  asm volatile("bar.sync 1, 256;" ::: "memory");
-#ifdef RGB_EXP_NOEPI2
-  return;
-#endif
+  if (phases & 1) asm volatile("bar.sync 1, 256;" ::: "memory");
+  if (!(phases & 2)) return;  // cluster split-K: the caller reduces the partial tiles first
   if constexpr (!IS_DW) {
     if (splits > 1) {
       // split-K: publish this partial tile and stop; splitk_epilogue_kernel
@@ -314,8 +314,9 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     }
   }
   const int ncols = (N - n0) < BN ? (N - n0) : BN;
-  const int nrows = (M - m0) < BM ? (M - m0) : BM;
-  const int total = ncols * nrows;
+  // local rows [r_lo, nrows) of the tile (a row slice under cluster split-K)
+  const int nrows = min((M - m0) < BM ? (M - m0) : BM, r_hi);
+  const int total = ncols * max(nrows - r_lo, 0);
   constexpr int U = 8;
   float* g_out = nullptr;
   float alpha = 0.0f;
@@ -335,10 +336,10 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     constexpr int LPR = BN >= 128 ? 32 : BN / 4;  // lanes per row
     constexpr int RPW = 32 / LPR;                  // rows per warp access
     constexpr int CG = BN / 4 / LPR;               // float4 groups per lane per row
-    constexpr int R = 2;
+    constexpr int R = 4;  // rows per thread and pass: one operand latency per op covers 4 rows
     const int sub = lane / LPR, lc = lane % LPR;
 #pragma unroll 1
-    for (int rb = warp * RPW + sub; rb < nrows; rb += 8 * RPW * R) {
+    for (int rb = r_lo + warp * RPW + sub; rb < nrows; rb += 8 * RPW * R) {
 #pragma unroll
       for (int g = 0; g < CG; ++g) {
         const int cl = (g * LPR + lc) * 4;
@@ -361,7 +362,7 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
                   make_float4(alpha * acc[u].x, alpha * acc[u].y, alpha * acc[u].z, alpha * acc[u].w));
         } else {
           const EwChain& epi = *chain_s;
-          for (int k = 0; k < epi.nops; ++k) ew_apply_vec<R>(epi.op[k], N, rr, n0 + cl, ok, ring, k == 0, acc);
+          ew_chain_vec<R>(epi, N, rr, n0 + cl, ok, ring, true, acc);
         }
       }
     }
@@ -377,7 +378,7 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     for (int u = 0; u < U; ++u) {
       const int idx = base + tid + 256 * u;
       ok[u] = idx < total;
-      const int rl = ok[u] ? idx / ncols : 0, cl = ok[u] ? idx - (idx / ncols) * ncols : 0;
+      const int rl = r_lo + (ok[u] ? idx / ncols : 0), cl = ok[u] ? idx - (idx / ncols) * ncols : 0;
       rr[u] = m0 + rl;
       cc[u] = n0 + cl;
       acc[u] = tile_s[rl * C::EPI_LD + cl];
@@ -388,16 +389,7 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
         if (ok[u]) g_out[rr[u] * N + cc[u]] = alpha * acc[u];
     } else {
       const EwChain& epi = *chain_s;
-#if defined(RGB_EXP_PLAINSTORE)
-      float* o = epi.op[0].out;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (ok[u]) o[rr[u] * N + cc[u]] = acc[u];
-#elif defined(RGB_EXP_NOSTORE)
-      if (acc[0] == 12345.f) epi.op[0].out[0] = acc[1];
-#else
       for (int k = 0; k < epi.nops; ++k) ew_apply_batch<U>(epi.op[k], N, rr, cc, ok, ring, k == 0, acc);
-#endif
     }
   }
 }
@@ -618,6 +610,18 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// 16-byte load from the same shared-memory offset in cluster CTA `rank`
+__device__ __forceinline__ float4 ld_dsmem4(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
 // arrive on the mbarrier at the same smem offset in cluster CTA `rank`
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
@@ -687,11 +691,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   int jid, tile;
   // block -> (output tile, split, pair rank); the splits of one tile are adjacent
   const int blk = blockIdx.x / NCTA;
-  int splits = 1, split = 0, tile_lin = blk;
+  int splits = 1, split = 0, tile_lin = blk, csplit = 1;
   if constexpr (!IS_DW) {
     splits = p.splits > 1 ? p.splits : 1;
     split = blk % splits;
     tile_lin = blk / splits;
+    if (p.csplit) csplit = splits;  // splits reduced inside the cluster (no scratch)
   }
   find_job(p.tile_start, p.njobs, tile_lin, jid, tile);
   const auto& job = p.job[jid];
@@ -930,10 +935,39 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
     CTA_MARK(1)
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // split-K partial tiles are indexed by 128-row tile: pair tile * 2 + rank
+    // split-K partial tiles are indexed by 128-row tile: pair tile * 2 + rank;
+    // cluster split-K stops after staging the partial accumulator in smem
     epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, reinterpret_cast<float*>(smem), chain_s, threadIdx.x,
-                        tile_lin * NCTA + (int)rank, split, splits);
+                        tile_lin * NCTA + (int)rank, split, csplit > 1 ? 1 : splits, 0, BM, csplit > 1 ? 1 : 3);
     CTA_MARK(2)
+  }
+  if constexpr (!IS_DW && !PAIR) {
+    if (csplit > 1) {
+      // cluster split-K: the splits of this tile are one cluster; CTA `split`
+      // sums rows [split*BM/csplit, ...) of all partial tiles in split order
+      // through distributed shared memory and runs the epilogue on them
+      __syncwarp();
+      cluster_sync();
+      const int r_lo = split * BM / csplit, r_hi = (split + 1) * BM / csplit;
+      float* tile_s = reinterpret_cast<float*>(smem);
+      if (warp < 8) {
+        constexpr int G4 = BN / 4;
+        using CE = Cfg<BN>;
+        for (int q = threadIdx.x; q < (r_hi - r_lo) * G4; q += 256) {
+          const int off = (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4;
+          float4 a = ld_dsmem4(tile_s + off, 0);
+          for (int k = 1; k < csplit; ++k) a = add4(a, ld_dsmem4(tile_s + off, (uint32_t)k));
+          *reinterpret_cast<float4*>(tile_s + off) = a;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        CTA_MARK(3)
+        epilogue<BN, IS_DW>(p, jid, m0, n0, M, N, tmem, tile_s, chain_s, threadIdx.x, 0, 0, 1, r_lo, r_hi, 2);
+        CTA_MARK(4)
+      }
+      __syncwarp();
+      cluster_sync();  // peers are done reading this CTA's partial tile
+      CTA_MARK(5)
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if constexpr (PAIR) {
@@ -962,8 +996,399 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 }
 
 // blocks = CTAs (2 per pair tile when PAIR)
+// ---------------------------------------------------------------------------
+// Persistent form of the TMA kernel for launches of several waves: each CTA
+// (pair) walks output tiles blockIdx, blockIdx + grid, ...; the accumulator is
+// double-buffered in TMEM so that 4 dedicated epilogue warps drain tile i
+// while the producers, converters and MMA issuer already run tile i+1 (in the
+// one-tile kernel the epilogue was ~25% of every multi-wave launch).
+//   warps 0-7 converters, 8 TMA A, 9 MMA, 10 TMA B, 11-14 epilogue.
+// Barriers: per stage tma_full / conv_full / empty (as above), per
+// accumulator buffer tmem_full (MMA commit -> epilogue) and tmem_empty
+// (epilogue -> MMA).  The epilogue stages 32-column chunks of the tile in a
+// private smem slice (TMEM -> smem -> coalesced 16-byte row walk).
+constexpr int kPersThreads = 480;
+constexpr int kEpiLd = 36;  // padded chunk row (floats)
+
+template <int BN, int BNL>
+struct PCfg {
+  static constexpr int BK = 32;
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BNL * BK * 4;
+  static constexpr int B_OFF = 2 * A_BYTES;
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  static constexpr int CHUNK_BYTES = BM * kEpiLd * 4;
+  static constexpr int BUDGET = 227 * 1024 - 1024 - 512 - kChainBytes - CHUNK_BYTES;
+  static constexpr int RAW = BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = RAW > 8 ? 8 : RAW;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512 + kChainBytes + CHUNK_BYTES;
+  static_assert(STAGES >= 2, "persistent pipeline needs two stages");
+  static_assert(TMEM_COLS <= 512, "two accumulators must fit in TMEM");
+};
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// tile geometry shared by every role of the persistent kernel
 template <int BN, bool IS_DW, bool PAIR, class P>
-void launch_tma(const P& p, int blocks, cudaStream_t s) {
+struct PTile {
+  int jid, m0, n0, nb0, M, N, nstages;
+  __device__ __forceinline__ PTile(const P& p, int t, uint32_t rank) {
+    constexpr int NCTA = PAIR ? 2 : 1;
+    int tile;
+    find_job(p.tile_start, p.njobs, t, jid, tile);
+    const int tiles_n = p.tiles_n[jid];
+    m0 = (tile / tiles_n) * (BM * NCTA) + (int)rank * BM;
+    n0 = (tile % tiles_n) * BN;
+    nb0 = n0 + (int)rank * (BN / NCTA);
+    if constexpr (IS_DW) {
+      M = p.job[jid].m;
+      N = p.job[jid].n;
+      nstages = (p.k + 31) / 32;
+    } else {
+      M = p.rows;
+      N = p.job[jid].n;
+      nstages = 0;
+      for (int s = 0; s < p.job[jid].nseg; ++s) nstages += (p.job[jid].seg[s].k + 31) / 32;
+    }
+  }
+};
+
+template <int BN, bool IS_DW, bool PAIR, class P>
+__global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles) {
+  constexpr int NCTA = PAIR ? 2 : 1;
+  constexpr int BNL = BN / NCTA;
+  using C = PCfg<BN, BNL>;
+  constexpr int BK = C::BK;
+  constexpr int kBoxIdx = box_idx<BNL>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* conv_full = tma_full + C::STAGES;
+  uint64_t* empty = conv_full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 512);
+  float* chunk_s = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512 + kChainBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const int first = blockIdx.x / NCTA, stride = gridDim.x / NCTA;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&tma_full[s], 2);
+      mbar_init(&conv_full[s], PAIR ? 2 : kProducers);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], NCTA);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8 || warp == 10) {
+    if (lane == 0) {
+      // ---------------- TMA producers (A: warp 8, B: warp 10) ----------------
+      const bool load_a = warp == 8;
+      int g = 0;  // global stage counter
+      for (int t = first; t < ntiles; t += stride) {
+        const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+        const auto& job = p.job[T.jid];
+        int seg = 0, k0 = 0;
+        for (int it = 0; it < T.nstages; ++it, ++g) {
+          const int s = g % C::STAGES;
+          mbar_wait(&empty[s], ((g / C::STAGES) & 1) ^ 1);
+          uint8_t* base = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
+          if constexpr (IS_DW) {
+            if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, T.m0 / 32, &tma_full[s]);
+            else tma_load_3d(base + C::B_OFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, T.nb0 / 32, &tma_full[s]);
+            k0 += BK;
+          } else {
+            const Seg& sg = job.seg[seg];
+            if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + T.m0, &tma_full[s]);
+            else tma_load_2d(base + C::B_OFF, map_at(sg.tb, kBoxIdx), k0, T.nb0, &tma_full[s]);
+            k0 += BK;
+            if (k0 >= sg.k) {
+              k0 = 0;
+              ++seg;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+      int g = 0, ti = 0;
+      for (int t = first; t < ntiles; t += stride, ++ti) {
+        const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+        const int b = ti & 1;
+        if constexpr (PAIR) mbar_wait_cluster(&tmem_empty[b], ((ti >> 1) & 1) ^ 1);
+        else mbar_wait(&tmem_empty[b], ((ti >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * BN;
+        for (int it = 0; it < T.nstages; ++it, ++g) {
+          const int s = g % C::STAGES;
+          if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (g / C::STAGES) & 1);
+          else mbar_wait(&conv_full[s], (g / C::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
+          const uint32_t b_hi = base + C::B_OFF, b_lo = b_hi + C::B_BYTES;
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {
+            uint64_t dah, dal, dbh, dbl;
+            if constexpr (IS_DW) {
+              const uint32_t off = j * 1024;
+              dah = smem_desc(a_hi + off, 4096, 512, 1);
+              dal = smem_desc(a_lo + off, 4096, 512, 1);
+              dbh = smem_desc(b_hi + off, 4096, 512, 1);
+              dbl = smem_desc(b_lo + off, 4096, 512, 1);
+            } else {
+              const uint32_t off = j * 32;
+              dah = smem_desc(a_hi + off, 16, 1024, 2);
+              dal = smem_desc(a_lo + off, 16, 1024, 2);
+              dbh = smem_desc(b_hi + off, 16, 1024, 2);
+              dbl = smem_desc(b_lo + off, 16, 1024, 2);
+            }
+            const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+            if constexpr (PAIR) {
+              mma_tf32_pair(acc, dal, dbh, idesc, acc0);
+              mma_tf32_pair(acc, dah, dbl, idesc, 1u);
+              mma_tf32_pair(acc, dah, dbh, idesc, 1u);
+            } else {
+              mma_tf32(acc, dal, dbh, idesc, acc0);
+              mma_tf32(acc, dah, dbl, idesc, 1u);
+              mma_tf32(acc, dah, dbh, idesc, 1u);
+            }
+          }
+          if constexpr (PAIR) mma_commit_pair(&empty[s]);
+          else mma_commit(&empty[s]);
+        }
+        if constexpr (PAIR) mma_commit_pair(&tmem_full[b]);
+        else mma_commit(&tmem_full[b]);
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------- converters ----------------
+    int g = 0;
+    for (int t = first; t < ntiles; t += stride) {
+      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+      for (int it = 0; it < T.nstages; ++it, ++g) {
+        const int s = g % C::STAGES;
+        mbar_wait(&tma_full[s], (g / C::STAGES) & 1);
+        uint8_t* base = smem + s * C::STAGE_BYTES;
+        const float4* a_hi = reinterpret_cast<const float4*>(base);
+        float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
+#pragma unroll
+        for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
+          const int q = threadIdx.x + i * kProducers;
+          const float4 x = a_hi[q];
+          a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        }
+        const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
+        float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
+#pragma unroll
+        for (int i = 0; i < C::B_BYTES / 16 / kProducers; ++i) {
+          const int q = threadIdx.x + i * kProducers;
+          const float4 x = b_hi[q];
+          b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if constexpr (PAIR) {
+          asm volatile("bar.sync 2, 256;" ::: "memory");
+          if (threadIdx.x == 0) {
+            if (rank == 0) mbar_arrive(&conv_full[s]);
+            else mbar_arrive_cluster(&conv_full[s], 0);
+          }
+        } else {
+          mbar_arrive(&conv_full[s]);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 11-14 ----------------
+    const int et = threadIdx.x - 11 * 32;  // 0..127
+    const int quarter = warp & 3;          // TMEM lane quarter this warp may read
+    const int r_loc = quarter * 32 + lane;
+    int ti = 0, staged_job = -1;
+    for (int t = first; t < ntiles; t += stride, ++ti) {
+      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+      const int b = ti & 1;
+      if constexpr (!IS_DW) {
+        if (T.jid != staged_job) {  // the chain of this tile's job
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          stage_chain(chain_s, p.job[T.jid].epi, et, 128);
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          staged_job = T.jid;
+        }
+      }
+      mbar_wait(&tmem_full[b], (ti >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t acc = tmem + b * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int ncols = (T.N - T.n0) < BN ? (T.N - T.n0) : BN;
+      const int nrows = (T.M - T.m0) < BM ? (T.M - T.m0) : BM;
+      bool vec;
+      float* g_out = nullptr;
+      if constexpr (IS_DW) {
+        g_out = p.job[T.jid].g;
+        vec = T.N % 4 == 0 && aligned16(g_out);
+      } else {
+        vec = chain_vec_ok(*chain_s, T.N);
+      }
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        float v[32];
+        tmem_ld32(acc + c0, v);
+        if (c0 + 32 >= ncols) {
+          // last TMEM read of this buffer: hand it back to the MMA issuer
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          if (et == 0) {
+            if (rank == 0) mbar_arrive(&tmem_empty[b]);
+            else mbar_arrive_cluster(&tmem_empty[b], 0);
+          }
+        }
+        float4* dst = reinterpret_cast<float4*>(chunk_s + r_loc * kEpiLd);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        const int cw = (ncols - c0) < 32 ? (ncols - c0) : 32;
+        if (vec) {
+          // 8 lanes per row (16-byte groups), 16 rows per pass, RE rows per thread
+          constexpr int RE = 2;
+          const int sub = et >> 3, lc = et & 7, cl = lc * 4;
+          if (cl < cw) {
+#pragma unroll 1
+            for (int rb = sub; rb < nrows; rb += 16 * RE) {
+              int64_t rr[RE];
+              bool ok[RE];
+              float4 a[RE];
+#pragma unroll
+              for (int u = 0; u < RE; ++u) {
+                const int rl = rb + 16 * u;
+                ok[u] = rl < nrows;
+                rr[u] = T.m0 + (ok[u] ? rl : 0);
+                a[u] = *reinterpret_cast<const float4*>(chunk_s + (ok[u] ? rl : 0) * kEpiLd + cl);
+              }
+              if constexpr (IS_DW) {
+#pragma unroll
+                for (int u = 0; u < RE; ++u)
+                  if (ok[u])
+                    st4(g_out, rr[u] * T.N + T.n0 + c0 + cl,
+                        make_float4(p.alpha * a[u].x, p.alpha * a[u].y, p.alpha * a[u].z, p.alpha * a[u].w));
+              } else {
+                const RingWrite ring = p.ring;
+                ew_chain_vec<RE>(*chain_s, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a);
+              }
+            }
+          }
+        } else {
+          for (int e = et; e < nrows * cw; e += 128) {
+            const int rl = e / cw, cl = e - rl * cw;
+            const float a = chunk_s[rl * kEpiLd + cl];
+            const int64_t r = T.m0 + rl;
+            const int c = T.n0 + c0 + cl;
+            if constexpr (IS_DW) {
+              p.job[T.jid].g[r * T.N + c] = p.alpha * a;
+            } else {
+              const RingWrite ring = p.ring;
+              for (int k = 0; k < chain_s->nops; ++k) ew_apply(chain_s->op[k], T.N, r, c, ring, k == 0, a);
+            }
+          }
+        }
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+      }
+      if (ncols <= 0) {  // (cannot happen: tiles cover N) keep the barrier protocol intact
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (et == 0) {
+          if (rank == 0) mbar_arrive(&tmem_empty[b]);
+          else mbar_arrive_cluster(&tmem_empty[b], 0);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
+  if (warp == 9) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+    }
+  }
+}
+
+// ntiles output tiles (pair tiles when PAIR) over min(ntiles, SMs/NCTA) CTAs / pairs
+template <int BN, bool IS_DW, bool PAIR, class P>
+void launch_persistent(const P& p, int ntiles, cudaStream_t s) {
+  using C = PCfg<BN, BN / (PAIR ? 2 : 1)>;
+  static bool configured = false;
+  auto k = tma_gemm_persistent<BN, IS_DW, PAIR, P>;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int units = PAIR ? sms / 2 : sms;
+  const int blocks = (ntiles < units ? ntiles : units) * (PAIR ? 2 : 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kPersThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = PAIR ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, p, ntiles);
+}
+
+template <int BN, bool IS_DW, bool PAIR, class P>
+void launch_tma(const P& p, int blocks, cudaStream_t s, int cluster = 1) {
 #ifdef RGB_EXP_NO_TMEM_A
   constexpr bool TA = false;
 #else
@@ -976,7 +1401,7 @@ void launch_tma(const P& p, int blocks, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     configured = true;
   }
-  if constexpr (PAIR) {
+  if (PAIR || cluster > 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(kTmaThreads);
@@ -984,7 +1409,7 @@ void launch_tma(const P& p, int blocks, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = PAIR ? 2 : cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -1030,7 +1455,7 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_const
       const int64_t rr[1] = {r};
       const bool ok[1] = {true};
       const float4 acc[1] = {a};
-      for (int k = 0; k < ch.nops; ++k) ew_apply_vec<1>(ch.op[k], N, rr, c, ok, ring, k == 0, acc);
+      ew_chain_vec<1>(ch, N, rr, c, ok, ring, true, acc);
     }
   } else {
     const int64_t ne = (int64_t)M * N;
@@ -1141,23 +1566,48 @@ long long nt_scratch(const GemmGroup& p, const NtConfig& c) {
   return c.splits > 1 ? (long long)nt_tiles(p, c.bn, c.pair) * (c.pair ? 2 : 1) * c.splits * tc::BM * c.bn : 0;
 }
 
-template <bool PAIR>
-void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s) {
-  if (bn == 256) tc::launch_tma<256, false, PAIR>(p, blocks, s);
-  else if (bn == 128) tc::launch_tma<128, false, PAIR>(p, blocks, s);
-  else if constexpr (!PAIR) {
-    if (bn == 64) tc::launch_tma<64, false, false>(p, blocks, s);
-    else tc::launch_tma<32, false, false>(p, blocks, s);
+bool persist_enabled() {  // RGB_TC_PERSIST=0 disables the persistent kernels (tuning experiments)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RGB_TC_PERSIST");
+    on = e ? atoi(e) != 0 : 1;
   }
+  return on == 1;
+}
+
+// persistent kernel for launches of at least two waves
+bool use_persistent(int blocks, int bn) { return persist_enabled() && blocks >= 2 * 148 && bn >= 128; }
+
+template <bool PAIR>
+void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s, int cluster = 1) {
+  if (bn == 256) tc::launch_tma<256, false, PAIR>(p, blocks, s, cluster);
+  else if (bn == 128) tc::launch_tma<128, false, PAIR>(p, blocks, s, cluster);
+  else if constexpr (!PAIR) {
+    if (bn == 64) tc::launch_tma<64, false, false>(p, blocks, s, cluster);
+    else tc::launch_tma<32, false, false>(p, blocks, s, cluster);
+  }
+}
+
+bool csplit_enabled() {  // RGB_TC_CSPLIT=0: split-K through global partials + fixup kernel (experiments)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RGB_TC_CSPLIT");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
 }
 
 }  // namespace
 
-long long tc_gemm_nt_scratch(const GemmGroup& p) { return nt_scratch(p, nt_config(p)); }
+long long tc_gemm_nt_scratch(const GemmGroup& p) {
+  const NtConfig c = nt_config(p);
+  return csplit_enabled() && !c.pair ? 0 : nt_scratch(p, c);
+}
 
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   NtConfig c = nt_config(p);
-  if (c.splits > 1 && (!p.part || nt_scratch(p, c) > p.part_cap)) c.splits = 1;  // no (or too small a) scratch
+  p.csplit = c.splits > 1 && !c.pair && csplit_enabled() ? 1 : 0;
+  if (c.splits > 1 && !p.csplit && (!p.part || nt_scratch(p, c) > p.part_cap)) c.splits = 1;  // no scratch
   if (!p.tma) c = NtConfig{tc::pick_bn([&](int b) { return nt_tiles(p, b, false); }), 1, false};
   p.splits = c.splits;
   p.pair = c.pair ? 1 : 0;
@@ -1169,16 +1619,25 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   }
   const int blocks = p.tile_start[p.njobs] * c.splits * (c.pair ? 2 : 1);
   if (blocks == 0) return 0;
-  if (p.tma) {
+  if (p.tma && c.splits == 1 && use_persistent(blocks, c.bn)) {
+    const int ntiles = p.tile_start[p.njobs];
+    if (c.pair) {
+      if (c.bn == 256) tc::launch_persistent<256, false, true>(p, ntiles, s);
+      else tc::launch_persistent<128, false, true>(p, ntiles, s);
+    } else {
+      if (c.bn == 256) tc::launch_persistent<256, false, false>(p, ntiles, s);
+      else tc::launch_persistent<128, false, false>(p, ntiles, s);
+    }
+  } else if (p.tma) {
     if (c.pair) launch_nt_bn<true>(p, c.bn, blocks, s);
-    else launch_nt_bn<false>(p, c.bn, blocks, s);
+    else launch_nt_bn<false>(p, c.bn, blocks, s, p.csplit ? c.splits : 1);
   } else {
     if (c.bn == 256) tc::launch_one<256, false>(p, blocks, s);
     else if (c.bn == 128) tc::launch_one<128, false>(p, blocks, s);
     else if (c.bn == 64) tc::launch_one<64, false>(p, blocks, s);
     else tc::launch_one<32, false>(p, blocks, s);
   }
-  if (c.splits == 1) return 1;
+  if (c.splits == 1 || p.csplit) return 1;
   int64_t maxq = 0;
   for (int j = 0; j < p.njobs; ++j) maxq = std::max<int64_t>(maxq, (int64_t)p.rows * p.job[j].n);
   maxq = (maxq + 3) / 4;
@@ -1206,7 +1665,16 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   }
   const int blocks = p.tile_start[p.njobs] * (pair ? 2 : 1);
   if (blocks == 0) return;
-  if (p.tma) {
+  if (p.tma && use_persistent(blocks, bn)) {
+    const int ntiles = p.tile_start[p.njobs];
+    if (pair) {
+      if (bn == 256) tc::launch_persistent<256, true, true>(p, ntiles, s);
+      else tc::launch_persistent<128, true, true>(p, ntiles, s);
+    } else {
+      if (bn == 256) tc::launch_persistent<256, true, false>(p, ntiles, s);
+      else tc::launch_persistent<128, true, false>(p, ntiles, s);
+    }
+  } else if (p.tma) {
     if (pair) {
       if (bn == 256) tc::launch_tma<256, true, true>(p, blocks, s);
       else tc::launch_tma<128, true, true>(p, blocks, s);

@@ -95,6 +95,7 @@ struct GemmGroup {
   long long part_cap;  // floats
   int splits;          // set by launch_tc_gemm_nt
   int pair;            // 1: CTA-pair (cta_group::2) tiles of 256 rows
+  int csplit;          // 1: the splits of a tile form a cluster and reduce through DSMEM
 };
 
 struct EwLaunch {
