@@ -362,12 +362,23 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
                   make_float4(alpha * acc[u].x, alpha * acc[u].y, alpha * acc[u].z, alpha * acc[u].w));
         } else {
           const EwChain& epi = *chain_s;
+#ifdef RGB_EXP_TRACE
+          if (threadIdx.x == 0) { TRACE(3, 16) }
+          for (int k = 0; k < epi.nops; ++k) {
+            ew_apply_vec<R>(epi.op[k], N, rr, n0 + cl, ok, ring, k == 0, acc);
+            if (threadIdx.x == 0) { TRACE(3, 17 + k) }
+          }
+#else
           ew_chain_vec<R>(epi, N, rr, n0 + cl, ok, ring, true, acc);
+#endif
         }
       }
     }
     return;
   }
+#ifdef RGB_EXP_TRACE
+  if (tid == 0) { TRACE(3, 15) }
+#endif
 #pragma unroll 1
   for (int base = 0; base < total; base += 256 * U) {
     int64_t rr[U];

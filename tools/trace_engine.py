@@ -41,6 +41,11 @@ def main():
     print("stages", nst)
     for it in range(nst):
         print(f"  it {it:4d} issue {rel[0, it]:8d} landed {rel[1, it]:8d} converted {rel[4, it]:8d} mma {rel[2, it]:8d}")
+    print("scalar epilogue path taken" if buf[3, 15] else "vector epilogue path")
+    ops = buf[3, 16:24]
+    ops = ops[ops != 0]
+    if len(ops) > 1:
+        print("epilogue ops (cycles, CTA 0 thread 0):", np.diff(ops).tolist())
     cta = np.zeros((1024, 6), dtype=np.int64)
     L.rgb_exp_cta(cta.ctypes.data_as(ctypes.c_void_p))
     nc = int((cta[:, 0] != 0).sum())
