@@ -361,8 +361,19 @@ def run_ours(args, cfg):
     else:
         achieved = p["bytes"] / p["launches"] / per_launch_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm}
-    roof.update({"traffic": None, "kernel": top, "peak_source": peak_src + " (MEASURED_PEAKS.json)",
+    traffic = None
+    tpath = os.path.join(HERE, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):  # committed ncu --set full capture (dram read + write per launch)
+        with open(tpath) as f:
+            traffic = json.load(f).get(top, {}).get("dram_bytes_per_launch")
+    roof.update({"traffic": traffic, "kernel": top, "peak_source": peak_src + " (MEASURED_PEAKS.json)",
                  "share_of_step": p["ms"] / sum(v["ms"] for v in prof.values())})
+    if roof["bound"] == "tensor":
+        # fp32 work on tensor cores is 3xTF32: three tf32 MMAs (half the bf16
+        # rate) per fp32 product, so the ceiling for this dtype is peak / 6
+        roof["fp32_emulation"] = "3xTF32"
+        roof["fp32_ceiling"] = tflops / 6.0
+        roof["frac_of_fp32_ceiling"] = achieved / (tflops / 6.0)
     F_iter = algorithmic_flops(net, S_total, h, hp)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
