@@ -127,8 +127,12 @@ int rgb_set_scc_mode(int on);
  * 2 tcgen05. */
 int rgb_gemm_nt(const float* a, const float* b, float* c, int m, int n, int k, int mode, void* stream);
 int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, float alpha, int mode, void* stream);
+/* mode 3 of rgb_gemm_dw: the TMA-fed tcgen05 kernels (m, n multiples of 32). */
 /* TMA-fed tcgen05 form of rgb_gemm_nt; b_lo = b - trunc_tf32(b) (k % 4 == 0). */
 int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c, int m, int n, int k, void* stream);
+/* Tensor-core kernel variants for A/B tests (1 on, 0 off, -1 unchanged): CTA
+ * pairs (cta_group::2), persistent multi-wave kernels, cluster split-K. */
+int rgb_set_tc_config(int pair, int persist, int csplit);
 
 /* Instrumentation (no reference counterpart; the reference times whole
  * iterations with perf_counter, engine.py:733-758).  rgb_launch_count: kernel

@@ -53,6 +53,7 @@ _SIGS = {
     "rgb_gemm_nt": ([_P, _P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_gemm_dw": ([_P, _P, _P, _I, _I, _I, ctypes.c_float, _I, _P], _I),
     "rgb_gemm_nt_tma": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),
+    "rgb_set_tc_config": ([_I, _I, _I], _I),
     "rgb_launch_count": ([ctypes.POINTER(_I64)], _I),
     "rgb_profile_enable": ([_I], _I),
     "rgb_profile_collect": ([], _I),

@@ -40,6 +40,9 @@ int launch_dw_narrow(const DwGroup& p, float* part, cudaStream_t s);
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s);
 // split-K scratch (floats) the TMA NT kernel would use for this group (0 = no split)
 long long tc_gemm_nt_scratch(const GemmGroup& p);
+// tensor-core kernel variants (1 on, 0 off, -1 unchanged): CTA pairs,
+// persistent multi-wave kernels, cluster (DSMEM) split-K
+void set_tc_config(int pair, int persist, int csplit);
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s);
 void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.

@@ -898,8 +898,13 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
   return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
 }
 
+int rgb_set_tc_config(int pair, int persist, int csplit) {
+  set_tc_config(pair, persist, csplit);
+  return RGB_OK;
+}
+
 int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, float alpha, int mode, void* stream) {
-  if (!e || !y || !g || m < 1 || n < 1 || k < 1 || mode < 1 || mode > 2) return fail(RGB_ERR_KERNEL, "bad arguments");
+  if (!e || !y || !g || m < 1 || n < 1 || k < 1 || mode < 1 || mode > 3) return fail(RGB_ERR_KERNEL, "bad arguments");
   DwGroup D;
   std::memset(&D, 0, sizeof D);
   D.njobs = 1;
@@ -909,6 +914,28 @@ int rgb_gemm_dw(const float* e, const float* y, float* g, int m, int n, int k, f
   D.tiles_n[0] = (n + 63) / 64;
   D.tile_start[1] = ((m + 63) / 64) * D.tiles_n[0];
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (mode == 3) {
+    // TMA-fed form: 3-D MN-major maps of E [k x m] and Y [k x n] (4 box variants each)
+    static CUtensorMap* dmaps = nullptr;
+    if (!dmaps && cudaMalloc(&dmaps, 8 * sizeof(CUtensorMap)) != cudaSuccess) return fail(RGB_ERR_CUDA, "alloc");
+    CUtensorMap hm[8];
+    bool ok = true;
+    for (int q = 0; q < 4; ++q) {
+      ok = ok && encode_map_mn(&hm[q], e, k, m, 1u << q);
+      ok = ok && encode_map_mn(&hm[4 + q], y, k, n, 1u << q);
+    }
+    if (!ok) return fail(RGB_ERR_KERNEL, "operands not TMA-compatible (m, n %% 32, 16-B alignment)");
+    if (cudaMemcpyAsync(dmaps, hm, sizeof hm, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return fail(RGB_ERR_CUDA, "map upload");
+    D.tma = 1;
+    D.job[0].te = dmaps;
+    D.job[0].ty = dmaps + 4;
+    launch_tc_gemm_dw(D, st);
+    note_launch();
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "dW launch: %s", cudaGetErrorString(err));
+  }
   if (mode == 2) launch_tc_gemm_dw(D, st);
   else launch_gemm_dw(D, st);
   note_launch();

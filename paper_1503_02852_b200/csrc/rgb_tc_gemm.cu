@@ -1500,8 +1500,10 @@ int pick_bn(F tiles_for) {
 
 namespace {
 
-bool pair_enabled() {  // RGB_TC_PAIR=0 disables the CTA-pair kernels (tuning experiments)
-  static int on = -1;
+int g_tc_opt[3] = {-1, -1, -1};  // pair, persistent, cluster split-K (-1: from the environment)
+
+bool pair_enabled() {  // RGB_TC_PAIR=0 disables the CTA-pair kernels (tuning experiments); rgb_set_tc_config overrides
+  int& on = g_tc_opt[0];
   if (on < 0) {
     const char* e = getenv("RGB_TC_PAIR");
     on = e ? atoi(e) != 0 : 1;
@@ -1577,8 +1579,8 @@ long long nt_scratch(const GemmGroup& p, const NtConfig& c) {
   return c.splits > 1 ? (long long)nt_tiles(p, c.bn, c.pair) * (c.pair ? 2 : 1) * c.splits * tc::BM * c.bn : 0;
 }
 
-bool persist_enabled() {  // RGB_TC_PERSIST=0 disables the persistent kernels (tuning experiments)
-  static int on = -1;
+bool persist_enabled() {  // RGB_TC_PERSIST=0 disables the persistent kernels (tuning experiments); rgb_set_tc_config overrides
+  int& on = g_tc_opt[1];
   if (on < 0) {
     const char* e = getenv("RGB_TC_PERSIST");
     on = e ? atoi(e) != 0 : 1;
@@ -1599,8 +1601,8 @@ void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s, int cl
   }
 }
 
-bool csplit_enabled() {  // RGB_TC_CSPLIT=0: split-K through global partials + fixup kernel (experiments)
-  static int on = -1;
+bool csplit_enabled() {  // RGB_TC_CSPLIT=0: split-K through global partials + fixup kernel (experiments); rgb_set_tc_config overrides
+  int& on = g_tc_opt[2];
   if (on < 0) {
     const char* e = getenv("RGB_TC_CSPLIT");
     on = e ? atoi(e) != 0 : 1;
@@ -1703,6 +1705,14 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   }
 }
 
+}  // namespace rgb
+
+namespace rgb {
+void set_tc_config(int pair, int persist, int csplit) {
+  if (pair >= 0) g_tc_opt[0] = pair != 0;
+  if (persist >= 0) g_tc_opt[1] = persist != 0;
+  if (csplit >= 0) g_tc_opt[2] = csplit != 0;
+}
 }  // namespace rgb
 
 #ifdef RGB_EXP_TRACE
