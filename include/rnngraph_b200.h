@@ -79,6 +79,9 @@ int rgb_inject_output_error(rgb_plan* plan, const void* target, int target_kind,
                             int criterion, int frames, void* stream);
 /* Read the last loss (synchronises the stream). */
 int rgb_read_loss(rgb_plan* plan, double* loss, void* stream);
+/* Enqueue the copy of the last loss into `dst` (pinned host or device memory)
+ * without synchronising; the caller waits on the stream / an event. */
+int rgb_read_loss_async(rgb_plan* plan, double* dst, void* stream);
 /* Copy the plan's injection buffer rows in/out (frames*S, n_out), device
  * pointers; used when the caller supplies its own delta_out. */
 int rgb_set_injection(rgb_plan* plan, const float* delta_out, int frames, void* stream);

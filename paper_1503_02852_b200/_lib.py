@@ -39,6 +39,7 @@ _SIGS = {
     "rgb_forward_chunk": ([_P, _P, _P, _I, _I, _I, _P], _I),
     "rgb_inject_output_error": ([_P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_read_loss": ([_P, ctypes.POINTER(ctypes.c_double), _P], _I),
+    "rgb_read_loss_async": ([_P, _P, _P], _I),
     "rgb_set_injection": ([_P, _P, _I, _P], _I),
     "rgb_get_injection": ([_P, _P, _I, _P], _I),
     "rgb_backward_window": ([_P, _P, _P, _I, _I, _I, _P], _I),

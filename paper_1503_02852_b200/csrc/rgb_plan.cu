@@ -1088,6 +1088,12 @@ int rgb_read_loss(rgb_plan* p, double* loss, void* stream) {
   return cuda_rc(cudaStreamSynchronize(st), "loss sync");
 }
 
+int rgb_read_loss_async(rgb_plan* p, double* dst, void* stream) {
+  if (!p || !p->ws || !dst) return fail(RGB_ERR_KERNEL, "null argument");
+  return cuda_rc(cudaMemcpyAsync(dst, p->ws + p->loss_off(), sizeof(double), cudaMemcpyDefault, as_stream(stream)),
+                 "loss copy");
+}
+
 int rgb_set_injection(rgb_plan* p, const float* d, int frames, void* stream) {
   if (!p || !p->ws || !d) return fail(RGB_ERR_KERNEL, "null argument");
   if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "bad frame count %d", frames);

@@ -634,14 +634,61 @@ class Trainer:
         self._graphs = {}
         self._exchange = exchange
         self._cap = self.state.program.layout.cap
+        # double-buffered staging of host inputs on a copy stream
+        self._copy_stream = torch.cuda.Stream(device=dev)
+        self._stage = [(torch.empty_like(self.gx), torch.empty_like(self.gt)) for _ in range(2)]
+        self._stage_free = [torch.cuda.Event() for _ in range(2)]
+        self._stage_ready = [torch.cuda.Event() for _ in range(2)]
+        self._stage_next = 0
+        self._staged = None
+        self._loss_host = torch.zeros(2, dtype=torch.float64).pin_memory()
+        self._loss_slot = 0
 
     def graph_inputs(self):
         """(x, targets) device buffers the next graphed step reads."""
         return self.gx, self.gt
 
+    def stage_inputs(self, inputs: torch.Tensor, targets: torch.Tensor) -> None:
+        """Start the host->device copy of the NEXT graphed iteration's inputs
+        (pinned host tensors) on a copy stream, overlapping the running
+        iteration; ``step_graphed`` consumes them."""
+        k = self._stage_next
+        sx, stt = self._stage[k]
+        with torch.cuda.stream(self._copy_stream):
+            self._copy_stream.wait_event(self._stage_free[k])  # previous consumer of this slot
+            sx.copy_(inputs, non_blocking=True)
+            stt.copy_(targets, non_blocking=True)
+            self._stage_ready[k].record(self._copy_stream)
+        self._staged = k
+        self._stage_next = 1 - k
+
+    def loss_async(self):
+        """Enqueue the read-back of this iteration's loss; returns a callable
+        that waits for it and returns the float."""
+        slot = self._loss_slot
+        self._loss_slot = 1 - slot
+        dst = self._loss_host[slot:slot + 1]
+        _lib.check(self._lib.rgb_read_loss_async(self.state._plan.handle, ctypes.c_void_p(dst.data_ptr()),
+                                                 self._stream()))
+        ev = torch.cuda.Event()
+        ev.record()
+
+        def wait() -> float:
+            ev.synchronize()
+            return float(dst[0])
+        return wait
+
     def step_graphed(self) -> None:
         """One iteration on (graph_inputs()), replayed from a captured graph."""
         hp = self.cfg.h_prime
+        if self._staged is not None:  # inputs staged by stage_inputs: device-to-device into the graph buffers
+            k = self._staged
+            cur = torch.cuda.current_stream()
+            cur.wait_event(self._stage_ready[k])
+            self.gx.copy_(self._stage[k][0], non_blocking=True)
+            self.gt.copy_(self._stage[k][1], non_blocking=True)
+            self._stage_free[k].record(cur)
+            self._staged = None
         if not self._graphs and not getattr(self, "_graph_warm", False):
             # first call runs eagerly: it builds the tensor maps and SCC plans
             # (host-synchronous work that must not happen inside a capture)

@@ -276,6 +276,37 @@ def test_graph_replay_equals_eager(net_fn, S):
     assert len(tb._graphs) == tb._cap // 4
 
 
+def test_staged_inputs_and_async_loss_equal_eager():
+    """Host inputs staged on the copy stream one iteration ahead and losses read
+    back one iteration late (the e2e loop of bench.py) give the eager results."""
+    net = P.build_lstm(16, 32, 8)
+    S = 8
+    cfg = P.TrainConfig(h=8, h_prime=4, lr=0.02, iterations=1)
+    wa, wb = P.Weights.init(net, 4), P.Weights.init(net, 4)
+    ta, tb = P.Trainer(net, wa, S, cfg), P.Trainer(net, wb, S, cfg)
+    tb.enable_graphs()
+    rng = np.random.default_rng(1)
+    xs = [torch.tensor(rng.uniform(-1, 1, size=(4 * S, 16)), dtype=torch.float32).pin_memory() for _ in range(7)]
+    ts = [torch.tensor(rng.integers(0, 8, size=4 * S)).pin_memory() for _ in range(7)]
+    want = []
+    for x, t in zip(xs, ts):
+        ta.step(x.cuda(), t.cuda())
+        want.append(ta.loss())
+    got, pending = [], None
+    tb.stage_inputs(xs[0], ts[0])
+    for i in range(7):
+        tb.step_graphed()
+        fut = tb.loss_async()
+        if i + 1 < 7:
+            tb.stage_inputs(xs[i + 1], ts[i + 1])
+        if pending is not None:
+            got.append(pending())
+        pending = fut
+    got.append(pending())
+    assert got == want
+    assert torch.equal(wa.flat, wb.flat)
+
+
 def test_train_loop_matches_oracle_training():
     """train_loop (fused inject + lazy loss) tracks the oracle's SGD run."""
     net = P.build_lstm(6, 12, 6)
