@@ -12,8 +12,8 @@ from .netdef import (Activation, Aggregation, ConnectionDef, LayerDef, NetdefErr
 from .condense import CondensedGraph, SuperNode, condense, export_dot, schedule_text, tarjan_scc
 from .builders import build_custom_graph, build_elman, build_lstm, build_stacked_lstm, count_params
 from .schedule import EngineError, build_program
-from .engine import (Batch, BpttWindow, Criterion, GradStore, IterationMetrics, StreamState, TrainConfig, Trainer,
-                     Weights, backward_window, forward_chunk, inject_output_error, loss_value, sgd_update,
-                     train_loop)
+from .engine import (Batch, BpttWindow, CheckpointError, Criterion, GradStore, IterationMetrics, StreamState,
+                     TrainConfig, Trainer, Weights, backward_window, forward_chunk, inject_output_error,
+                     load_checkpoint, loss_value, save_checkpoint, sgd_update, structure_hash, train_loop)
 
 __version__ = "0.1.0"

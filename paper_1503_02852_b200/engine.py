@@ -22,7 +22,9 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import hashlib
 import math
+import struct
 import time
 from dataclasses import dataclass, field
 from typing import Protocol
@@ -32,7 +34,7 @@ import torch
 
 from . import _lib
 from .condense import CondensedGraph, condense
-from .netdef import Activation, NetworkDef, Role, infer_shapes
+from .netdef import Activation, NetworkDef, Role, infer_shapes, save_network
 from .schedule import EngineError, build_program, weight_offsets, weights_program
 
 __all__ = [
@@ -516,6 +518,78 @@ def sgd_update(weights: Weights, grads: GradStore, lr: float) -> None:
         raise EngineError(f"learning rate must be positive, got {lr}")
     _lib.check(_lib.lib().rgb_sgd_update(weights._plan.handle, _ptr(weights.flat), _ptr(weights.flat_t),
                                          _ptr(grads.flat), ctypes.c_float(lr), _stream()))
+
+
+# ---------------------------------------------------------------------------
+# checkpoints (reference engine.py:615-665; same RNNG v1 byte format, so files
+# move between the two implementations)
+
+
+class CheckpointError(EngineError):
+    """Mirror of the reference ``CheckpointError`` (engine.py:90)."""
+
+
+_CKPT_MAGIC = b"RNNG"
+_CKPT_VERSION = 1
+
+
+def structure_hash(net: NetworkDef) -> bytes:
+    """First 8 bytes of SHA-256 over the canonical network document."""
+    return hashlib.sha256(save_network(net).encode()).digest()[:8]
+
+
+def save_checkpoint(path: str, net: NetworkDef, weights: Weights) -> None:
+    """Header (magic, version, structure hash, count) then, per dense
+    connection in ascending id, (id, rows, cols) and the matrix as
+    little-endian float64 (fp32 values widen exactly)."""
+    mats = weights.numpy()
+    parts = [_CKPT_MAGIC, struct.pack("<I", _CKPT_VERSION), structure_hash(net), struct.pack("<I", len(mats))]
+    for cid in sorted(mats):
+        m = np.asarray(mats[cid], dtype="<f8")
+        parts.append(struct.pack("<III", cid, m.shape[0], m.shape[1]))
+        parts.append(np.ascontiguousarray(m).tobytes())
+    with open(path, "wb") as fh:
+        fh.write(b"".join(parts))
+
+
+def load_checkpoint(path: str, net: NetworkDef) -> Weights:
+    """Read an RNNG v1 file into device weights (float64 -> fp32)."""
+    return Weights(net, read_checkpoint(path, net))
+
+
+def read_checkpoint(path: str, net: NetworkDef) -> dict:
+    """Parse and validate an RNNG v1 file: {connection id: float64 matrix}."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    pos = 0
+
+    def take(n: int) -> bytes:
+        nonlocal pos
+        if pos + n > len(blob):
+            raise CheckpointError(f"{path}: truncated checkpoint")
+        out = blob[pos:pos + n]
+        pos += n
+        return out
+
+    if take(4) != _CKPT_MAGIC:
+        raise CheckpointError(f"{path}: not a checkpoint file")
+    (version,) = struct.unpack("<I", take(4))
+    if version != _CKPT_VERSION:
+        raise CheckpointError(f"{path}: unsupported version {version}")
+    if take(8) != structure_hash(net):
+        raise CheckpointError(f"{path}: checkpoint belongs to a different network structure")
+    shapes = infer_shapes(net)
+    (count,) = struct.unpack("<I", take(4))
+    mats: dict[int, np.ndarray] = {}
+    for _ in range(count):
+        cid, rows, cols = struct.unpack("<III", take(12))
+        if shapes.get(cid) != (rows, cols):
+            raise CheckpointError(f"{path}: connection {cid} has shape {(rows, cols)}")
+        mats[cid] = np.frombuffer(take(rows * cols * 8), dtype="<f8").reshape(rows, cols)
+    want = {c.id for c in net.iter_dense()}
+    if set(mats) != want:
+        raise CheckpointError(f"{path}: connection ids {sorted(mats)} != network {sorted(want)}")
+    return mats
 
 
 # ---------------------------------------------------------------------------

@@ -336,3 +336,20 @@ def test_train_loop_matches_oracle_training():
     wn = w.numpy()
     for cid in W:
         assert normwise(wn[cid], W[cid]) < TOL
+
+
+def test_checkpoint_roundtrip_device_weights(tmp_path):
+    """save_checkpoint / load_checkpoint on device weights after training steps."""
+    net = P.build_lstm(16, 32, 8)
+    w = P.Weights.init(net, 9)
+    tr = P.Trainer(net, w, 4, P.TrainConfig(h=8, h_prime=4, lr=0.05, iterations=1))
+    rng = np.random.default_rng(2)
+    for _ in range(3):
+        tr.step(torch.tensor(rng.uniform(-1, 1, size=(16, 16)), dtype=torch.float32, device="cuda"),
+                torch.tensor(rng.integers(0, 8, size=16), device="cuda"))
+    path = str(tmp_path / "w.rnng")
+    P.save_checkpoint(path, net, w)
+    w2 = P.load_checkpoint(path, net)
+    assert torch.equal(w.flat[: w.n_params], w2.flat[: w2.n_params])
+    for cid in w.w:
+        assert torch.equal(w2.wt[cid], w2.w[cid].T.contiguous())
