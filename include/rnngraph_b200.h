@@ -70,6 +70,15 @@ int rgb_plan_set_cursor(rgb_plan* plan, int64_t cursor);
 int rgb_forward_chunk(rgb_plan* plan, const float* w, const float* x, int x_on_host, int frames,
                       int sequential, void* stream);
 
+/* forward_chunk with token-id inputs (engine.py:308-316, 372-403): `ids` is
+ * (frames*S) int64, frame-major, in [0, n_in) (host pointer if ids_on_host).
+ * The plan keeps an id history instead of one-hot rows: dense edges out of
+ * the input layer gather rows of W^T (hence `wt`), and backward_window
+ * computes their gradient as a deterministic sorted scatter (kernels.py:
+ * 106-140).  A plan is in id mode from its first id chunk on. */
+int rgb_forward_chunk_ids(rgb_plan* plan, const float* w, const float* wt, const int64_t* ids, int ids_on_host,
+                          int frames, int sequential, void* stream);
+
 /* inject_output_error + loss_value (engine.py:425-474) for the newest
  * `frames` frames: delta_out = d - y into the plan's injection buffer and
  * the summed loss into the plan's device loss slot.  target_kind: 0 int64

@@ -37,6 +37,7 @@ _SIGS = {
     "rgb_plan_get_cursor": ([_P, ctypes.POINTER(_I64)], _I),
     "rgb_plan_set_cursor": ([_P, _I64], _I),
     "rgb_forward_chunk": ([_P, _P, _P, _I, _I, _I, _P], _I),
+    "rgb_forward_chunk_ids": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),
     "rgb_inject_output_error": ([_P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_read_loss": ([_P, ctypes.POINTER(ctypes.c_double), _P], _I),
     "rgb_read_loss_async": ([_P, _P, _P], _I),

@@ -483,3 +483,143 @@ void launch_count_nonfinite(const float* p, int64_t n, unsigned long long* out, 
 }
 
 }  // namespace rgb
+
+// ---------------------------------------------------------------------------
+// Token-id input path (reference engine.py:308-316, 588-592; kernels.py:106-140):
+// the input layer's history holds ids (int32, -1 = pre-start / reset frame)
+// instead of one-hot rows; dense edges out of it gather rows of W^T, their
+// gradient is a deterministic scatter over a stable sort of the window rows.
+namespace rgb {
+
+__global__ void ids_ring_write_kernel(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t t = t_a + r / S;
+  const int64_t slot = ((t % cap) + cap) % cap;
+  const int n = r % S;
+  const int32_t v = (int32_t)ids[r];
+  ring[slot * S + n] = v;            // the frame's slot
+  ring[(slot + cap) * S + n] = v;    // and its mirror
+}
+
+void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, cudaStream_t s) {
+  if (rows > 0) ids_ring_write_kernel<<<(rows + 255) / 256, 256, 0, s>>>(ids, ring, rows, S, t_a, cap);
+}
+
+__global__ void ids_reset_kernel(int32_t* ring, int S, int frames, int stream) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < frames) ring[(int64_t)f * S + stream] = -1;
+}
+
+void launch_ids_reset(int32_t* ring, int S, int frames, int stream, cudaStream_t s) {
+  ids_reset_kernel<<<(frames + 255) / 256, 256, 0, s>>>(ring, S, frames, stream);
+}
+
+// out[r, :] (+)= W^T[ids[r], :]  (a zero row for id < 0); W^T is (V x n) row-major
+__global__ void gather_rows_kernel(const int32_t* ids, const float* wt, float* out, int rows, int n, int accumulate) {
+  const int64_t total = (int64_t)rows * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n), j = (int)(e - (int64_t)r * n);
+    const int v = ids[r];
+    const float g = v >= 0 ? wt[(int64_t)v * n + j] : 0.0f;
+    out[e] = accumulate ? out[e] + g : g;
+  }
+}
+
+void launch_gather_rows(const int32_t* ids, const float* wt, float* out, int rows, int n, bool accumulate,
+                        cudaStream_t s) {
+  const int64_t total = (int64_t)rows * n;
+  int blocks = (int)((total + 255) / 256);
+  blocks = blocks > 148 * 16 ? 148 * 16 : (blocks < 1 ? 1 : blocks);
+  gather_rows_kernel<<<blocks, 256, 0, s>>>(ids, wt, out, rows, n, accumulate ? 1 : 0);
+}
+
+// stable counting sort of the K window rows by id: counts -> offsets -> order
+__global__ void id_hist_kernel(const int32_t* ids, int K, int* counts) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < K && ids[r] >= 0) atomicAdd(&counts[ids[r]], 1);  // integer: order-independent
+}
+
+// single block: exclusive scan of counts[V] in place (sequential chunks with carry)
+__global__ void id_scan_kernel(int* counts, int V) {
+  __shared__ int buf[1024];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < V; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int x = i < V ? counts[i] : 0;
+    buf[threadIdx.x] = x;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int y = threadIdx.x >= off ? buf[threadIdx.x - off] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (i < V) counts[i] = carry + buf[threadIdx.x] - x;  // exclusive
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += buf[1023];
+    __syncthreads();
+  }
+}
+
+// one warp walks the rows in order; lanes with equal ids take consecutive
+// slots in row order (match_any + rank), so the order is stable and fixed
+__global__ void id_place_kernel(const int32_t* ids, int K, int* cursor, int* order) {
+  const int lane = threadIdx.x;
+  for (int base = 0; base < K; base += 32) {
+    const int r = base + lane;
+    const int v = r < K ? ids[r] : -2;
+    const unsigned same = __match_any_sync(0xffffffffu, v);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    const int leader = __ffs(same) - 1;
+    int start = 0;
+    if (lane == leader && v >= 0) start = cursor[v];
+    start = __shfl_sync(0xffffffffu, start, leader);
+    if (v >= 0) order[start + rank] = r;
+    __syncwarp();
+    if (lane == leader && v >= 0) cursor[v] = start + __popc(same);
+    __syncwarp();
+  }
+}
+
+// G[i, v] = alpha * sum over the sorted rows with id v of E[row, i]; one
+// thread per unit i walks the sorted rows (coalesced E rows), writing each
+// (i, v) once; G must be zero where no row has id v
+__global__ void id_scatter_dw_kernel(const float* e, const int32_t* ids, const int* order, int K, int m, int V,
+                                     float alpha, float* g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  float acc = 0.0f;
+  int cur = -1;
+  for (int p = 0; p < K; ++p) {
+    const int r = order[p];
+    if (r < 0) break;  // fewer valid rows than K (pre-start ids)
+    const int v = ids[r];
+    if (v != cur) {
+      if (cur >= 0) g[(int64_t)i * V + cur] = alpha * acc;
+      cur = v;
+      acc = 0.0f;
+    }
+    acc += e[(int64_t)r * m + i];
+  }
+  if (cur >= 0) g[(int64_t)i * V + cur] = alpha * acc;
+}
+
+// scratch: counts[V] + order[K] ints
+int launch_id_scatter_dw(const float* e, const int32_t* ids, int K, int m, int V, float alpha, float* g, int* scratch,
+                         cudaStream_t s) {
+  int* counts = scratch;
+  int* order = scratch + V;
+  cudaMemsetAsync(counts, 0, (size_t)V * 4, s);
+  cudaMemsetAsync(order, 0xff, (size_t)K * 4, s);
+  id_hist_kernel<<<(K + 255) / 256, 256, 0, s>>>(ids, K, counts);
+  id_scan_kernel<<<1, 1024, 0, s>>>(counts, V);
+  id_place_kernel<<<1, 32, 0, s>>>(ids, K, counts, order);
+  launch_fill(g, 0.0f, (int64_t)m * V, s);
+  id_scatter_dw_kernel<<<(m + 127) / 128, 128, 0, s>>>(e, ids, order, K, m, V, alpha, g);
+  return 5;
+}
+
+}  // namespace rgb

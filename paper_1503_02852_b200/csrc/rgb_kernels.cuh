@@ -55,6 +55,14 @@ void launch_sgd(float* w, float* lo, const float* g, float lr, int64_t n, cudaSt
 void launch_transpose(const TransposeGroup& p, cudaStream_t s);
 void launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s);
+// token-id input path (rgb_kernels.cu): id history ring, W^T row gather,
+// deterministic scatter dW (returns the kernel launch count)
+void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, cudaStream_t s);
+void launch_ids_reset(int32_t* ring, int S, int frames, int stream, cudaStream_t s);
+void launch_gather_rows(const int32_t* ids, const float* wt, float* out, int rows, int n, bool accumulate,
+                        cudaStream_t s);
+int launch_id_scatter_dw(const float* e, const int32_t* ids, int K, int m, int V, float alpha, float* g, int* scratch,
+                         cudaStream_t s);
 void launch_count_nonfinite(const float* p, int64_t n, unsigned long long* out, cudaStream_t s);
 
 }  // namespace rgb

@@ -13,6 +13,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -183,6 +184,42 @@ struct rgb_plan {
   };
   std::map<std::pair<int, int64_t>, SccPlan> scc_plans;
 
+  // token-id input mode (rgb_forward_chunk_ids): the input layer's history is
+  // an int32 id ring with the y rings' slot layout (-1 = zero row); dense
+  // edges out of it gather W^T rows, their dW is a sorted scatter
+  int32_t* ids_ring = nullptr;
+  int64_t* ids_stage = nullptr;
+  bool id_mode = false;
+  float* gbuf = nullptr;  // gathered partial rows
+  long long gbuf_cap = 0;
+  int* iscratch = nullptr;  // counts + sorted row order of the id scatter
+  long long iscratch_cap = 0;
+
+  int grow_buf(void** ptr, long long* cap, long long need_bytes, cudaStream_t st) {
+    if (need_bytes <= *cap) return RGB_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(RGB_ERR_CUDA, "id-path scratch must be sized by an eager step before graph capture");
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(RGB_ERR_CUDA, "scratch sync");
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    if (cudaMalloc(ptr, need_bytes) != cudaSuccess) return fail(RGB_ERR_CUDA, "id-path scratch allocation");
+    *cap = need_bytes;
+    return RGB_OK;
+  }
+
+  // is this pointer inside the input layer's history ring?
+  bool in_input_ring(const float* q) const {
+    if (in_buf < 0) return false;
+    const float* b = ws + bufs[in_buf].off;
+    return q >= b && q < b + (int64_t)2 * cap * S * bufs[in_buf].width;
+  }
+  const int32_t* ids_for(const float* q) const {
+    return ids_ring + (q - (ws + bufs[in_buf].off)) / bufs[in_buf].width;
+  }
+
   // split-K scratch of the TMA GEMM (tc_gemm_nt_scratch): grown on demand
   // outside stream capture; a captured launch that would need more falls back
   // to the unsplit configuration (launch_tc_gemm_nt checks the capacity)
@@ -215,6 +252,10 @@ struct rgb_plan {
   }
 
   ~rgb_plan() {
+    if (ids_ring) cudaFree(ids_ring);
+    if (ids_stage) cudaFree(ids_stage);
+    if (gbuf) cudaFree(gbuf);
+    if (iscratch) cudaFree(iscratch);
     if (part) cudaFree(part);
     if (maps_dev) cudaFree(maps_dev);
     for (auto* q : prog_dev)
@@ -556,6 +597,77 @@ struct rgb_plan {
     return RGB_OK;
   }
 
+  const int* cur_seg_cid = nullptr;  // [kMaxJobs][kMaxSegs] connection ids of the GEMM being parsed
+
+  // Id mode: segments whose A operand is the input ring become W^T row
+  // gathers into gbuf (one partial per job), added to the job's chain as an
+  // identity term; a job left without segments runs as an elementwise chain
+  // whose base is the gathered partial.  Forward direction only (dense edges
+  // out of the input layer), so B = W and the gather reads W^T = c.wt.
+  int gather_input_segments(GemmGroup& G, const Ctx& c, cudaStream_t st) {
+    bool any = false;
+    for (int j = 0; j < G.njobs; ++j)
+      for (int s = 0; s < G.job[j].nseg; ++s) any = any || in_input_ring(G.job[j].seg[s].a);
+    if (!any) return RGB_OK;
+    if (!c.wt) return fail(RGB_ERR_KERNEL, "id-mode forward needs the W^T buffer");
+    int rc = grow_buf(reinterpret_cast<void**>(&gbuf), &gbuf_cap,
+                      (long long)G.njobs * G.rows * 4 * [&] {
+                        int w = 0;
+                        for (int j = 0; j < G.njobs; ++j) w = std::max(w, G.job[j].n);
+                        return w;
+                      }(),
+                      st);
+    if (rc) return rc;
+    int wmax = 0;
+    for (int j = 0; j < G.njobs; ++j) wmax = std::max(wmax, G.job[j].n);
+    EwLaunch L;
+    std::memset(&L, 0, sizeof L);
+    L.rows = G.rows;
+    L.ring = G.ring;
+    int kept = 0;
+    for (int j = 0; j < G.njobs; ++j) {
+      GemmJob jb = G.job[j];
+      float* part_j = gbuf + (size_t)j * G.rows * wmax;
+      int ns = 0, ng = 0;
+      for (int s = 0; s < jb.nseg; ++s) {
+        const Seg& sg = jb.seg[s];
+        if (!in_input_ring(sg.a)) {
+          jb.seg[ns++] = sg;
+          continue;
+        }
+        const int cid = cur_seg_cid[j * kMaxSegs + s];
+        launch_gather_rows(ids_for(sg.a), c.wt + wts[cid].off, part_j, G.rows, jb.n, ng > 0, st);
+        note_launch();
+        ++ng;
+      }
+      jb.nseg = ns;
+      if (ng == 0) {
+        G.job[kept++] = jb;
+        continue;
+      }
+      EwOp& op0 = jb.epi.op[0];
+      if (ns > 0) {
+        if (op0.nterm >= kMaxTerms) return fail(RGB_ERR_ENGINE, "id-mode gather: too many terms on one layer");
+        op0.term[op0.nterm++] = part_j;
+        G.job[kept++] = jb;
+      } else {
+        if (L.nchains >= kMaxChains) return fail(RGB_ERR_KERNEL, "id-mode gather: too many chains");
+        op0.base = part_j;  // elementwise chain on the gathered rows
+        L.chain[L.nchains++] = jb.epi;
+      }
+    }
+    G.njobs = kept;
+    for (int j = 0; j < G.njobs; ++j) {
+      G.tiles_n[j] = (G.job[j].n + 63) / 64;
+      G.tile_start[j + 1] = G.tile_start[j] + ((G.rows + 63) / 64) * G.tiles_n[j];
+    }
+    if (L.nchains) {
+      launch_ew(L, st);
+      note_launch();
+    }
+    return RGB_OK;
+  }
+
   int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) {
     Reader rd{p, n};
     while (rd.i < n) {
@@ -570,6 +682,20 @@ struct rgb_plan {
         L.ring = ring_for(c);
         for (int i = 0; i < L.nchains; ++i)
           if ((rc = parse_chain(rd, c, false, L.chain[i]))) return rc;
+        if (id_mode) {
+          // the dense input copy into the input ring does not exist in id mode
+          int kept = 0;
+          for (int i = 0; i < L.nchains; ++i) {
+            EwChain ch = L.chain[i];
+            int nk = 0;
+            for (int k = 0; k < ch.nops; ++k)
+              if (!in_input_ring(ch.op[k].out)) ch.op[nk++] = ch.op[k];
+            ch.nops = nk;
+            if (nk) L.chain[kept++] = ch;
+          }
+          L.nchains = kept;
+          if (!kept) continue;
+        }
         double bytes = 0;
         for (int i = 0; i < L.nchains; ++i) bytes += ew_bytes(L.chain[i], L.rows);
         const int slot = prof_start(st);
@@ -577,6 +703,8 @@ struct rgb_plan {
         note_launch();
         prof_stop(slot, st, c.in_loop ? PROF_EW_FRAME : PROF_EW, 0.0, bytes);
       } else if (kind == STEP_GEMM) {
+        int seg_cid[kMaxJobs][kMaxSegs];
+        cur_seg_cid = &seg_cid[0][0];
         GemmGroup G;
         std::memset(&G, 0, sizeof G);
         G.njobs = rd.next();
@@ -592,6 +720,7 @@ struct rgb_plan {
           if (jb.nseg < 1 || jb.nseg > kMaxSegs) return fail(RGB_ERR_KERNEL, "bad segment count");
           for (int s = 0; s < jb.nseg; ++s) {
             const int ab = rd.next(), ash = rd.next(), cid = rd.next(), trans = rd.next();
+            seg_cid[j][s] = cid;
             float* a;
             if ((rc = resolve(c, ab, ash, c.frames, &a))) return rc;
             if (cid < 0 || cid >= (int)wts.size() || wts[cid].rows == 0)
@@ -618,6 +747,8 @@ struct rgb_plan {
           G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
         }
         G.tma = all_tma ? 1 : 0;
+        if (id_mode && (rc = gather_input_segments(G, c, st))) return rc;
+        if (G.njobs == 0) continue;
         double flops = 0, bytes = 0;
         for (int j = 0; j < G.njobs; ++j) {
           int64_t ksum = 0;
@@ -646,7 +777,7 @@ struct rgb_plan {
         const int len = rd.next();
         if (rd.i + len > n) return fail(RGB_ERR_KERNEL, "truncated loop body");
         const int32_t* body = p + rd.i;
-        if (g_scc_mode && g_gemm_mode != 2 && c.section >= 0 && c.frames >= 2 && prog_dev[c.section]) {
+        if (g_scc_mode && g_gemm_mode != 2 && !id_mode && c.section >= 0 && c.frames >= 2 && prog_dev[c.section]) {
           const std::pair<int, int64_t> key{c.section, (int64_t)(body - c.sec_base)};
           auto found = scc_plans.find(key);
           if (found == scc_plans.end()) found = scc_plans.emplace(key, plan_scc(body, len)).first;
@@ -729,6 +860,23 @@ struct rgb_plan {
         }
         // jobs with TMA maps -> TMA-fed tcgen05 launch; the rest (e.g. width-1
         // bias sources) -> one SIMT / register-fed launch
+        if (id_mode) {  // dW of dense edges out of the id input: sorted scatter (no one-hot)
+          int kept = 0;
+          for (int j = 0; j < D.njobs; ++j) {
+            const DwJob& jb = D.job[j];
+            if (!in_input_ring(jb.y)) {
+              D.job[kept++] = jb;
+              continue;
+            }
+            if ((rc = grow_buf(reinterpret_cast<void**>(&iscratch), &iscratch_cap,
+                               ((long long)jb.n + D.k) * 4, st)))
+              return rc;
+            const int nl = launch_id_scatter_dw(jb.e, ids_for(jb.y), D.k, jb.m, jb.n, D.alpha, jb.g, iscratch, st);
+            for (int q = 0; q < nl; ++q) note_launch();
+          }
+          D.njobs = kept;
+          if (!kept) continue;
+        }
         // narrow sources (bias edges, n <= 4) -> GEMV-shaped stream (V) when the
         // step is large enough for the tensor cores; the rest of the TC-eligible
         // jobs -> TMA launch (T); remainder -> SIMT / register-fed launch (R)
@@ -1025,6 +1173,7 @@ int rgb_plan_set_cursor(rgb_plan* p, int64_t c) {
 int rgb_forward_chunk(rgb_plan* p, const float* w, const float* x, int x_on_host, int frames, int sequential,
                       void* stream) {
   if (!p || !p->ws || !x) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (p->id_mode) return fail(RGB_ERR_ENGINE, "chunk mode 'dense' != stream mode 'ids'");
   if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "advance by %d outside [1, h=%d]", frames, p->hmax);
   cudaStream_t st = as_stream(stream);
   float* stage = p->ws + p->bufs[p->stage_buf].off;
@@ -1040,6 +1189,45 @@ int rgb_forward_chunk(rgb_plan* p, const float* w, const float* x, int x_on_host
   c.t1 = p->cursor;
   c.t0 = p->cursor;
   c.w = w;
+  c.section = sequential ? 2 : 0;
+  const auto& prog = p->prog[c.section];
+  c.sec_base = prog.data();
+  return p->run(prog.data(), (int64_t)prog.size(), c, st);
+}
+
+int rgb_forward_chunk_ids(rgb_plan* p, const float* w, const float* wt, const int64_t* ids, int ids_on_host,
+                          int frames, int sequential, void* stream) {
+  if (!p || !p->ws || !ids || !w || !wt) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (frames < 1 || frames > p->hmax) return fail(RGB_ERR_ENGINE, "advance by %d outside [1, h=%d]", frames, p->hmax);
+  cudaStream_t st = as_stream(stream);
+  const int rows = frames * p->S;
+  if (!p->ids_ring) {
+    // first id chunk: id ring (2*cap frames, -1 = zero row) + staging
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return fail(RGB_ERR_CUDA, "first id chunk inside a graph capture");
+    const size_t ring_bytes = (size_t)2 * p->cap * p->S * 4;
+    if (cudaMalloc(&p->ids_ring, ring_bytes) != cudaSuccess ||
+        cudaMalloc(&p->ids_stage, (size_t)p->hmax * p->S * 8) != cudaSuccess ||
+        cudaMemset(p->ids_ring, 0xff, ring_bytes) != cudaSuccess)
+      return fail(RGB_ERR_CUDA, "id ring allocation");
+  }
+  int rc = cuda_rc(cudaMemcpyAsync(p->ids_stage, ids, (size_t)rows * 8,
+                                   ids_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st),
+                   "id copy");
+  if (rc) return rc;
+  p->id_mode = true;
+  p->cursor += frames;
+  launch_ids_ring_write(p->ids_stage, p->ids_ring, rows, p->S, p->cursor - frames + 1, p->cap, st);
+  note_launch();
+  Ctx c;
+  c.t_a = p->cursor - frames + 1;
+  c.frames = frames;
+  c.chunk_base = c.t_a;
+  c.t1 = p->cursor;
+  c.t0 = p->cursor;
+  c.w = w;
+  c.wt = wt;
   c.section = sequential ? 2 : 0;
   const auto& prog = p->prog[c.section];
   c.sec_base = prog.data();
@@ -1190,6 +1378,10 @@ extern "C" {
 int rgb_reset_stream(rgb_plan* p, int s, void* stream) {
   if (!p || !p->ws) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
   if (s < 0 || s >= p->S) return fail(RGB_ERR_ENGINE, "stream %d outside [0, %d)", s, p->S);
+  if (p->ids_ring) {  // id history of the stream: -1 (reference engine.py:267-276)
+    launch_ids_reset(p->ids_ring, p->S, 2 * p->cap, s, as_stream(stream));
+    note_launch();
+  }
   for (const BufDesc& b : p->bufs) {
     if (b.kind != BUF_RING) continue;
     float* base = p->ws + b.off + (int64_t)s * b.width;

@@ -371,7 +371,7 @@ def _single_io(net: NetworkDef):
 
 
 def _input_rows(lin, state: StreamState, inputs):
-    """Validate a chunk and return (device fp32 rows, frames, mode)."""
+    """Validate a chunk and return (device fp32 rows or int64 ids, frames, mode)."""
     if isinstance(inputs, Batch):
         if inputs.streams != state.n:
             raise EngineError(f"chunk has {inputs.streams} streams, state has {state.n}")
@@ -390,11 +390,9 @@ def _input_rows(lin, state: StreamState, inputs):
     for c in state.net.posterior(lin.id):
         if state.net.connection(c).weight_kind.value != "dense":
             raise EngineError(f"connection {c}: identity weight from an id-driven input layer is not supported")
-    dev_ids = torch.as_tensor(ids, dtype=torch.int64).to(_device()).contiguous()
-    x = torch.empty((max(dev_ids.shape[0], 1), lin.size), dtype=DTYPE, device=_device())
-    if dev_ids.shape[0]:
-        _lib.check(_lib.lib().rgb_onehot_rows(_ptr(dev_ids), dev_ids.shape[0], lin.size, _ptr(x), _stream()))
-    return x, frames, "ids"
+    # the device keeps an id history: no one-hot rows (W^T row gathers forward,
+    # sorted scatter for dW -- rgb_forward_chunk_ids)
+    return torch.as_tensor(ids, dtype=torch.int64).to(_device()).contiguous(), frames, "ids"
 
 
 def forward_chunk(net: NetworkDef, cg: CondensedGraph, weights: Weights, state: StreamState, inputs, *,
@@ -415,8 +413,12 @@ def forward_chunk(net: NetworkDef, cg: CondensedGraph, weights: Weights, state: 
     if frames > state.h:
         raise EngineError(f"advance by {frames} outside [1, h={state.h}]")
     L = _lib.lib()
-    _lib.check(L.rgb_forward_chunk(state._plan.handle, _ptr(weights.flat), _ptr(x), 0, frames,
-                                   0 if frame_parallel else 1, _stream()), "forward_chunk")
+    if mode == "ids":
+        _lib.check(L.rgb_forward_chunk_ids(state._plan.handle, _ptr(weights.flat), _ptr(weights.flat_t), _ptr(x), 0,
+                                           frames, 0 if frame_parallel else 1, _stream()), "forward_chunk")
+    else:
+        _lib.check(L.rgb_forward_chunk(state._plan.handle, _ptr(weights.flat), _ptr(x), 0, frames,
+                                       0 if frame_parallel else 1, _stream()), "forward_chunk")
     t_hi = state.cursor
     t_lo = t_hi - frames + 1
     if check_finite:
@@ -585,7 +587,7 @@ def read_checkpoint(path: str, net: NetworkDef) -> dict:
         cid, rows, cols = struct.unpack("<III", take(12))
         if shapes.get(cid) != (rows, cols):
             raise CheckpointError(f"{path}: connection {cid} has shape {(rows, cols)}")
-        mats[cid] = np.frombuffer(take(rows * cols * 8), dtype="<f8").reshape(rows, cols)
+        mats[cid] = np.frombuffer(take(rows * cols * 8), dtype="<f8").reshape(rows, cols).copy()
     want = {c.id for c in net.iter_dense()}
     if set(mats) != want:
         raise CheckpointError(f"{path}: connection ids {sorted(mats)} != network {sorted(want)}")
@@ -653,14 +655,18 @@ class Trainer:
         gradient buffer over ranks between backward and SGD."""
         L, st, plan = self._lib, self._stream(), self.state._plan.handle
         hp = self.cfg.h_prime
-        if isinstance(inputs, torch.Tensor) and inputs.is_cuda:
-            x, on_host = inputs, 0
-        elif isinstance(inputs, torch.Tensor):
-            x, on_host = inputs, 1
+        if isinstance(inputs, torch.Tensor):
+            x, on_host, mode = inputs, 0 if inputs.is_cuda else 1, "dense" if inputs.is_floating_point() else "ids"
+            if mode == "ids" and x.dtype != torch.int64:
+                x = x.to(torch.int64)
         else:
-            x, _, _ = _input_rows(self.net.layer(self.net.input_layers()[0].id), self.state, inputs)
+            x, _, mode = _input_rows(self.net.layer(self.net.input_layers()[0].id), self.state, inputs)
             on_host = 0
-        _lib.check(L.rgb_forward_chunk(plan, _ptr(self.weights.flat), _ptr(x), on_host, hp, self._seq, st))
+        if mode == "ids":  # token ids: id history, W^T row gathers, sorted-scatter dW
+            _lib.check(L.rgb_forward_chunk_ids(plan, _ptr(self.weights.flat), _ptr(self.weights.flat_t), _ptr(x),
+                                               on_host, hp, self._seq, st))
+        else:
+            _lib.check(L.rgb_forward_chunk(plan, _ptr(self.weights.flat), _ptr(x), on_host, hp, self._seq, st))
         if self.cfg.check_finite:
             t_hi = self.state.cursor
             for l in self.net.layers:
@@ -691,7 +697,7 @@ class Trainer:
         return v.value
 
     # ---- CUDA-graph replay of whole iterations --------------------------------
-    def enable_graphs(self, exchange=None) -> None:
+    def enable_graphs(self, exchange=None, ids: bool = False) -> None:
         """Capture the iteration once per ring phase and replay it.
 
         Every kernel argument of an iteration depends on the cursor only
@@ -703,7 +709,9 @@ class Trainer:
         n_in = self.net.input_layers()[0].size
         dev = _device()
         S = self.state.n
-        self.gx = torch.zeros((hp * S, n_in), dtype=DTYPE, device=dev)
+        # ids=True: the graphs read token ids (int64) instead of dense rows
+        self.gx = (torch.zeros((hp * S,), dtype=torch.int64, device=dev) if ids
+                   else torch.zeros((hp * S, n_in), dtype=DTYPE, device=dev))
         self.gt = torch.zeros((hp * S,), dtype=torch.int64, device=dev)
         self._graphs = {}
         self._exchange = exchange
