@@ -102,6 +102,13 @@ int rgb_get_injection(rgb_plan* plan, float* delta_out, int frames, void* stream
 int rgb_inject_rows(const float* y, const void* target, int target_kind, int criterion, float* delta,
                     double* row_loss, double* loss, int rows, int width, void* stream);
 
+/* Device-fed token tapes (reference data.py:117-207): gather the ids at
+ * corpus positions pos[(n_streams, h_prime + 1)] (planned by the host tape
+ * cursors) into frame-major inputs and one-ahead targets, (h_prime*n_streams)
+ * int64 each. */
+int rgb_tape_gather(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets, int n_streams,
+                    int h_prime, void* stream);
+
 /* Token-id chunk -> dense one-hot rows (rows, width) on the device; id -1
  * gives a zero row.  Feeds forward_chunk's id-input mode (engine.py:372-403;
  * bitwise equal to one-hot dense input in the reference, test_engine.py:277-312). */

@@ -16,4 +16,6 @@ from .engine import (Batch, BpttWindow, CheckpointError, Criterion, GradStore, I
                      TrainConfig, Trainer, Weights, backward_window, forward_chunk, inject_output_error,
                      load_checkpoint, loss_value, save_checkpoint, sgd_update, structure_hash, train_loop)
 
+from .tapes import DeviceStreamSet, TapePlanner
+
 __version__ = "0.1.0"

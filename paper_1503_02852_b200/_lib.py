@@ -50,6 +50,7 @@ _SIGS = {
     "rgb_count_nonfinite": ([_P, _I, _I64, _I64, ctypes.POINTER(_I64), _P], _I),
     "rgb_inject_rows": ([_P, _P, _I, _I, _P, _P, _P, _I, _I, _P], _I),
     "rgb_onehot_rows": ([_P, _I, _I, _P, _P], _I),
+    "rgb_tape_gather": ([_P, _P, _P, _P, _I, _I, _P], _I),
     "rgb_set_gemm_mode": ([_I], _I),
     "rgb_set_scc_mode": ([_I], _I),
     "rgb_gemm_nt": ([_P, _P, _P, _I, _I, _I, _I, _P], _I),

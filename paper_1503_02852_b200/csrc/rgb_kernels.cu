@@ -623,3 +623,26 @@ int launch_id_scatter_dw(const float* e, const int32_t* ids, int K, int m, int V
 }
 
 }  // namespace rgb
+
+// ---------------------------------------------------------------------------
+// Token tapes (reference data.py:117-207): gather the ids of h'+1 tokens per
+// stream (positions planned on the host) into frame-major inputs / targets.
+namespace rgb {
+
+__global__ void tape_gather_kernel(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets,
+                                   int S, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S * (k + 1)) return;
+  const int s = i / (k + 1), j = i % (k + 1);
+  const int64_t tok = corpus[pos[i]];
+  if (j < k) inputs[(int64_t)j * S + s] = tok;
+  if (j > 0) targets[(int64_t)(j - 1) * S + s] = tok;
+}
+
+void launch_tape_gather(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets, int S, int k,
+                        cudaStream_t s) {
+  const int n = S * (k + 1);
+  if (n > 0) tape_gather_kernel<<<(n + 255) / 256, 256, 0, s>>>(corpus, pos, inputs, targets, S, k);
+}
+
+}  // namespace rgb

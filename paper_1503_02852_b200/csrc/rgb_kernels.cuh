@@ -59,6 +59,8 @@ void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStre
 // deterministic scatter dW (returns the kernel launch count)
 void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, cudaStream_t s);
 void launch_ids_reset(int32_t* ring, int S, int frames, int stream, cudaStream_t s);
+void launch_tape_gather(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets, int S, int k,
+                        cudaStream_t s);
 void launch_gather_rows(const int32_t* ids, const float* wt, float* out, int rows, int n, bool accumulate,
                         cudaStream_t s);
 int launch_id_scatter_dw(const float* e, const int32_t* ids, int K, int m, int V, float alpha, float* g, int* scratch,

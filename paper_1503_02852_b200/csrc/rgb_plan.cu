@@ -1393,6 +1393,14 @@ int rgb_reset_stream(rgb_plan* p, int s, void* stream) {
   return RGB_OK;
 }
 
+int rgb_tape_gather(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets, int n_streams,
+                    int h_prime, void* stream) {
+  if (!corpus || !pos || !inputs || !targets || n_streams < 1 || h_prime < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
+  launch_tape_gather(corpus, pos, inputs, targets, n_streams, h_prime, as_stream(stream));
+  note_launch();
+  return cuda_rc(cudaGetLastError(), "tape gather");
+}
+
 int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* stream) {
   if (!ids || !out || rows < 1 || width < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
   launch_onehot(ids, rows, width, out, as_stream(stream));

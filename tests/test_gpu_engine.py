@@ -393,3 +393,23 @@ def test_id_trainer_graphs_and_reset():
     out_f = P.forward_chunk(net, P.condense(net), wa, fresh, ids)
     rows = torch.arange(4, device="cuda") * 4 + 1
     assert torch.equal(out_a.values[rows], out_f.values[rows])
+
+
+def test_device_tapes_gather_and_train_loop():
+    """DeviceStreamSet chunks equal the host planner's tokens, and train_loop
+    runs on them (ids path, resets on document boundaries)."""
+    from paper_1503_02852_b200.tapes import DeviceStreamSet, TapePlanner
+    rng = np.random.default_rng(4)
+    docs = [rng.integers(0, 30, size=int(rng.integers(2, 20))) for _ in range(12)]
+    dev, host = DeviceStreamSet(docs, 4, seed=5), TapePlanner(docs, 4, seed=5)
+    for _ in range(10):
+        ch = dev.next_batch(6)
+        pos, new_seq = host.next_positions(6)
+        tok = host.corpus[pos]
+        assert np.array_equal(ch.inputs.cpu().numpy().reshape(6, 4).T, tok[:, :6])
+        assert np.array_equal(ch.targets.cpu().numpy().reshape(6, 4).T, tok[:, 1:])
+        assert np.array_equal(ch.new_sequence, new_seq)
+    net = P.build_lstm(30, 16, 30)
+    cfg = P.TrainConfig(h=8, h_prime=4, lr=0.05, iterations=12, reset_on_sequence_boundary=True)
+    _, metrics = P.train_loop(net, DeviceStreamSet(docs, 4, seed=5), cfg)
+    assert len(metrics) == 12 and all(np.isfinite(m.loss) for m in metrics)
