@@ -1019,7 +1019,9 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // (epilogue -> MMA).  The epilogue stages 32-column chunks of the tile in a
 // private smem slice (TMEM -> smem -> coalesced 16-byte row walk).
 constexpr int kPersThreads = 480;
-constexpr int kEpiLd = 36;  // padded chunk row (floats)
+constexpr int kPersConv = 128;  // converter threads (warps 0-3)
+constexpr int kEpiCols = 16;    // columns per epilogue chunk
+constexpr int kEpiLd = 20;      // padded chunk row (floats)
 
 template <int BN, int BNL>
 struct PCfg {
@@ -1028,12 +1030,12 @@ struct PCfg {
   static constexpr int B_BYTES = BNL * BK * 4;
   static constexpr int B_OFF = 2 * A_BYTES;
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
-  static constexpr int CHUNK_BYTES = BM * kEpiLd * 4;
-  static constexpr int BUDGET = 227 * 1024 - 1024 - 512 - kChainBytes - CHUNK_BYTES;
+  static constexpr int CHUNK_BYTES = 2 * BM * kEpiLd * 4;  // one staging chunk per epilogue group
+  static constexpr int BUDGET = 227 * 1024 - 1024 - 512 - 2 * kChainBytes - CHUNK_BYTES;
   static constexpr int RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = RAW > 8 ? 8 : RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512 + kChainBytes + CHUNK_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512 + 2 * kChainBytes + CHUNK_BYTES;
   static_assert(STAGES >= 2, "persistent pipeline needs two stages");
   static_assert(TMEM_COLS <= 512, "two accumulators must fit in TMEM");
 };
@@ -1094,7 +1096,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   uint64_t* tmem_empty = tmem_full + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 512);
-  float* chunk_s = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512 + kChainBytes);
+  float* chunk_s = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512 + 2 * kChainBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0;
@@ -1103,12 +1105,12 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&tma_full[s], 2);
-      mbar_init(&conv_full[s], PAIR ? 2 : kProducers);
+      mbar_init(&conv_full[s], PAIR ? 2 : kPersConv);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], NCTA);
+      mbar_init(&tmem_empty[b], 2 * NCTA);  // both epilogue groups of every CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1214,8 +1216,8 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         else mma_commit(&tmem_full[b]);
       }
     }
-  } else if (warp < 8) {
-    // ---------------- converters ----------------
+  } else if (warp < 4) {
+    // ---------------- converters (warps 0-3) ----------------
     int g = 0;
     for (int t = first; t < ntiles; t += stride) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
@@ -1226,22 +1228,22 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         const float4* a_hi = reinterpret_cast<const float4*>(base);
         float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
-        for (int i = 0; i < C::A_BYTES / 16 / kProducers; ++i) {
-          const int q = threadIdx.x + i * kProducers;
+        for (int i = 0; i < C::A_BYTES / 16 / kPersConv; ++i) {
+          const int q = threadIdx.x + i * kPersConv;
           const float4 x = a_hi[q];
           a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
         const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
         float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
 #pragma unroll
-        for (int i = 0; i < C::B_BYTES / 16 / kProducers; ++i) {
-          const int q = threadIdx.x + i * kProducers;
+        for (int i = 0; i < C::B_BYTES / 16 / kPersConv; ++i) {
+          const int q = threadIdx.x + i * kPersConv;
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if constexpr (PAIR) {
-          asm volatile("bar.sync 2, 256;" ::: "memory");
+          asm volatile("bar.sync 2, 128;" ::: "memory");
           if (threadIdx.x == 0) {
             if (rank == 0) mbar_arrive(&conv_full[s]);
             else mbar_arrive_cluster(&conv_full[s], 0);
@@ -1251,20 +1253,35 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         }
       }
     }
-  } else {
-    // ---------------- epilogue warps 11-14 ----------------
-    const int et = threadIdx.x - 11 * 32;  // 0..127
-    const int quarter = warp & 3;          // TMEM lane quarter this warp may read
+  } else if ((warp >= 4 && warp < 8) || warp >= 11) {
+    // ---------------- epilogue: two groups of 4 warps (4-7, 11-14) ----------------
+    // group g drains 16-column chunks g, g+2, ... of the tile through its own
+    // SMEM staging chunk and chain copy; named barrier 3+g
+    const int grp = warp >= 11 ? 1 : 0;
+    const int et = threadIdx.x - (grp ? 11 : 4) * 32;  // 0..127
+    const int quarter = warp & 3;                      // TMEM lane quarter this warp may read
     const int r_loc = quarter * 32 + lane;
+    EwChain* my_chain = reinterpret_cast<EwChain*>(reinterpret_cast<uint8_t*>(chain_s) + grp * kChainBytes);
+    float* my_chunk = chunk_s + grp * (BM * kEpiLd);
+    const int bar = 3 + grp;
+    auto gsync = [&] { asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory"); };
+    auto release = [&](int b) {  // this group's last TMEM read of buffer b is done
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      gsync();
+      if (et == 0) {
+        if (rank == 0) mbar_arrive(&tmem_empty[b]);
+        else mbar_arrive_cluster(&tmem_empty[b], 0);
+      }
+    };
     int ti = 0, staged_job = -1;
     for (int t = first; t < ntiles; t += stride, ++ti) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
       const int b = ti & 1;
       if constexpr (!IS_DW) {
         if (T.jid != staged_job) {  // the chain of this tile's job
-          asm volatile("bar.sync 3, 128;" ::: "memory");
-          stage_chain(chain_s, p.job[T.jid].epi, et, 128);
-          asm volatile("bar.sync 3, 128;" ::: "memory");
+          gsync();
+          stage_chain(my_chain, p.job[T.jid].epi, et, 128);
+          gsync();
           staged_job = T.jid;
         }
       }
@@ -1279,77 +1296,63 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         g_out = p.job[T.jid].g;
         vec = T.N % 4 == 0 && aligned16(g_out);
       } else {
-        vec = chain_vec_ok(*chain_s, T.N);
+        vec = chain_vec_ok(*my_chain, T.N);
       }
-      for (int c0 = 0; c0 < ncols; c0 += 32) {
-        float v[32];
-        tmem_ld32(acc + c0, v);
-        if (c0 + 32 >= ncols) {
-          // last TMEM read of this buffer: hand it back to the MMA issuer
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          asm volatile("bar.sync 3, 128;" ::: "memory");
-          if (et == 0) {
-            if (rank == 0) mbar_arrive(&tmem_empty[b]);
-            else mbar_arrive_cluster(&tmem_empty[b], 0);
-          }
-        }
-        float4* dst = reinterpret_cast<float4*>(chunk_s + r_loc * kEpiLd);
+      const int first_c = grp * kEpiCols;
+      if (first_c >= ncols) release(b);  // no chunk for this group
+      for (int c0 = first_c; c0 < ncols; c0 += 2 * kEpiCols) {
+        float v[16];
+        tmem_ld16(acc + c0, v);
+        if (c0 + 2 * kEpiCols >= ncols) release(b);
+        float4* dst = reinterpret_cast<float4*>(my_chunk + r_loc * kEpiLd);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-        const int cw = (ncols - c0) < 32 ? (ncols - c0) : 32;
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        gsync();
+        const int cw = (ncols - c0) < kEpiCols ? (ncols - c0) : kEpiCols;
         if (vec) {
-          // 8 lanes per row (16-byte groups), 16 rows per pass, RE rows per thread
+          // 4 lanes per row (16-byte groups), 32 rows per pass, RE rows per thread
           constexpr int RE = 2;
-          const int sub = et >> 3, lc = et & 7, cl = lc * 4;
+          const int sub = et >> 2, lc = et & 3, cl = lc * 4;
           if (cl < cw) {
 #pragma unroll 1
-            for (int rb = sub; rb < nrows; rb += 16 * RE) {
+            for (int rb = sub; rb < nrows; rb += 32 * RE) {
               int64_t rr[RE];
               bool ok[RE];
-              float4 a[RE];
+              float4 a4[RE];
 #pragma unroll
               for (int u = 0; u < RE; ++u) {
-                const int rl = rb + 16 * u;
+                const int rl = rb + 32 * u;
                 ok[u] = rl < nrows;
                 rr[u] = T.m0 + (ok[u] ? rl : 0);
-                a[u] = *reinterpret_cast<const float4*>(chunk_s + (ok[u] ? rl : 0) * kEpiLd + cl);
+                a4[u] = *reinterpret_cast<const float4*>(my_chunk + (ok[u] ? rl : 0) * kEpiLd + cl);
               }
               if constexpr (IS_DW) {
 #pragma unroll
                 for (int u = 0; u < RE; ++u)
                   if (ok[u])
                     st4(g_out, rr[u] * T.N + T.n0 + c0 + cl,
-                        make_float4(p.alpha * a[u].x, p.alpha * a[u].y, p.alpha * a[u].z, p.alpha * a[u].w));
+                        make_float4(p.alpha * a4[u].x, p.alpha * a4[u].y, p.alpha * a4[u].z, p.alpha * a4[u].w));
               } else {
                 const RingWrite ring = p.ring;
-                ew_chain_vec<RE>(*chain_s, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a);
+                ew_chain_vec<RE>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
               }
             }
           }
         } else {
           for (int e = et; e < nrows * cw; e += 128) {
             const int rl = e / cw, cl = e - rl * cw;
-            const float a = chunk_s[rl * kEpiLd + cl];
+            const float a = my_chunk[rl * kEpiLd + cl];
             const int64_t r = T.m0 + rl;
             const int c = T.n0 + c0 + cl;
             if constexpr (IS_DW) {
               p.job[T.jid].g[r * T.N + c] = p.alpha * a;
             } else {
               const RingWrite ring = p.ring;
-              for (int k = 0; k < chain_s->nops; ++k) ew_apply(chain_s->op[k], T.N, r, c, ring, k == 0, a);
+              for (int k = 0; k < my_chain->nops; ++k) ew_apply(my_chain->op[k], T.N, r, c, ring, k == 0, a);
             }
           }
         }
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-      }
-      if (ncols <= 0) {  // (cannot happen: tiles cover N) keep the barrier protocol intact
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-        if (et == 0) {
-          if (rank == 0) mbar_arrive(&tmem_empty[b]);
-          else mbar_arrive_cluster(&tmem_empty[b], 0);
-        }
+        gsync();
       }
     }
   }
