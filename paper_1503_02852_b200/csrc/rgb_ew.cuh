@@ -6,6 +6,13 @@
 
 namespace rgb {
 
+// Programmatic dependent launch: kernels of the per-frame loops may be
+// launched before their predecessor finishes (prologue overlap); they call
+// pdl_wait() before touching global memory the predecessor writes or reads.
+// Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // activations (kernels.py:143-189): accurate expf/tanhf, no fast-math
 
 __device__ __forceinline__ float act_apply(int act, float x) {

@@ -4,6 +4,7 @@
 #include "rgb_ew.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace rgb {
 
@@ -16,6 +17,8 @@ __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ E
   for (int i = threadIdx.x; i < (int)(sizeof(EwChain) / 4); i += blockDim.x) chain_words[i] = src[i];
   __syncthreads();
   const EwChain& ch = *reinterpret_cast<const EwChain*>(chain_words);
+  pdl_wait();  // predecessor complete (PDL launches inside frame loops)
+  pdl_trigger();
   if (chain_vec_ok(ch, ch.width)) {
     // 16-byte path: one thread per 4 consecutive units of a row
     const int w4 = ch.width / 4;
@@ -41,6 +44,21 @@ __global__ void __launch_bounds__(256) ew_chain_kernel(const __grid_constant__ E
   }
 }
 
+namespace {
+bool g_pdl_scope = false;
+}
+
+void set_pdl_scope(bool on) { g_pdl_scope = on; }
+
+bool pdl_active() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("RGB_PDL");
+    env = e ? atoi(e) != 0 : 1;
+  }
+  return env == 1 && g_pdl_scope;
+}
+
 void launch_ew(const EwLaunch& p, cudaStream_t s) {
   int64_t maxw = 1;
   for (int c = 0; c < p.nchains; ++c) maxw = maxw > p.chain[c].width ? maxw : p.chain[c].width;
@@ -48,7 +66,20 @@ void launch_ew(const EwLaunch& p, cudaStream_t s) {
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  ew_chain_kernel<<<dim3(blocks, p.nchains), 256, 0, s>>>(p);
+  if (pdl_active()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks, p.nchains);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, ew_chain_kernel, p);
+  } else {
+    ew_chain_kernel<<<dim3(blocks, p.nchains), 256, 0, s>>>(p);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -28,6 +28,14 @@ struct TransposeGroup {
 };
 
 void launch_ew(const EwLaunch& p, cudaStream_t s);
+// programmatic dependent launch for the launches that follow (the executor
+// enables it inside frame loops); RGB_PDL=0 disables it
+void set_pdl_scope(bool on);
+bool pdl_active();
+// programmatic dependent launch for the launches that follow (the executor
+// enables it inside frame loops); RGB_PDL=0 disables it
+void set_pdl_scope(bool on);
+bool pdl_active();
 void launch_gemm_nt(const GemmGroup& p, cudaStream_t s);
 void launch_gemm_dw(const DwGroup& p, cudaStream_t s);
 // dW of narrow sources (n <= 4, bias edges): two deterministic GEMV passes

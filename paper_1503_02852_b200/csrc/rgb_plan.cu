@@ -673,6 +673,9 @@ struct rgb_plan {
     while (rd.i < n) {
       const int kind = rd.next();
       int rc = RGB_OK;
+      // per-frame loop bodies: launch with programmatic dependent launch
+      // (the TMA GEMM and EW kernels wait for their predecessor on device)
+      set_pdl_scope(c.in_loop && (kind == STEP_EW || kind == STEP_GEMM));
       if (kind == STEP_EW) {
         EwLaunch L;
         std::memset(&L, 0, sizeof L);
