@@ -33,7 +33,7 @@
 namespace rgb {
 
 #ifdef RGB_EXP_TRACE
-// tuning aid: clock64 marks of CTA 0 / thread 0 for the first frames
+// tuning aid: clock64 marks of CTA 0 / thread 0 for the first frames (tools/trace_scc.py)
 __device__ long long g_scc_trace[64][16];
 #define SCC_MARK(f, k) \
   if (blockIdx.x == 0 && threadIdx.x == 0 && (f) < 64) g_scc_trace[f][k] = clock64();
@@ -63,9 +63,7 @@ struct SJob {
 struct Slot {
   int off;      // byte offset of the pointer field inside the template arena
   short buf, shift;
-  short inj;    // 1: only valid on injected frames (t > t0)
-  short role;   // 0 elementwise operand (width W), 1 output, 2 other (rank-1 source)
-  int shadow;   // >= 0: operand not written by the loop, staged in SMEM per frame
+  int inj;      // 1: only valid on injected frames (t > t0)
 };
 
 struct Step {
@@ -110,26 +108,25 @@ struct Builder {
     used += count * (int)sizeof(T);
     return reinterpret_cast<T*>(arena + off);
   }
-  __device__ void slot(const void* field, int buf, int shift, int inj = 0, int role = 0) {
+  __device__ void slot(const void* field, int buf, int shift, int inj = 0) {
     if (nslots >= kMaxSlots) {
       ok = false;
       return;
     }
-    slots[nslots++] = Slot{(int)(reinterpret_cast<const unsigned char*>(field) - arena), (short)buf, (short)shift,
-                           (short)inj, (short)role, -1};
+    slots[nslots++] = Slot{(int)(reinterpret_cast<const unsigned char*>(field) - arena), (short)buf, (short)shift, inj};
   }
   __device__ void op(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwOp& o) {
     o.kind = w[pos++];
     o.act = w[pos++];
     const int out = w[pos++];
     o.out = nullptr;
-    slot(&o.out, out, 0, 0, 1);
+    slot(&o.out, out, 0);
     o.out_is_ring = bufs[out].kind == 0;
     o.nterm = w[pos++];
     for (int i = 0; i < o.nterm; ++i, pos += 2) slot(&o.term[i], w[pos], w[pos + 1]);
     o.nrank1 = w[pos++];
     for (int i = 0; i < o.nrank1; ++i, pos += 3) {
-      slot(&o.r1src[i], w[pos], w[pos + 1], 0, 2);
+      slot(&o.r1src[i], w[pos], w[pos + 1]);
       o.r1w[i] = c.w + wts[w[pos + 2]].off;  // frame-independent
     }
     o.nfac = w[pos++];
@@ -146,7 +143,7 @@ struct Builder {
     const int neps = w[pos++];
     for (int i = 0; i < kMaxFac; ++i) o.eps[i] = nullptr;
     for (int i = 0; i < neps; ++i, ++pos)
-      if (w[pos] >= 0) slot(&o.eps[i], w[pos], 0, 0, 1);
+      if (w[pos] >= 0) slot(&o.eps[i], w[pos], 0);
   }
   __device__ void chain(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwChain& ch) {
     ch.width = w[pos++];
@@ -198,11 +195,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   float* astage = accs + ((c.acc_floats + 3) & ~3LL);
   unsigned char* arena = reinterpret_cast<unsigned char*>(astage + ((c.stage_floats + 3) & ~3LL));
   Slot* slots = reinterpret_cast<Slot*>(arena + c.arena_bytes);
-  float* shadow = reinterpret_cast<float*>(slots + kMaxSlots);
   __shared__ Step steps[kMaxSteps];
   __shared__ int s_nsteps;
-  __shared__ int s_nslots, s_nshadow;
-  __shared__ short s_shadow_slot[64];
 
   for (int i = threadIdx.x; i < c.nbufs; i += blockDim.x) sbufs[i] = c.bufs[i];
   for (int i = threadIdx.x; i < c.nwts; i += blockDim.x) swts[i] = c.wts[i];
@@ -253,25 +247,6 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       st.slot_end = B.nslots;
     }
     s_nsteps = nsteps;
-    s_nslots = B.nslots;
-    // Operands of buffers the loop never writes (hoisted partials, forward
-    // activations read by the backward, ...) do not depend on the recurrence:
-    // every frame copies this CTA's columns of them into SMEM *before* the
-    // inter-CTA barrier, so the elementwise ops read SMEM instead of paying a
-    // global-memory latency each after it.
-    int nsh = 0;
-    const long long per = (long long)c.S * W;
-    for (int i = 0; i < B.nslots; ++i) {
-      Slot& sl = slots[i];
-      if (sl.role != 0 || sl.inj || nsh >= 64 || (long long)(nsh + 1) * per > c.shadow_floats) continue;
-      if (sbufs[sl.buf].width != W) continue;
-      bool written = false;
-      for (int q = 0; q < B.nslots && !written; ++q) written = slots[q].role == 1 && slots[q].buf == sl.buf;
-      if (written) continue;
-      sl.shadow = nsh;
-      s_shadow_slot[nsh++] = (short)i;
-    }
-    s_nshadow = nsh;
   }
   __syncthreads();
   if (c.use_cache) {
@@ -304,16 +279,6 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     ring.split = (long long)(c.cap - fi.tmod) * c.S;
     ring.frame_rows = (long long)c.cap * c.S;
     SCC_MARK(f, 0)
-    if (s_nshadow) {  // this frame's loop-external operands, own columns (overlaps the barrier)
-      const int per_slot = c.S * ncol;
-      for (int i = threadIdx.x; i < s_nshadow * per_slot; i += blockDim.x) {
-        const int k = i / per_slot, rem = i - k * per_slot;
-        const int srow = rem / ncol, col = j0 + (rem - srow * ncol);
-        const Slot sl = slots[s_shadow_slot[k]];
-        const float* g = resolve(c, sbufs, fi, sl.buf, sl.shift);
-        shadow[(long long)k * c.S * W + (long long)srow * W + col] = g[(long long)srow * W + col];
-      }
-    }
     for (int si = 0; si < s_nsteps; ++si) {
       const Step st = steps[si];
       // the CTAs only exchange data through the dense (GEMM) reads
@@ -323,8 +288,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       for (int i = st.slot_begin + threadIdx.x; i < st.slot_end; i += blockDim.x) {
         const Slot sl = slots[i];
         *reinterpret_cast<float**>(arena + sl.off) =
-            sl.shadow >= 0 ? shadow + (long long)sl.shadow * c.S * W
-                           : ((sl.inj && !fi.inj) ? nullptr : resolve(c, sbufs, fi, sl.buf, sl.shift));
+            (sl.inj && !fi.inj) ? nullptr : resolve(c, sbufs, fi, sl.buf, sl.shift);
       }
       __syncthreads();
       const EwChain* chains = reinterpret_cast<const EwChain*>(arena + st.chains_off);
@@ -390,13 +354,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
           const int srow = rem / ncol, col = rem - srow * ncol;
           const EwChain& ch = chains[jb];
           const float acc = accs[it];
-          FwdScalar fw;
-          for (int k = 0; k < ch.nops; ++k) {
-            ew_apply_fwd(ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc, fw);
-#ifdef RGB_EXP_TRACE
-            if (it == 0 && si == 0 && k < 8) SCC_MARK(f, 6 + k)
-#endif
-          }
+          for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
         }
       } else {
         const int items = c.S * ncol;
@@ -404,8 +362,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
           const EwChain& ch = chains[i];
           for (int e = threadIdx.x; e < items; e += blockDim.x) {
             const int srow = e / ncol, col = j0 + (e - (e / ncol) * ncol);
-            FwdScalar fw;
-            for (int k = 0; k < ch.nops; ++k) ew_apply_fwd(ch.op[k], ch.width, srow, col, ring, false, 0.0f, fw);
+            for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, col, ring, false, 0.0f);
           }
         }
       }
@@ -423,8 +380,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
 size_t scc_smem_bytes(const SccCtx& c) {
   return ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)) +
          (size_t)((c.wcache_floats + 3) & ~3LL) * 4 + (size_t)((c.acc_floats + 3) & ~3LL) * 4 +
-         (size_t)((c.stage_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots +
-         (size_t)c.shadow_floats * 4 + 64;
+         (size_t)((c.stage_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots + 64;
 }
 
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total) {
