@@ -38,41 +38,62 @@ __device__ __forceinline__ void ring_store(float* out, int64_t e, int64_t r, int
 }
 
 // One elementwise op at (row r, unit j).  `acc` replaces op.base when has_acc.
+// Every operand load is issued before the first use (predicated, fully
+// unrolled over the slot counts): the warp stalls once per op instead of once
+// per operand -- the single-stream recurrent loops run these chains on a
+// handful of threads, where each stall is a full memory latency.  Summation
+// order is unchanged (ascending slots).
 __device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
                                          bool has_acc, float acc) {
   const int64_t e = r * width + j;
-  switch (op.kind) {
-    case EW_CONST1:
-      ring_store(op.out, e, r, width, op.out_is_ring, ring, 1.0f);
-      return;
-    case EW_FWD_MUL: {
-      float v = op.fac[0][e];
-      for (int i = 1; i < op.nfac; ++i) v *= op.fac[i][e];
-      ring_store(op.out, e, r, width, op.out_is_ring, ring, v);
-      return;
-    }
-    case EW_FWD_ADD: {
-      float v = has_acc ? acc : (op.base ? op.base[e] : 0.0f);
-      for (int i = 0; i < op.nterm; ++i) v += op.term[i][e];
-      for (int i = 0; i < op.nrank1; ++i) v += op.r1w[i][j] * op.r1src[i][r];
-      ring_store(op.out, e, r, width, op.out_is_ring, ring, act_apply(op.act, v));
-      return;
-    }
-    case EW_BWD: {
-      float v = has_acc ? acc : (op.base ? op.base[e] : 0.0f);
-      for (int i = 0; i < op.nterm; ++i) v += op.term[i][e];
-      if (op.act == ACT_SIGMOID || op.act == ACT_TANH) v *= act_deriv(op.act, op.y[e]);
-      if (op.inj && r >= op.inj_row0) v += op.inj[(r - op.inj_row0) * width + j];  // after f' (engine.py:548-554)
-      op.out[e] = v;
-      for (int i = 0; i < op.nfac; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
-        if (!op.eps[i]) continue;
-        float p = v;
-        for (int k = 0; k < op.nfac; ++k)
-          if (k != i) p *= op.fac[k][e];
-        op.eps[i][e] = p;
-      }
-      return;
-    }
+  const int kind = op.kind;
+  if (kind == EW_CONST1) {
+    ring_store(op.out, e, r, width, op.out_is_ring, ring, 1.0f);
+    return;
+  }
+  const bool mul = kind == EW_FWD_MUL, bwd = kind == EW_BWD;
+  float t[kMaxTerms], f[kMaxFac], rk[kMaxRank1];
+#pragma unroll
+  for (int i = 0; i < kMaxTerms; ++i) t[i] = (!mul && i < op.nterm) ? op.term[i][e] : 0.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) f[i] = ((mul || bwd) && i < op.nfac) ? op.fac[i][e] : 1.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxRank1; ++i) rk[i] = (kind == EW_FWD_ADD && i < op.nrank1) ? op.r1w[i][j] * op.r1src[i][r] : 0.0f;
+  const float base = (!mul && !has_acc && op.base) ? op.base[e] : 0.0f;
+  const bool fprime = bwd && (op.act == ACT_SIGMOID || op.act == ACT_TANH);
+  const float yv = fprime ? op.y[e] : 0.0f;
+  const float inj = (bwd && op.inj && r >= op.inj_row0) ? op.inj[(r - op.inj_row0) * width + j] : 0.0f;
+  if (mul) {
+    float v = f[0];
+#pragma unroll
+    for (int i = 1; i < kMaxFac; ++i)
+      if (i < op.nfac) v *= f[i];
+    ring_store(op.out, e, r, width, op.out_is_ring, ring, v);
+    return;
+  }
+  float v = has_acc ? acc : base;
+#pragma unroll
+  for (int i = 0; i < kMaxTerms; ++i)
+    if (i < op.nterm) v += t[i];
+  if (kind == EW_FWD_ADD) {
+#pragma unroll
+    for (int i = 0; i < kMaxRank1; ++i)
+      if (i < op.nrank1) v += rk[i];
+    ring_store(op.out, e, r, width, op.out_is_ring, ring, act_apply(op.act, v));
+    return;
+  }
+  // EW_BWD
+  if (fprime) v *= act_deriv(op.act, yv);
+  if (op.inj && r >= op.inj_row0) v += inj;  // after f' (engine.py:548-554)
+  op.out[e] = v;
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
+    if (i >= op.nfac || !op.eps[i]) continue;
+    float p = v;
+#pragma unroll
+    for (int k = 0; k < kMaxFac; ++k)
+      if (k != i && k < op.nfac) p *= f[k];
+    op.eps[i][e] = p;
   }
 }
 
@@ -221,26 +242,39 @@ __device__ __forceinline__ void ew_apply_vec(const EwOp& op, int width, const in
     return;
   }
   if (kind == EW_FWD_MUL) {
+    float4 ff[kMaxFac][R];
 #pragma unroll
-    for (int u = 0; u < R; ++u) v[u] = ok[u] ? ld4(op.fac[0], e[u]) : zero;
-    for (int i = 1; i < op.nfac; ++i) {
+    for (int i = 0; i < kMaxFac; ++i) {
 #pragma unroll
-      for (int u = 0; u < R; ++u) t[u] = ok[u] ? ld4(op.fac[i], e[u]) : zero;
+      for (int u = 0; u < R; ++u) ff[i][u] = (i < op.nfac && ok[u]) ? ld4(op.fac[i], e[u]) : zero;
+    }
 #pragma unroll
-      for (int u = 0; u < R; ++u) v[u] = mul4(v[u], t[u]);
+    for (int u = 0; u < R; ++u) v[u] = ff[0][u];
+#pragma unroll
+    for (int i = 1; i < kMaxFac; ++i) {
+      if (i >= op.nfac) break;
+#pragma unroll
+      for (int u = 0; u < R; ++u) v[u] = mul4(v[u], ff[i][u]);
     }
 #pragma unroll
     for (int u = 0; u < R; ++u)
       if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
     return;
   }
+  // all term loads first (one stall per op, not per operand); ascending sum
+  float4 tt[kMaxTerms][R];
+#pragma unroll
+  for (int i = 0; i < kMaxTerms; ++i) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) tt[i][u] = (i < op.nterm && ok[u]) ? ld4(op.term[i], e[u]) : zero;
+  }
 #pragma unroll
   for (int u = 0; u < R; ++u) v[u] = has_acc ? acc[u] : ((op.base && ok[u]) ? ld4(op.base, e[u]) : zero);
-  for (int i = 0; i < op.nterm; ++i) {
 #pragma unroll
-    for (int u = 0; u < R; ++u) t[u] = ok[u] ? ld4(op.term[i], e[u]) : zero;
+  for (int i = 0; i < kMaxTerms; ++i) {
+    if (i >= op.nterm) break;
 #pragma unroll
-    for (int u = 0; u < R; ++u) v[u] = add4(v[u], t[u]);
+    for (int u = 0; u < R; ++u) v[u] = add4(v[u], tt[i][u]);
   }
   if (kind == EW_FWD_ADD) {
     for (int i = 0; i < op.nrank1; ++i) {
