@@ -1608,7 +1608,7 @@ bool persist_enabled() {  // RGB_TC_PERSIST=0 disables the persistent kernels (t
 }
 
 // persistent kernel for launches of at least two waves
-bool use_persistent(int blocks, int bn) { return persist_enabled() && blocks >= 2 * 148 && bn >= 128; }
+bool use_persistent(int blocks, int bn) { return persist_enabled() && blocks > 148 && bn >= 128; }
 
 template <bool PAIR>
 void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s, int cluster = 1) {
