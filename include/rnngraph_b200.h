@@ -13,14 +13,12 @@
  *    buffers and scratch live in ONE caller-allocated device workspace whose
  *    size rgb_plan_workspace_bytes() reports and whose internal layout is
  *    fixed by the schedule program (emitted by paper_1503_02852_b200/schedule.py).
- *  - Weights: one flat fp32 buffer W of 2*n_params floats: every dense
+ *  - Weights: one flat fp32 buffer W of n_params floats: every dense
  *    connection's (dst_size x src_size) row-major matrix at the offset the
- *    program's weight table gives, followed (at +n_params) by its tf32
- *    residual W - trunc_tf32(W) that the 3xTF32 tensor-core GEMMs consume; a
- *    same-layout buffer WT holding the transposes (the reference keeps the
- *    same cache, engine.py:111-139) and their residuals; and a gradient
- *    buffer G of n_params floats.  rgb_sgd_update / rgb_refresh_transpose
- *    maintain the residual halves.
+ *    program's weight table gives; a same-layout buffer WT holding the
+ *    transposes (the reference keeps the same cache, engine.py:111-139); and
+ *    a gradient buffer G of n_params floats.  (The 3xTF32 tensor-core GEMMs
+ *    form the tf32 residuals of their operands in shared memory.)
  *  - Work is enqueued on `stream` (a cudaStream_t); nothing synchronises
  *    except rgb_read_loss().
  *  - Every function returns RGB_OK (0) or an error code; rgb_last_error()
@@ -120,7 +118,7 @@ int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* s
 int rgb_backward_window(rgb_plan* plan, const float* wt, float* g, int h, int h_prime, int sequential,
                         void* stream);
 
-/* sgd_update (engine.py:606-612): W -= lr*G, then WT = W^T. */
+/* sgd_update (engine.py:606-612): W -= lr*G fused with the WT = W^T refresh. */
 int rgb_sgd_update(rgb_plan* plan, float* w, float* wt, const float* g, float lr, void* stream);
 /* Weights.refresh (engine.py:138-139): WT = W^T. */
 int rgb_refresh_transpose(rgb_plan* plan, const float* w, float* wt, void* stream);

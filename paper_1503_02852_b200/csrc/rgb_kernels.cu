@@ -405,44 +405,10 @@ void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t
 }
 
 // ---------------------------------------------------------------------------
-// W <- W - lr * G (engine.py:606-612)
-
-// tf32 residual consumed by the tcgen05 3xTF32 GEMMs (the tensor core truncates
-// its fp32 operands to tf32; see rgb_tc_gemm.cu)
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-
-// lr == 0: only recompute the residual half lo = W - trunc(W) (Weights refresh).
-__global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ lo, const float* __restrict__ g, float lr,
-                           int64_t n) {
-  const int64_t n4 = n / 4;
-  float4* w4 = reinterpret_cast<float4*>(w);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 a = w4[i];
-    if (g) {
-      const float4 b = g4[i];
-      a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
-      w4[i] = a;
-    }
-    l4[i] = make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w));
-  }
-  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    if (g) w[i] -= lr * g[i];
-    lo[i] = tf32_lo(w[i]);
-  }
-}
-
-void launch_sgd(float* w, float* lo, const float* g, float lr, int64_t n, cudaStream_t s) {
-  int64_t blocks = (n / 4 + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  if (blocks < 1) blocks = 1;
-  sgd_kernel<<<(int)blocks, 256, 0, s>>>(w, lo, g, lr, n);
-}
-
-// ---------------------------------------------------------------------------
-// W^T refresh (engine.py:138-139), 32x32 smem tiles, grouped over connections
-
+// SGD fused with the W^T refresh (engine.py:606-612, 138-139): per 32x32 tile
+// of every dense connection, W -= lr * G in place and the updated tile is
+// written transposed into W^T -- one pass (8 B read + 8 B written per
+// parameter instead of a separate update and transpose pass).
 __global__ void transpose_kernel(const __grid_constant__ TransposeGroup p) {
   __shared__ float t[32][33];
   int jid, tile;
@@ -452,16 +418,20 @@ __global__ void transpose_kernel(const __grid_constant__ TransposeGroup p) {
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
   for (int i = ty; i < 32; i += 8) {
     const int r = r0 + i, c = c0 + tx;
-    if (r < jb.rows && c < jb.cols) t[i][tx] = jb.src[(int64_t)r * jb.cols + c];
+    if (r < jb.rows && c < jb.cols) {
+      const int64_t e = (int64_t)r * jb.cols + c;
+      float v = jb.src[e];
+      if (jb.g) {
+        v -= p.lr * jb.g[e];
+        jb.src[e] = v;
+      }
+      t[i][tx] = v;
+    }
   }
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
     const int c = c0 + i, r = r0 + tx;
-    if (r < jb.rows && c < jb.cols) {
-      const float v = t[tx][i];
-      jb.dst[(int64_t)c * jb.rows + r] = v;
-      if (jb.dst_lo) jb.dst_lo[(int64_t)c * jb.rows + r] = tf32_lo(v);
-    }
+    if (r < jb.rows && c < jb.cols) jb.dst[(int64_t)c * jb.rows + r] = t[tx][i];
   }
 }
 

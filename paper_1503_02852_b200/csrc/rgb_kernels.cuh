@@ -14,14 +14,15 @@
 namespace rgb {
 
 struct TransposeJob {
-  const float* src;  // [rows x cols]
-  float* dst;        // [cols x rows]
-  float* dst_lo;     // tf32 residual of dst (or null)
+  float* src;        // [rows x cols] W (updated in place when g is set)
+  float* dst;        // [cols x rows] W^T
+  const float* g;    // [rows x cols] gradient (null: transpose only)
   int rows, cols;
 };
 constexpr int kMaxTr = 48;
 struct TransposeGroup {
-  int njobs, pad;
+  int njobs;
+  float lr;          // W -= lr * g before the transpose (fused SGD)
   int tile_start[kMaxTr + 1];
   int tiles_c[kMaxTr];
   TransposeJob job[kMaxTr];
@@ -59,7 +60,6 @@ void launch_inject_loss(const float* y, const void* target, int target_kind, int
                         double* row_loss, int rows, int width, cudaStream_t s);
 void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t s);
 // W -= lr * G over n floats and lo = W - trunc_tf32(W); g == nullptr: residual only.
-void launch_sgd(float* w, float* lo, const float* g, float lr, int64_t n, cudaStream_t s);
 void launch_transpose(const TransposeGroup& p, cudaStream_t s);
 void launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s);

@@ -956,7 +956,7 @@ int cuda_rc(cudaError_t e, const char* what) {
 
 }  // namespace
 
-static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* stream);
+static int transpose_weights(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream);
 
 extern "C" {
 
@@ -1326,32 +1326,21 @@ int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_pri
 int rgb_sgd_update(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream) {
   if (!p || !w || !wt || !g) return fail(RGB_ERR_KERNEL, "null argument");
   if (!(lr > 0.0f)) return fail(RGB_ERR_ENGINE, "learning rate must be positive, got %g", (double)lr);
-  cudaStream_t st = as_stream(stream);
-  const int slot = prof_start(st);
-  launch_sgd(w, w + p->n_params, g, lr, p->n_params, st);
-  note_launch();
-  prof_stop(slot, st, PROF_SGD, 2.0 * p->n_params, 16.0 * p->n_params);
-  int rc = cuda_rc(cudaGetLastError(), "sgd launch");
-  if (rc) return rc;
-  return transpose_weights(p, w, wt, stream);
+  return transpose_weights(p, w, wt, g, lr, stream);
 }
 
 int rgb_refresh_transpose(rgb_plan* p, const float* w, float* wt, void* stream) {
   if (!p || !w || !wt) return fail(RGB_ERR_KERNEL, "null argument");
-  launch_sgd(const_cast<float*>(w), const_cast<float*>(w) + p->n_params, nullptr, 0.0f, p->n_params,
-             as_stream(stream));
-  note_launch();
-  int rc = cuda_rc(cudaGetLastError(), "residual launch");
-  if (rc) return rc;
-  return transpose_weights(p, w, wt, stream);
+  return transpose_weights(p, const_cast<float*>(w), wt, nullptr, 0.0f, stream);
 }
 
 }  // extern "C"
 
-// W^T and its tf32 residual for every dense connection (grouped launches).
-static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* stream) {
+// (SGD +) W^T for every dense connection (grouped launches).
+static int transpose_weights(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream) {
   TransposeGroup T;
   std::memset(&T, 0, sizeof T);
+  T.lr = lr;
   for (size_t cid = 0; cid < p->wts.size(); ++cid) {
     const WDesc& d = p->wts[cid];
     if (d.rows == 0) continue;
@@ -1359,9 +1348,10 @@ static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* strea
       launch_transpose(T, as_stream(stream));
       note_launch();
       std::memset(&T, 0, sizeof T);
+      T.lr = lr;
     }
     const int j = T.njobs++;
-    T.job[j] = TransposeJob{w + d.off, wt + d.off, wt + p->n_params + d.off, d.rows, d.cols};
+    T.job[j] = TransposeJob{w + d.off, wt + d.off, g ? g + d.off : nullptr, d.rows, d.cols};
     T.tiles_c[j] = (d.cols + 31) / 32;
     T.tile_start[j + 1] = T.tile_start[j] + ((d.rows + 31) / 32) * T.tiles_c[j];
   }
@@ -1371,7 +1361,8 @@ static int transpose_weights(rgb_plan* p, const float* w, float* wt, void* strea
     const int slot = prof_start(as_stream(stream));
     launch_transpose(T, as_stream(stream));
     note_launch();
-    prof_stop(slot, as_stream(stream), PROF_TRANSPOSE, 0.0, 8.0 * elems);
+    prof_stop(slot, as_stream(stream), g ? PROF_SGD : PROF_TRANSPOSE, g ? 2.0 * elems : 0.0,
+              (g ? 16.0 : 8.0) * elems);
   }
   return cuda_rc(cudaGetLastError(), "transpose launch");
 }

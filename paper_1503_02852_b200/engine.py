@@ -176,7 +176,7 @@ class Weights:
         dev = _device()
         # [W | W_lo] and [W^T | W^T_lo]: the second halves hold the tf32 residuals
         # the tensor-core GEMMs consume (refreshed by every update)
-        n2 = 2 * max(self.n_params, 4)
+        n2 = max(self.n_params, 4)
         self.flat = _flat if _flat is not None else torch.zeros(n2, dtype=DTYPE, device=dev)
         self.flat_t = _flat_t if _flat_t is not None else torch.zeros_like(self.flat)
         self._plan = _Plan(weights_program(net))
