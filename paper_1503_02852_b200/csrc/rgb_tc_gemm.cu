@@ -762,7 +762,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // predecessor complete before any global access (PDL launches in frame loops)
+  // PDL (frame loops): only the A operand and the epilogue touch data the
+  // predecessor kernel writes; the weight (B) loads and the whole SMEM/TMEM
+  // pipeline start before it completes.  IS_DW launches are never PDL.
   pdl_trigger();
 
   if (warp == 8 || warp == 10) {
@@ -771,6 +773,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       // (two issuing warps: a single thread's TMA instructions complete one
       // after another at ~25-55 B/clk per SM -- tools/tma_probe.cu)
       const bool load_a = warp == 8;
+      if (load_a) pdl_wait();
       int seg = 0, k0 = 0;
       if constexpr (!IS_DW) {
         for (int skip = s_begin; skip > 0;) {  // locate the first stage of this split
@@ -943,6 +946,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       }
     }
     // ---------------- epilogue ----------------
+    pdl_wait();  // the epilogue reads / writes global data of the frame
     mbar_wait(done, 0);
     if (threadIdx.x == 0) { TRACE(3, 0) }
     CTA_MARK(1)
