@@ -63,6 +63,7 @@ void launch_ew(const EwLaunch& p, cudaStream_t s) {
   int64_t maxw = 1;
   for (int c = 0; c < p.nchains; ++c) maxw = maxw > p.chain[c].width ? maxw : p.chain[c].width;
   int64_t total = (int64_t)p.rows * maxw;
+  if (maxw % 4 == 0) total /= 4;  // the 16-byte path: one thread per 4 units
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
