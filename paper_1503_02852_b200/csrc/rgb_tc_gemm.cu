@@ -1581,7 +1581,13 @@ NtConfig nt_config(const GemmGroup& p) {
     // pairs only when they fill the machine without split-K: small (per-frame)
     // products with a short K range lose more to the pair's longer pipeline
     // start than they gain (cfg4 per-frame GEMMs: 5.2 -> 6.0 ms per step)
+    static int pair_bn = -1;  // RGB_TC_PAIR_BN: force 256 / 128 (tuning experiments)
+    if (pair_bn < 0) {
+      const char* e = getenv("RGB_TC_PAIR_BN");
+      pair_bn = e ? atoi(e) : 0;
+    }
     for (int bn : {256, 128}) {
+      if (pair_bn && bn != pair_bn) continue;
       if (2 * nt_tiles(p, bn, true) >= 120) {
         c.bn = bn;
         c.pair = true;
