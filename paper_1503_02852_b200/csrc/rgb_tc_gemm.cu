@@ -663,11 +663,11 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint6
 }
 
 // commit to the mbarrier at this offset in both CTAs of the pair
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint32_t leader = 0) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"((uint16_t)(3u << leader))
       : "memory");
 }
 
@@ -697,7 +697,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  // cluster rank: a pair is ranks (2i, 2i+1) (cta_group::2 peers differ in
+  // bit 0); with cluster split-K a pair tile's splits are pairs 0..splits-1
+  const uint32_t ctarank = PAIR ? cluster_rank() : 0;
+  const uint32_t rank = ctarank & 1u;        // rank inside the CTA pair
+  const uint32_t leader = ctarank & ~1u;     // the pair's MMA-issuing CTA
   CTA_MARK(0)
   int jid, tile;
   // block -> (output tile, split, pair rank); the splits of one tile are adjacent
@@ -877,10 +881,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
 #endif
           }
         }
-        if constexpr (PAIR) mma_commit_pair(&empty[s]);
+        if constexpr (PAIR) mma_commit_pair(&empty[s], leader);
         else mma_commit(&empty[s]);
       }
-      if constexpr (PAIR) mma_commit_pair(done);
+      if constexpr (PAIR) mma_commit_pair(done, leader);
       else mma_commit(done);
     }
   } else {
@@ -939,7 +943,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         asm volatile("bar.sync 2, 256;" ::: "memory");
         if (threadIdx.x == 0) {
           if (rank == 0) mbar_arrive(&conv_full[s]);
-          else mbar_arrive_cluster(&conv_full[s], 0);
+          else mbar_arrive_cluster(&conv_full[s], leader);
         }
       } else {
         mbar_arrive(&conv_full[s]);
@@ -958,11 +962,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
                         tile_lin * NCTA + (int)rank, split, csplit > 1 ? 1 : splits, 0, BM, csplit > 1 ? 1 : 3);
     CTA_MARK(2)
   }
-  if constexpr (!IS_DW && !PAIR) {
+  if constexpr (!IS_DW) {
     if (csplit > 1) {
       // cluster split-K: the splits of this tile are one cluster; CTA `split`
       // sums rows [split*BM/csplit, ...) of all partial tiles in split order
-      // through distributed shared memory and runs the epilogue on them
+      // through distributed shared memory and runs the epilogue on them (with
+      // pairs: over the split CTAs of the same pair rank, cluster ranks 2k+rank)
       __syncwarp();
       cluster_sync();
       const int r_lo = split * BM / csplit, r_hi = (split + 1) * BM / csplit;
@@ -972,8 +977,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         using CE = Cfg<BN>;
         for (int q = threadIdx.x; q < (r_hi - r_lo) * G4; q += 256) {
           const int off = (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4;
-          float4 a = ld_dsmem4(tile_s + off, 0);
-          for (int k = 1; k < csplit; ++k) a = add4(a, ld_dsmem4(tile_s + off, (uint32_t)k));
+          float4 a = ld_dsmem4(tile_s + off, PAIR ? rank : 0u);
+          for (int k = 1; k < csplit; ++k)
+            a = add4(a, ld_dsmem4(tile_s + off, PAIR ? (uint32_t)(2 * k) + rank : (uint32_t)k));
           *reinterpret_cast<float4*>(tile_s + off) = a;
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -1429,7 +1435,7 @@ void launch_tma(const P& p, int blocks, cudaStream_t s, int cluster = 1) {
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = PAIR ? 2 : cluster;
+    attr[0].val.clusterDim.x = PAIR ? 2 * cluster : cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1552,6 +1558,8 @@ int nt_min_stages(const GemmGroup& p) {
   return kst;
 }
 
+bool csplit_enabled();
+
 struct NtConfig {
   int bn = 32, splits = 1;
   bool pair = false;
@@ -1592,6 +1600,29 @@ NtConfig nt_config(const GemmGroup& p) {
         c.bn = bn;
         c.pair = true;
         return c;
+      }
+    }
+    // few pair tiles, deep K: CTA pairs with cluster split-K (the splits of a
+    // pair tile form one cluster of 2*splits CTAs and reduce through DSMEM)
+    // (opt-in, RGB_TC_PAIRSPLIT=1: measured 2x slower than unpaired split-K on
+    // the cfg4 per-frame shapes -- 8-CTA clusters of ~200 KB CTAs do not all
+    // fit at once -- kept for other shapes / future tuning)
+    static int pair_split = -1;
+    if (pair_split < 0) {
+      const char* e = getenv("RGB_TC_PAIRSPLIT");
+      pair_split = e ? atoi(e) != 0 : 0;
+    }
+    if (pair_split && csplit_enabled() && split_env != 0) {
+      for (int bn : {256, 128}) {
+        if (pair_bn && bn != pair_bn) continue;
+        const int ctas = 2 * nt_tiles(p, bn, true);
+        const int sp = split_for(ctas);
+        if (sp > 1 && ctas * sp >= 96) {
+          c.bn = bn;
+          c.pair = true;
+          c.splits = sp;
+          return c;
+        }
       }
     }
   }
@@ -1648,7 +1679,8 @@ long long tc_gemm_nt_scratch(const GemmGroup& p) {
 
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   NtConfig c = nt_config(p);
-  p.csplit = c.splits > 1 && !c.pair && csplit_enabled() ? 1 : 0;
+  p.csplit = c.splits > 1 && csplit_enabled() ? 1 : 0;
+  if (c.pair && c.splits > 1 && !p.csplit) c.splits = 1;  // pairs split only through the cluster
   if (c.splits > 1 && !p.csplit && (!p.part || nt_scratch(p, c) > p.part_cap)) c.splits = 1;  // no scratch
   if (!p.tma) c = NtConfig{tc::pick_bn([&](int b) { return nt_tiles(p, b, false); }), 1, false};
   p.splits = c.splits;
@@ -1671,7 +1703,7 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
       else tc::launch_persistent<128, false, false>(p, ntiles, s);
     }
   } else if (p.tma) {
-    if (c.pair) launch_nt_bn<true>(p, c.bn, blocks, s);
+    if (c.pair) launch_nt_bn<true>(p, c.bn, blocks, s, p.csplit ? c.splits : 1);
     else launch_nt_bn<false>(p, c.bn, blocks, s, p.csplit ? c.splits : 1);
   } else {
     if (c.bn == 256) tc::launch_one<256, false>(p, blocks, s);

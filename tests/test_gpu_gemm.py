@@ -214,3 +214,32 @@ def test_engine_kernel_variants_agree(restore_tc_modes):
         results.append((out, tr.grads.flat.cpu().numpy(), w.flat[: w.n_params].cpu().numpy()))
     for a, b in zip(results[0], results[1]):
         assert normwise(a, b.astype(np.float64)) < 1e-5
+
+
+def test_pair_cluster_split_k_opt_in():
+    """CTA pairs combined with cluster split-K (opt-in variant, RGB_TC_PAIRSPLIT=1)
+    computed in a subprocess so the environment switch takes effect."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import ctypes, numpy as np, torch\n"
+        "from paper_1503_02852_b200 import _lib\n"
+        "L = _lib.lib()\n"
+        "rng = np.random.default_rng(3)\n"
+        "m, n, k = 512, 2048, 1024\n"
+        "a = rng.uniform(-1, 1, size=(m, k)); b = rng.uniform(-1, 1, size=(n, k))\n"
+        "ta = torch.tensor(a, dtype=torch.float32, device='cuda'); tb = torch.tensor(b, dtype=torch.float32, device='cuda')\n"
+        "tc = torch.full((m, n), float('nan'), device='cuda')\n"
+        "P = lambda t: ctypes.c_void_p(t.data_ptr())\n"
+        "_lib.check(L.rgb_gemm_nt_tma(P(ta), P(tb), P(tb), P(tc), m, n, k, ctypes.c_void_p(0)))\n"
+        "torch.cuda.synchronize()\n"
+        "ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T\n"
+        "err = np.abs(tc.cpu().numpy() - ref).max() / np.abs(ref).max()\n"
+        "assert err < 1e-5, err\n"
+        "print('ok', err)\n")
+    env = dict(os.environ, RGB_TC_PAIRSPLIT="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
