@@ -241,9 +241,24 @@ def measure_intra_stream(P, steps=2):
         e1.record()
         torch.cuda.synchronize()
         res[label] = cfg["hp"] / (e0.elapsed_time(e1) / steps / 1000.0)
+    from paper_1503_02852_b200.condense import condense
+    frame_steps = sum(1 for sn in condense(net).nodes if sn.recurrent) * (cfg["hp"] + cfg["h"])
+    step_us = 1e6 * cfg["hp"] / res["hoisted"]
     return {"workload": "cfg2: " + cfg["desc"], "hoisted_frames_per_s": res["hoisted"],
             "sequential_frames_per_s": res["sequential"], "speedup": res["hoisted"] / res["sequential"],
-            "steps": steps}
+            # whole iteration / recurrent frame steps: an upper bound on the
+            # persistent SCC kernel's per-frame latency (it is ~97% of the step)
+            "us_per_recurrent_frame_step": step_us / frame_steps, "steps": steps}
+
+
+def recurrent_summary(prof, steps, net, hp, h):
+    from paper_1503_02852_b200.condense import condense
+    n_scc = sum(1 for sn in condense(net).nodes if getattr(sn, "recurrent", False))
+    frame_steps = n_scc * (hp + h)
+    ms = sum(prof.get(k, {}).get("ms", 0.0) for k in ("gemm_frame", "ew_frame", "scc")) / steps
+    return {"frame_steps_per_iter": frame_steps, "ms_per_iter": ms,
+            "us_per_frame_step": 1000.0 * ms / frame_steps if frame_steps else None,
+            "share_of_step": ms / max(1e-9, sum(v["ms"] for v in prof.values()) / steps)}
 
 
 def run_ours(args, cfg):
@@ -405,6 +420,10 @@ def run_ours(args, cfg):
                    "schedule": "hoisted (paper §3.1)",
                    "launch": "CUDA-graph replay per ring phase" if graphs else "eager"},
         "algorithmic_tflops": F_iter / (ms / 1000.0) / 1e12,
+        # the frame-sequential (recurrent) part of an iteration: device time of
+        # the per-frame launches (or persistent SCC kernels) per frame step
+        # (layers x frames of the forward chunk and the backward window)
+        "recurrent": recurrent_summary(prof, args.steps, net, hp, h),
         "roofline": roof,
         "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                         "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
