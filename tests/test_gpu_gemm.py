@@ -243,3 +243,14 @@ def test_pair_cluster_split_k_opt_in():
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
+
+
+def test_id_inputs_with_tensor_cores_forced():
+    """Token-id gathers / sorted-scatter dW combined with tcgen05 GEMMs everywhere else."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_gemm_mode(2))
+    try:
+        assert run_pair(P.build_lstm(300, 32, 16), 3, 8, 4, 3, 0.05, 21, ids=True) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_gemm_mode(0))
