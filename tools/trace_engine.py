@@ -26,7 +26,7 @@ def main():
     cfg = dict(bench.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "cfg4"], name="x")
     net = bench.build_net(cfg)
     w = P.Weights.init(net, 0)
-    S = cfg["S"]
+    S = int(sys.argv[3]) if len(sys.argv) > 3 else cfg["S"]
     tr = P.Trainer(net, w, S, P.TrainConfig(h=cfg["h"], h_prime=cfg["hp"], lr=cfg["lr"], iterations=1))
     x = torch.rand((cfg["hp"] * S, cfg["n_in"]), device="cuda") * 2 - 1
     t = torch.randint(0, cfg["n_out"], (cfg["hp"] * S,), device="cuda")
