@@ -28,13 +28,29 @@ __device__ __forceinline__ float act_deriv(int act, float y) {
   return 1.0f;  // identity; softmax only ever appears fused with CE (engine.py:537-543)
 }
 
-__device__ __forceinline__ void ring_store(float* out, int64_t e, int64_t r, int width, bool is_ring,
+// Operand access policy of ew_apply: DirectMem reads and writes global memory
+// only; the recurrent-SCC kernel substitutes a policy that serves operands
+// produced earlier in the same loop body from shared memory (rgb_scc.cu).
+// Slot ids: terms 0-3, factors 4-7, y 8, base 9; stores: out 0, eps 1-4.
+struct DirectMem {
+  __device__ __forceinline__ float ld(int, const float* p) const { return *p; }
+  __device__ __forceinline__ void st(int, float* p, float v) { *p = v; }
+};
+
+template <class M>
+__device__ __forceinline__ void ring_store(M& m, float* out, int64_t e, int64_t r, int width, bool is_ring,
                                            const RingWrite& ring, float v) {
-  out[e] = v;
+  m.st(0, out + e, v);
   if (is_ring) {
     const int64_t moff = ring.frame_rows * width;
-    out[e + (r < ring.split ? moff : -moff)] = v;
+    out[e + (r < ring.split ? moff : -moff)] = v;  // mirror copy: never re-read by the writer's chain
   }
+}
+
+__device__ __forceinline__ void ring_store(float* out, int64_t e, int64_t r, int width, bool is_ring,
+                                           const RingWrite& ring, float v) {
+  DirectMem m;
+  ring_store(m, out, e, r, width, is_ring, ring, v);
 }
 
 // One elementwise op at (row r, unit j).  `acc` replaces op.base when has_acc.
@@ -43,58 +59,108 @@ __device__ __forceinline__ void ring_store(float* out, int64_t e, int64_t r, int
 // per operand -- the single-stream recurrent loops run these chains on a
 // handful of threads, where each stall is a full memory latency.  Summation
 // order is unchanged (ascending slots).
-__device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
-                                         bool has_acc, float acc) {
+//
+// KIND / NT / NF >= 0 fix the op kind and the term / factor counts at compile
+// time (straight-line code, no per-slot branches: the recurrent-SCC kernel
+// dispatches its ops to these, ew_variant below); -1 reads them from the op.
+template <int KIND, int NT, int NF, class M>
+__device__ __forceinline__ void ew_apply_t(M& m, const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
+                                           bool has_acc, float acc) {
+  constexpr int kT = NT >= 0 ? NT : kMaxTerms, kF = NF >= 0 ? NF : kMaxFac;
+  constexpr int kR = KIND < 0 ? kMaxRank1 : 0;  // rank-1 terms only on the generic path
   const int64_t e = r * width + j;
-  const int kind = op.kind;
+  const int kind = KIND >= 0 ? KIND : op.kind;
+  const int nterm = NT >= 0 ? NT : op.nterm, nfac = NF >= 0 ? NF : op.nfac;
   if (kind == EW_CONST1) {
-    ring_store(op.out, e, r, width, op.out_is_ring, ring, 1.0f);
+    ring_store(m, op.out, e, r, width, op.out_is_ring, ring, 1.0f);
     return;
   }
   const bool mul = kind == EW_FWD_MUL, bwd = kind == EW_BWD;
-  float t[kMaxTerms], f[kMaxFac], rk[kMaxRank1];
+  float t[kT > 0 ? kT : 1], f[kF > 0 ? kF : 1], rk[kR > 0 ? kR : 1];
 #pragma unroll
-  for (int i = 0; i < kMaxTerms; ++i) t[i] = (!mul && i < op.nterm) ? op.term[i][e] : 0.0f;
+  for (int i = 0; i < kT; ++i) t[i] = (!mul && i < nterm) ? m.ld(i, op.term[i] + e) : 0.0f;
 #pragma unroll
-  for (int i = 0; i < kMaxFac; ++i) f[i] = ((mul || bwd) && i < op.nfac) ? op.fac[i][e] : 1.0f;
+  for (int i = 0; i < kF; ++i) f[i] = ((mul || bwd) && i < nfac) ? m.ld(4 + i, op.fac[i] + e) : 1.0f;
 #pragma unroll
-  for (int i = 0; i < kMaxRank1; ++i) rk[i] = (kind == EW_FWD_ADD && i < op.nrank1) ? op.r1w[i][j] * op.r1src[i][r] : 0.0f;
-  const float base = (!mul && !has_acc && op.base) ? op.base[e] : 0.0f;
+  for (int i = 0; i < kR; ++i) rk[i] = (kind == EW_FWD_ADD && i < op.nrank1) ? op.r1w[i][j] * op.r1src[i][r] : 0.0f;
+  const float base = (!mul && !has_acc && op.base) ? m.ld(9, op.base + e) : 0.0f;
   const bool fprime = bwd && (op.act == ACT_SIGMOID || op.act == ACT_TANH);
-  const float yv = fprime ? op.y[e] : 0.0f;
+  const float yv = fprime ? m.ld(8, op.y + e) : 0.0f;
   const float inj = (bwd && op.inj && r >= op.inj_row0) ? op.inj[(r - op.inj_row0) * width + j] : 0.0f;
   if (mul) {
     float v = f[0];
 #pragma unroll
-    for (int i = 1; i < kMaxFac; ++i)
-      if (i < op.nfac) v *= f[i];
-    ring_store(op.out, e, r, width, op.out_is_ring, ring, v);
+    for (int i = 1; i < kF; ++i)
+      if (i < nfac) v *= f[i];
+    ring_store(m, op.out, e, r, width, op.out_is_ring, ring, v);
     return;
   }
   float v = has_acc ? acc : base;
 #pragma unroll
-  for (int i = 0; i < kMaxTerms; ++i)
-    if (i < op.nterm) v += t[i];
+  for (int i = 0; i < kT; ++i)
+    if (i < nterm) v += t[i];
   if (kind == EW_FWD_ADD) {
 #pragma unroll
-    for (int i = 0; i < kMaxRank1; ++i)
+    for (int i = 0; i < kR; ++i)
       if (i < op.nrank1) v += rk[i];
-    ring_store(op.out, e, r, width, op.out_is_ring, ring, act_apply(op.act, v));
+    ring_store(m, op.out, e, r, width, op.out_is_ring, ring, act_apply(op.act, v));
     return;
   }
   // EW_BWD
   if (fprime) v *= act_deriv(op.act, yv);
   if (op.inj && r >= op.inj_row0) v += inj;  // after f' (engine.py:548-554)
-  op.out[e] = v;
+  m.st(0, op.out + e, v);
 #pragma unroll
-  for (int i = 0; i < kMaxFac; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
-    if (i >= op.nfac || !op.eps[i]) continue;
+  for (int i = 0; i < kF; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
+    if (i >= nfac || !op.eps[i]) continue;
     float p = v;
 #pragma unroll
-    for (int k = 0; k < kMaxFac; ++k)
-      if (k != i && k < op.nfac) p *= f[k];
-    op.eps[i][e] = p;
+    for (int k = 0; k < kF; ++k)
+      if (k != i && k < nfac) p *= f[k];
+    m.st(1 + i, op.eps[i] + e, p);
   }
+}
+
+template <class M>
+__device__ __forceinline__ void ew_apply(M& m, const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
+                                         bool has_acc, float acc) {
+  ew_apply_t<-1, -1, -1>(m, op, width, r, j, ring, has_acc, acc);
+}
+
+// Specialised instantiations of ew_apply_t for the op shapes the builders
+// emit (LSTM / Elman cells); 0 = generic.
+__host__ __device__ __forceinline__ int ew_variant(int kind, int nterm, int nfac, int nrank1) {
+  if (kind == EW_CONST1) return 1;
+  if (kind == EW_FWD_ADD && nrank1 == 0 && nterm <= 2) return 2 + nterm;         // 2..4
+  if (kind == EW_FWD_MUL && (nfac == 2 || nfac == 3)) return 3 + nfac;            // 5, 6
+  if (kind == EW_BWD && nterm <= 2 && (nfac == 0 || nfac == 2)) return 7 + nterm + (nfac ? 3 : 0);  // 7..12
+  return 0;
+}
+
+template <class M>
+__device__ __forceinline__ void ew_apply_variant(int var, M& m, const EwOp& op, int width, int64_t r, int j,
+                                                 const RingWrite& ring, bool has_acc, float acc) {
+  switch (var) {
+    case 1: ew_apply_t<EW_CONST1, 0, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 2: ew_apply_t<EW_FWD_ADD, 0, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 3: ew_apply_t<EW_FWD_ADD, 1, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 4: ew_apply_t<EW_FWD_ADD, 2, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 5: ew_apply_t<EW_FWD_MUL, 0, 2>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 6: ew_apply_t<EW_FWD_MUL, 0, 3>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 7: ew_apply_t<EW_BWD, 0, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 8: ew_apply_t<EW_BWD, 1, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 9: ew_apply_t<EW_BWD, 2, 0>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 10: ew_apply_t<EW_BWD, 0, 2>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 11: ew_apply_t<EW_BWD, 1, 2>(m, op, width, r, j, ring, has_acc, acc); break;
+    case 12: ew_apply_t<EW_BWD, 2, 2>(m, op, width, r, j, ring, has_acc, acc); break;
+    default: ew_apply_t<-1, -1, -1>(m, op, width, r, j, ring, has_acc, acc); break;
+  }
+}
+
+__device__ __forceinline__ void ew_apply(const EwOp& op, int width, int64_t r, int j, const RingWrite& ring,
+                                         bool has_acc, float acc) {
+  DirectMem m;
+  ew_apply(m, op, width, r, j, ring, has_acc, acc);
 }
 
 // The same op over U independent elements at once.  Every operand stream is

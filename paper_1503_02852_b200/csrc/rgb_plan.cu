@@ -179,6 +179,7 @@ struct rgb_plan {
     bool ok = false;
     int width = 0, blocks = 0, use_cache = 0, cluster = 0;
     long long cache_floats = 0, acc_floats = 0, stage_floats = 0, arena_bytes = 0;
+    int vals_cap = 0, vals_stride = 0;
     size_t smem = 0;
     double flops_per_frame = 0;
   };
@@ -382,7 +383,18 @@ struct rgb_plan {
       sp.smem = scc_smem_bytes(probe);
       if (sp.smem > 200 * 1024) return sp;
     }
-    if (!cluster && scc_max_blocks(sp.smem) < blocks) return sp;  // cooperative: all CTAs co-resident
+    // shared-memory rows for chain values forwarded between ops / frames
+    sp.vals_stride = S * ncol;
+    sp.vals_cap = (int)std::min<long long>(32, (200LL * 1024 - (long long)sp.smem) / (4LL * sp.vals_stride));
+    if (sp.vals_cap < 0) sp.vals_cap = 0;
+    probe.vals_floats = (long long)sp.vals_cap * sp.vals_stride;
+    sp.smem = scc_smem_bytes(probe);
+    if (!cluster && scc_max_blocks(sp.smem) < blocks) {  // cooperative: all CTAs must be co-resident
+      sp.vals_cap = 0;
+      probe.vals_floats = 0;
+      sp.smem = scc_smem_bytes(probe);
+      if (scc_max_blocks(sp.smem) < blocks) return sp;
+    }
     sp.ok = true;
     sp.cluster = cluster ? 1 : 0;
     sp.width = W;
@@ -814,6 +826,9 @@ struct rgb_plan {
             sc.acc_floats = sp.acc_floats;
             sc.stage_floats = sp.stage_floats;
             sc.arena_bytes = sp.arena_bytes;
+            sc.vals_floats = (long long)sp.vals_cap * sp.vals_stride;
+            sc.vals_cap = sp.vals_cap;
+            sc.vals_stride = sp.vals_stride;
             sc.bar = bar_dev;
             const int slot = prof_start(st);
             cudaError_t e = launch_scc(sc, sp.blocks, sp.smem, st);

@@ -35,10 +35,14 @@ namespace rgb {
 #ifdef RGB_EXP_TRACE
 // tuning aid: clock64 marks of CTA 0 / thread 0 for the first frames (tools/trace_scc.py)
 __device__ long long g_scc_trace[64][16];
+__device__ long long g_scc_pro[8];
 #define SCC_MARK(f, k) \
   if (blockIdx.x == 0 && threadIdx.x == 0 && (f) < 64) g_scc_trace[f][k] = clock64();
+#define SCC_PRO(k) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_scc_pro[k] = clock64();
 #else
 #define SCC_MARK(f, k)
+#define SCC_PRO(k)
 #endif
 
 namespace {
@@ -63,13 +67,60 @@ struct SJob {
 struct Slot {
   int off;      // byte offset of the pointer field inside the template arena
   short buf, shift;
-  int inj;      // 1: only valid on injected frames (t > t0)
+  short inj;    // 1: only valid on injected frames (t > t0)
+  short kind;   // SL_READ (element-indexed operand), SL_WRITE, SL_ROW (rank-1 source); SL_EXT: read of
+                // a buffer the loop body never writes (prefetchable)
+};
+enum { SL_READ = 0, SL_WRITE = 1, SL_ROW = 2, SL_EXT = 3 };
+constexpr int kMaxBufBits = 2048;
+
+// Forwarded chain values.  Every op carries 16 code bytes: [0..9] the source
+// of each operand slot (terms 0-3, factors 4-7, y 8, base 9), [10..14]
+// the value index its stores (out, eps 0-3) also write, [15] its ew_variant.  kMem = global
+// memory; otherwise a row of the CTA's shared `vals` array, optionally
+// (kPrev) holding the previous frame's value.
+constexpr unsigned char kMem = 0xFF, kPrev = 0x40;
+constexpr int kMaxRecs = 64;
+constexpr int kMaxExt = 32;
+struct ExtRow {  // an operand the body reads but never writes: staged per frame into vals row `row`
+  short buf, shift, row;
+};
+struct ChainCode {
+  unsigned char c[kMaxChain][16];
+};
+struct OpRec {  // build-time record of one op of the body (thread 0 only)
+  short step, chain, k;
+  short rb[10], rs[10];  // read slots: buffer (-1 none), frame shift
+  short wb[5];           // written buffers (out, eps 0-3), -1 none
+  unsigned char* code;
+};
+
+// ew_apply policy: operands produced earlier in the body by this CTA come from
+// shared memory instead of a global-memory round trip.  The value for local
+// element `el` lives in vals[idx * stride + el]; every (buffer, frame) is
+// written by exactly one op, so a row holds exactly what memory holds.
+struct SccVals {
+  const unsigned char* code;
+  float* vals;
+  int el, stride;
+  bool first;  // first frame of the launch: previous-frame rows are not filled yet
+  __device__ __forceinline__ float ld(int s, const float* p) const {
+    const unsigned cd = code[s];
+    if (cd != kMem && !(first && (cd & kPrev))) return vals[(cd & 0x3F) * stride + el];
+    return *p;
+  }
+  __device__ __forceinline__ void st(int s, float* p, float v) {
+    *p = v;
+    const unsigned cd = code[10 + s];
+    if (cd != kMem) vals[cd * stride + el] = v;
+  }
 };
 
 struct Step {
   int kind, n;          // S_GEMM: n jobs; S_EW: n chains
-  int jobs_off, chains_off;
+  int jobs_off, chains_off, codes_off;
   int slot_begin, slot_end;
+  int pf_end;           // prefetch range [slot_begin, pf_end): up to the next CTA barrier
 };
 
 // Per-frame index bases: ring slot, window index, chunk index of frame t.
@@ -100,6 +151,8 @@ struct Builder {
   Slot* slots;
   int nslots;
   bool ok;
+  OpRec* recs;
+  int nrec, step, nchain;
 
   template <class T>
   __device__ T* alloc(int count, int& off) {
@@ -108,47 +161,76 @@ struct Builder {
     used += count * (int)sizeof(T);
     return reinterpret_cast<T*>(arena + off);
   }
-  __device__ void slot(const void* field, int buf, int shift, int inj = 0) {
+  __device__ void slot(const void* field, int buf, int shift, int inj = 0, int kind = SL_READ) {
     if (nslots >= kMaxSlots) {
       ok = false;
       return;
     }
-    slots[nslots++] = Slot{(int)(reinterpret_cast<const unsigned char*>(field) - arena), (short)buf, (short)shift, inj};
+    slots[nslots++] = Slot{(int)(reinterpret_cast<const unsigned char*>(field) - arena), (short)buf, (short)shift,
+                           (short)inj, (short)kind};
   }
-  __device__ void op(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwOp& o) {
+  __device__ void op(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwOp& o, int k, unsigned char* code) {
+    OpRec dummy;  // past kMaxRecs ops: nrec > kMaxRecs disables forwarding
+    OpRec& R = nrec < kMaxRecs ? recs[nrec] : dummy;
+    ++nrec;
+    R.step = (short)step;
+    R.chain = (short)nchain;
+    R.k = (short)k;
+    R.code = code;
+    for (int i = 0; i < 10; ++i) R.rb[i] = -1, R.rs[i] = 0;
+    for (int i = 0; i < 5; ++i) R.wb[i] = -1;
+    for (int i = 0; i < 16; ++i) code[i] = kMem;
     o.kind = w[pos++];
     o.act = w[pos++];
     const int out = w[pos++];
     o.out = nullptr;
-    slot(&o.out, out, 0);
+    slot(&o.out, out, 0, 0, SL_WRITE);
+    R.wb[0] = (short)out;
     o.out_is_ring = bufs[out].kind == 0;
     o.nterm = w[pos++];
-    for (int i = 0; i < o.nterm; ++i, pos += 2) slot(&o.term[i], w[pos], w[pos + 1]);
+    for (int i = 0; i < o.nterm; ++i, pos += 2) {
+      slot(&o.term[i], w[pos], w[pos + 1]);
+      R.rb[i] = (short)w[pos], R.rs[i] = (short)w[pos + 1];
+    }
     o.nrank1 = w[pos++];
     for (int i = 0; i < o.nrank1; ++i, pos += 3) {
-      slot(&o.r1src[i], w[pos], w[pos + 1]);
+      slot(&o.r1src[i], w[pos], w[pos + 1], 0, SL_ROW);
       o.r1w[i] = c.w + wts[w[pos + 2]].off;  // frame-independent
     }
     o.nfac = w[pos++];
-    for (int i = 0; i < o.nfac; ++i, pos += 2) slot(&o.fac[i], w[pos], w[pos + 1]);
+    for (int i = 0; i < o.nfac; ++i, pos += 2) {
+      slot(&o.fac[i], w[pos], w[pos + 1]);
+      R.rb[4 + i] = (short)w[pos], R.rs[4 + i] = (short)w[pos + 1];
+    }
     o.y = nullptr;
-    if (w[pos] >= 0) slot(&o.y, w[pos], w[pos + 1]);
+    if (w[pos] >= 0) {
+      slot(&o.y, w[pos], w[pos + 1]);
+      R.rb[8] = (short)w[pos], R.rs[8] = (short)w[pos + 1];
+    }
     pos += 2;
     o.base = nullptr;  // -2 (accumulator) stays null
-    if (w[pos] >= 0) slot(&o.base, w[pos], w[pos + 1]);
+    if (w[pos] >= 0) {
+      slot(&o.base, w[pos], w[pos + 1]);
+      R.rb[9] = (short)w[pos], R.rs[9] = (short)w[pos + 1];
+    }
     pos += 2;
     o.inj = nullptr;
     o.inj_row0 = 0;
     if (w[pos++]) slot(&o.inj, c.inj_buf, 0, 1);
     const int neps = w[pos++];
     for (int i = 0; i < kMaxFac; ++i) o.eps[i] = nullptr;
+    code[15] = (unsigned char)ew_variant(o.kind, o.nterm, o.nfac, o.nrank1);
     for (int i = 0; i < neps; ++i, ++pos)
-      if (w[pos] >= 0) slot(&o.eps[i], w[pos], 0);
+      if (w[pos] >= 0) {
+        slot(&o.eps[i], w[pos], 0, 0, SL_WRITE);
+        R.wb[1 + i] = (short)w[pos];
+      }
   }
-  __device__ void chain(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwChain& ch) {
+  __device__ void chain(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwChain& ch, ChainCode& cc) {
     ch.width = w[pos++];
     ch.nops = w[pos++];
-    for (int k = 0; k < ch.nops; ++k) op(c, bufs, wts, ch.op[k]);
+    for (int k = 0; k < ch.nops; ++k) op(c, bufs, wts, ch.op[k], k, cc.c[k]);
+    ++nchain;
   }
 };
 
@@ -186,18 +268,25 @@ __device__ __forceinline__ void sync_ctas(const SccCtx& c, unsigned& my_gen) {
 
 __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_constant__ SccCtx c) {
   extern __shared__ __align__(16) unsigned char sm[];
-  // layout: [tables][weight cache][accumulators][template arena][slots]
+  // layout: [tables][weight cache][accumulators][A stage][forwarded values][template arena][slots]
   SccBuf* sbufs = reinterpret_cast<SccBuf*>(sm);
   SccW* swts = reinterpret_cast<SccW*>(sbufs + c.nbufs);
   float* wcache = reinterpret_cast<float*>(
       sm + ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)));
   float* accs = wcache + ((c.wcache_floats + 3) & ~3LL);
   float* astage = accs + ((c.acc_floats + 3) & ~3LL);
-  unsigned char* arena = reinterpret_cast<unsigned char*>(astage + ((c.stage_floats + 3) & ~3LL));
+  float* vals = astage + ((c.stage_floats + 3) & ~3LL);
+  unsigned char* arena = reinterpret_cast<unsigned char*>(vals + ((c.vals_floats + 3) & ~3LL));
   Slot* slots = reinterpret_cast<Slot*>(arena + c.arena_bytes);
   __shared__ Step steps[kMaxSteps];
   __shared__ int s_nsteps;
+  __shared__ unsigned s_wbits[kMaxBufBits / 32];
+  __shared__ OpRec s_recs[kMaxRecs];
+  __shared__ short s_pend[kMaxRecs * 10];
+  __shared__ int s_nrec, s_next;
+  __shared__ ExtRow s_ext[kMaxExt];
 
+  SCC_PRO(0)
   for (int i = threadIdx.x; i < c.nbufs; i += blockDim.x) sbufs[i] = c.bufs[i];
   for (int i = threadIdx.x; i < c.nwts; i += blockDim.x) swts[i] = c.wts[i];
   const int W = c.width;
@@ -208,16 +297,18 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
 
   // ---- build the templates once (thread 0), preload W_rec rows (all threads)
   if (threadIdx.x == 0) {
-    Builder B{c.body, 0, arena, 0, slots, 0, true};
+    Builder B{c.body, 0, arena, 0, slots, 0, true, s_recs, 0, 0, 0};
     int nsteps = 0, woff = 0;
     while (B.pos < c.body_len && nsteps < kMaxSteps) {
       Step& st = steps[nsteps++];
       st.kind = B.w[B.pos++];
       st.n = B.w[B.pos++];
       st.slot_begin = B.nslots;
+      B.step = nsteps - 1;
       if (st.kind == S_GEMM) {
         SJob* jobs = B.alloc<SJob>(st.n, st.jobs_off);
         EwChain* chains = B.alloc<EwChain>(st.n, st.chains_off);
+        ChainCode* codes = B.alloc<ChainCode>(st.n, st.codes_off);
         for (int jb = 0; jb < st.n; ++jb) {
           SJob& J = jobs[jb];
           J.nseg = B.w[B.pos++];
@@ -236,19 +327,98 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
               J.bs[s] = J.bsrc[s];
             }
           }
-          B.chain(c, sbufs, swts, chains[jb]);
+          B.chain(c, sbufs, swts, chains[jb], codes[jb]);
           J.n = chains[jb].width;
         }
       } else {
         st.jobs_off = 0;
         EwChain* chains = B.alloc<EwChain>(st.n, st.chains_off);
-        for (int i = 0; i < st.n; ++i) B.chain(c, sbufs, swts, chains[i]);
+        ChainCode* codes = B.alloc<ChainCode>(st.n, st.codes_off);
+        for (int i = 0; i < st.n; ++i) B.chain(c, sbufs, swts, chains[i], codes[i]);
       }
       st.slot_end = B.nslots;
     }
     s_nsteps = nsteps;
+    // reads of buffers the body never writes can be prefetched into L1 right
+    // after a CTA barrier (the barrier's acquire is what would drop them)
+    unsigned* wbits = s_wbits;
+    for (int i = 0; i < kMaxBufBits / 32; ++i) wbits[i] = 0;
+    for (int i = 0; i < B.nslots; ++i)
+      if (slots[i].kind == SL_WRITE && slots[i].buf < kMaxBufBits) wbits[slots[i].buf >> 5] |= 1u << (slots[i].buf & 31);
+    for (int i = 0; i < B.nslots; ++i)
+      if (slots[i].kind == SL_READ && slots[i].buf < kMaxBufBits && !(wbits[slots[i].buf >> 5] >> (slots[i].buf & 31) & 1))
+        slots[i].kind = SL_EXT;
+    for (int si = 0; si < nsteps; ++si) {
+      int e = si + 1;
+      while (e < nsteps && steps[e].kind != S_GEMM) ++e;
+      steps[si].pf_end = e < nsteps ? steps[e].slot_begin : B.nslots;
+    }
+    s_nrec = B.nrec;
+    s_next = 0;
   }
   __syncthreads();
+  SCC_PRO(1)
+  // forwarding: a read of (buffer, frame) written by exactly one op of the
+  // body is served from `vals` when that write is already done when the read
+  // runs -- same frame: an earlier step, or an earlier op of the same chain
+  // (same thread); previous frame: a later step, or a later-or-same op of the
+  // same chain (not yet overwritten this frame).  Ops of different chains in
+  // one step run concurrently on other threads: memory.  Pass 1 (all
+  // threads) finds the writer of every read slot, pass 2 (thread 0, body
+  // order) numbers the value rows.
+  if (s_nrec <= kMaxRecs) {
+    const int prev = c.reverse ? 1 : -1;
+    const int nrec = s_nrec;
+    for (int q = threadIdx.x; q < nrec * 10; q += blockDim.x) {
+      const OpRec& R = s_recs[q / 10];
+      const int sl = q % 10;
+      short found = -1;
+      if (R.rb[sl] >= 0 && (R.rs[sl] == 0 || R.rs[sl] == prev)) {
+        int writers = 0, wr = -1, wsl = -1;
+        for (int g = 0; g < nrec; ++g)
+          for (int x = 0; x < 5; ++x)
+            if (s_recs[g].wb[x] == R.rb[sl]) ++writers, wr = g, wsl = x;
+        if (writers == 1) {
+          const OpRec& Wr = s_recs[wr];
+          const bool ok = R.rs[sl] == 0 ? (Wr.step < R.step || (Wr.chain == R.chain && Wr.k < R.k))
+                                        : (Wr.step > R.step || (Wr.chain == R.chain && Wr.k >= R.k));
+          if (ok) found = (short)(wr * 5 + wsl);
+        }
+      }
+      s_pend[q] = found;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nv = 0, next = 0;
+      for (int q = 0; q < nrec * 10; ++q) {
+        const int b = s_recs[q / 10].rb[q % 10], sh = s_recs[q / 10].rs[q % 10];
+        if (b < 0) continue;
+        if (s_pend[q] < 0) {
+          // never written by the body: staged into a row at every frame start
+          if (b >= kMaxBufBits || (s_wbits[b >> 5] >> (b & 31) & 1)) continue;
+          int row = -1;
+          for (int x = 0; x < next; ++x)
+            if (s_ext[x].buf == b && s_ext[x].shift == sh) row = s_ext[x].row;
+          if (row < 0) {
+            if (nv >= c.vals_cap || next >= kMaxExt) continue;
+            row = nv++;
+            s_ext[next++] = ExtRow{(short)b, (short)sh, (short)row};
+          }
+          s_recs[q / 10].code[q % 10] = (unsigned char)row;
+          continue;
+        }
+        unsigned char& dst = s_recs[s_pend[q] / 5].code[10 + s_pend[q] % 5];
+        if (dst == kMem) {
+          if (nv >= c.vals_cap) continue;
+          dst = (unsigned char)nv++;
+        }
+        s_recs[q / 10].code[q % 10] = (unsigned char)(dst | (sh == 0 ? 0 : kPrev));
+      }
+      s_next = next;
+    }
+  }
+  __syncthreads();
+  SCC_PRO(2)
   if (c.use_cache) {
     int off = 0;
     for (int si = 0; si < s_nsteps; ++si) {
@@ -267,6 +437,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   if (!c.cluster && threadIdx.x == 0) my_gen = *reinterpret_cast<volatile unsigned*>(c.bar + 1);
   __syncthreads();
 
+  SCC_PRO(3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int f = 0; f < c.frames; ++f) {
     const long long t = c.reverse ? c.t_first + c.frames - 1 - f : c.t_first + f;
@@ -279,19 +450,44 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     ring.split = (long long)(c.cap - fi.tmod) * c.S;
     ring.frame_rows = (long long)c.cap * c.S;
     SCC_MARK(f, 0)
+    // stage this frame's read-only operands into their vals rows, overlapped
+    // with the first CTA barrier (split arrive / wait on a cluster)
+    const bool g0 = steps[0].kind == S_GEMM;
+    if (g0 && c.cluster) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    {
+      const int nel = c.S * ncol;
+      for (int q = threadIdx.x; q < s_next * nel; q += blockDim.x) {
+        const int x = q / nel, el = q - x * nel;
+        const ExtRow er = s_ext[x];
+        const int srow = el / ncol, col = el - srow * ncol;
+        const float* base = resolve(c, sbufs, fi, er.buf, er.shift);
+        vals[er.row * c.vals_stride + el] = base[(long long)srow * sbufs[er.buf].width + j0 + col];
+      }
+    }
+    if (g0) {
+      if (c.cluster)
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      else
+        grid_barrier(c.bar, c.bar + 1, gridDim.x, my_gen);
+    }
     for (int si = 0; si < s_nsteps; ++si) {
       const Step st = steps[si];
       // the CTAs only exchange data through the dense (GEMM) reads
       SCC_MARK(f, 1 + si * 5)
-      if (st.kind == S_GEMM) sync_ctas(c, my_gen);
+      if (st.kind == S_GEMM && si > 0) sync_ctas(c, my_gen);
       SCC_MARK(f, 2 + si * 5)
-      for (int i = st.slot_begin + threadIdx.x; i < st.slot_end; i += blockDim.x) {
-        const Slot sl = slots[i];
-        *reinterpret_cast<float**>(arena + sl.off) =
-            (sl.inj && !fi.inj) ? nullptr : resolve(c, sbufs, fi, sl.buf, sl.shift);
+      if (si == 0 || st.kind == S_GEMM) {
+        // resolve the frame's pointers up to the next barrier
+        for (int i = st.slot_begin + threadIdx.x; i < st.pf_end; i += blockDim.x) {
+          const Slot sl = slots[i];
+          *reinterpret_cast<float**>(arena + sl.off) =
+              (sl.inj && !fi.inj) ? nullptr : resolve(c, sbufs, fi, sl.buf, sl.shift);
+        }
+        __syncthreads();
       }
-      __syncthreads();
       const EwChain* chains = reinterpret_cast<const EwChain*>(arena + st.chains_off);
+      const ChainCode* codes = reinterpret_cast<const ChainCode*>(arena + st.codes_off);
+      SccVals m{nullptr, vals, 0, c.vals_stride, f == 0};
       if (st.kind == S_GEMM) {
         const SJob* jobs = reinterpret_cast<const SJob*>(arena + st.jobs_off);
         // stage the (small) A operands in shared memory once: every CTA reads
@@ -354,7 +550,12 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
           const int srow = rem / ncol, col = rem - srow * ncol;
           const EwChain& ch = chains[jb];
           const float acc = accs[it];
-          for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
+          m.el = rem;
+          for (int k = 0; k < ch.nops; ++k) {
+            m.code = codes[jb].c[k];
+            ew_apply_variant(m.code[15], m, ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
+            SCC_MARK(f, 6 + k + si * 5)
+          }
         }
       } else {
         const int items = c.S * ncol;
@@ -362,7 +563,11 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
           const EwChain& ch = chains[i];
           for (int e = threadIdx.x; e < items; e += blockDim.x) {
             const int srow = e / ncol, col = j0 + (e - (e / ncol) * ncol);
-            for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, srow, col, ring, false, 0.0f);
+            m.el = e;
+            for (int k = 0; k < ch.nops; ++k) {
+              m.code = codes[i].c[k];
+              ew_apply_variant(m.code[15], m, ch.op[k], ch.width, srow, col, ring, false, 0.0f);
+            }
           }
         }
       }
@@ -380,11 +585,12 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
 size_t scc_smem_bytes(const SccCtx& c) {
   return ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)) +
          (size_t)((c.wcache_floats + 3) & ~3LL) * 4 + (size_t)((c.acc_floats + 3) & ~3LL) * 4 +
-         (size_t)((c.stage_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots + 64;
+         (size_t)((c.stage_floats + 3) & ~3LL) * 4 + (size_t)((c.vals_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots + 64;
 }
 
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total) {
-  return (size_t)max_jobs_total * (sizeof(SJob) + 16) + (size_t)max_chains_total * (sizeof(EwChain) + 16) + 64;
+  return (size_t)max_jobs_total * (sizeof(SJob) + 16) +
+         (size_t)max_chains_total * (sizeof(EwChain) + sizeof(ChainCode) + 32) + 64;
 }
 
 int scc_max_blocks(size_t smem) {
@@ -430,6 +636,7 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
 
 #ifdef RGB_EXP_TRACE
 extern "C" int rgb_exp_scc_trace(long long* out) {
+  if (cudaMemcpyFromSymbol(out + 64 * 16, rgb::g_scc_pro, sizeof(rgb::g_scc_pro)) != cudaSuccess) return 3;
   return cudaMemcpyFromSymbol(out, rgb::g_scc_trace, sizeof(rgb::g_scc_trace)) == cudaSuccess ? 0 : 3;
 }
 #endif

@@ -38,6 +38,8 @@ struct SccCtx {
   long long acc_floats;     // per-CTA accumulator staging
   long long stage_floats;   // per-CTA A-operand staging (0 = read A from global)
   long long arena_bytes;    // per-CTA template arena
+  long long vals_floats;    // per-CTA forwarded chain values: vals_cap x vals_stride floats
+  int vals_cap, vals_stride;
   unsigned* bar;            // [count, generation] of the grid barrier
 };
 

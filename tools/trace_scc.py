@@ -34,9 +34,13 @@ def main():
     for _ in range(3):
         tr.step(x, t)
     torch.cuda.synchronize()
-    buf = np.zeros((64, 16), dtype=np.int64)
+    buf = np.zeros((64 * 16 + 8), dtype=np.int64)
     lib = ctypes.CDLL(sys.argv[1])
     lib.rgb_exp_scc_trace(buf.ctypes.data_as(ctypes.c_void_p))
+    pro = buf[64 * 16:]
+    print("prologue (cycles from entry): build", pro[1] - pro[0], "analysis", pro[2] - pro[0],
+          "W cache", pro[3] - pro[0])
+    buf = buf[:64 * 16].reshape(64, 16)
     for f in range(1, 6):
         row = buf[f]
         nz = np.nonzero(row)[0]
