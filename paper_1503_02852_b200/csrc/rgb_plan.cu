@@ -179,7 +179,7 @@ struct rgb_plan {
     bool ok = false;
     int width = 0, blocks = 0, use_cache = 0, cluster = 0;
     long long cache_floats = 0, acc_floats = 0, stage_floats = 0, arena_bytes = 0;
-    int vals_cap = 0, vals_stride = 0;
+    int vals_cap = 0, vals_stride = 0, ncb = 1, nrb = 1;
     size_t smem = 0;
     double flops_per_frame = 0;
   };
@@ -299,7 +299,7 @@ struct rgb_plan {
     SccPlan sp;
     int64_t pos = 0;
     int W = -1, max_jobs = 0, nsteps = 0, njobs_total = 0, nchains_total = 0, nslots = 0;
-    long long max_step_akf = 0;  // A floats per stream row read by one GEMM step
+    long long max_step_akf = 0;  // A floats per stream row read by one GEMM step (rows padded to round4)
     double macs = 0;
     std::vector<int> ks;  // K of every GEMM segment, in walk order
     auto width_ok = [&](int w) {
@@ -328,7 +328,7 @@ struct rgb_plan {
         if (njobs > max_jobs) max_jobs = njobs;
         njobs_total += njobs;
         nchains_total += njobs;
-        long long step_akf = 0;
+        long long step_akf = 0, step_akf_pad = 0;
         for (int j = 0; j < njobs; ++j) {
           const int nseg = body[pos++];
           nslots += nseg;
@@ -338,6 +338,7 @@ struct rgb_plan {
             const int K = body[pos + 3] ? d.rows : d.cols;
             ks.push_back(K);
             ksum += K;
+            step_akf_pad += (K + 3) & ~3;
           }
           const int width = body[pos], nops = body[pos + 1];
           if (!width_ok(width)) return sp;
@@ -346,7 +347,8 @@ struct rgb_plan {
           macs += (double)S * width * ksum;
           step_akf += ksum;
         }
-        if (step_akf > max_step_akf) max_step_akf = step_akf;
+        (void)step_akf;
+        if (step_akf_pad > max_step_akf) max_step_akf = step_akf_pad;
       } else if (kind == STEP_EW) {
         const int nch = body[pos++];
         nchains_total += nch;
@@ -361,30 +363,58 @@ struct rgb_plan {
       }
     }
     if (W <= 0 || macs > 64.0 * 1024 * 1024 || S > 256 || nsteps > 8 || nslots > 512) return sp;
-    // small per-frame work: one cluster of <= 16 CTAs (hardware cluster barrier,
-    // ~0.2 us); otherwise up to 148 CTAs with the atomic grid barrier (~2.3 us)
-    const bool cluster = macs / 16.0 <= 1024.0 * 1024.0;
-    int blocks = cluster ? (W / 4 < 1 ? 1 : (W / 4 > 16 ? 16 : W / 4)) : (W / 4 < 1 ? 1 : W / 4);
-    if (blocks > 148) blocks = 148;
-    const int ncol = (W + blocks - 1) / blocks;
+    // Preferred: row blocks of streams x a column split of W over ncb <= 16
+    // CTAs, one hardware cluster per row block (cluster barrier ~0.2-0.6 us;
+    // streams never exchange data, so row blocks run independently) with
+    // W_rec rows resident in shared memory.  Fallback when W_rec does not fit
+    // 16 CTAs: one row block over up to 148 CTAs with the atomic grid barrier.
+    auto sizes = [&](int ncb_, int nrb_, SccCtx& pr) {
+      const int ncol_ = (W + ncb_ - 1) / ncb_, nrow_ = (S + nrb_ - 1) / nrb_;
+      pr = SccCtx{};
+      pr.nbufs = (int)bufs.size();
+      pr.nwts = (int)wts.size();
+      pr.acc_floats = (long long)std::max(256, max_jobs * ncol_) * nrow_;
+      pr.arena_bytes = (long long)scc_arena_bytes(njobs_total, nchains_total);
+      pr.wcache_floats = 0;
+      for (int K : ks) pr.wcache_floats += (long long)ncol_ * (((K + 3) & ~3) + 4);
+      pr.stage_floats = max_step_akf * nrow_ <= 16384 ? max_step_akf * nrow_ : 0;
+      return std::make_pair(ncol_, nrow_);
+    };
     SccCtx probe{};
-    probe.nbufs = (int)bufs.size();
-    probe.nwts = (int)wts.size();
-    probe.acc_floats = (long long)max_jobs * S * ncol;
-    probe.arena_bytes = (long long)scc_arena_bytes(njobs_total, nchains_total);
-    probe.wcache_floats = 0;
-    for (int K : ks) probe.wcache_floats += (long long)ncol * K;
-    probe.stage_floats = max_step_akf * S <= 16384 ? max_step_akf * S : 0;
+    int ncb = W / 4 < 1 ? 1 : (W / 4 > 16 ? 16 : W / 4);
+    int nrb = std::max(1, std::min(S, 148 / ncb));
+    bool cluster = true;
+    auto nc = sizes(ncb, nrb, probe);
     sp.use_cache = 1;
     sp.smem = scc_smem_bytes(probe);
-    if (sp.smem > 200 * 1024) {
-      sp.use_cache = 0;
-      probe.wcache_floats = 0;
-      sp.smem = scc_smem_bytes(probe);
-      if (sp.smem > 200 * 1024) return sp;
+    if (sp.smem <= 200 * 1024 && nrb > 1) {
+      // all row blocks must be resident at once (a waiting cluster would
+      // serialise the loop): as many as the GPCs hold clusters of ncb CTAs
+      const int mc = scc_max_clusters(ncb, sp.smem);
+      if (mc < nrb) {
+        nrb = mc;
+        nc = sizes(ncb, nrb, probe);
+        sp.smem = scc_smem_bytes(probe);
+      }
     }
+    if (sp.smem > 200 * 1024) {
+      // W_rec too large for one cluster: the whole width over many CTAs, grid barrier
+      cluster = false;
+      nrb = 1;
+      ncb = W / 4 < 1 ? 1 : (W / 4 > 148 ? 148 : W / 4);
+      nc = sizes(ncb, nrb, probe);
+      sp.smem = scc_smem_bytes(probe);
+      if (sp.smem > 200 * 1024) {
+        sp.use_cache = 0;
+        probe.wcache_floats = 0;
+        sp.smem = scc_smem_bytes(probe);
+        if (sp.smem > 200 * 1024) return sp;
+      }
+    }
+    const int blocks = ncb * nrb;
+    const int ncol = nc.first, nrow = nc.second;
     // shared-memory rows for chain values forwarded between ops / frames
-    sp.vals_stride = S * ncol;
+    sp.vals_stride = nrow * ncol;
     sp.vals_cap = (int)std::min<long long>(32, (200LL * 1024 - (long long)sp.smem) / (4LL * sp.vals_stride));
     if (sp.vals_cap < 0) sp.vals_cap = 0;
     probe.vals_floats = (long long)sp.vals_cap * sp.vals_stride;
@@ -397,6 +427,8 @@ struct rgb_plan {
     }
     sp.ok = true;
     sp.cluster = cluster ? 1 : 0;
+    sp.ncb = ncb;
+    sp.nrb = nrb;
     sp.width = W;
     sp.blocks = blocks;
     sp.cache_floats = probe.wcache_floats;
@@ -828,6 +860,8 @@ struct rgb_plan {
             sc.arena_bytes = sp.arena_bytes;
             sc.vals_floats = (long long)sp.vals_cap * sp.vals_stride;
             sc.vals_cap = sp.vals_cap;
+            sc.ncb = sp.ncb;
+            sc.nrb = sp.nrb;
             sc.vals_stride = sp.vals_stride;
             sc.bar = bar_dev;
             const int slot = prof_start(st);

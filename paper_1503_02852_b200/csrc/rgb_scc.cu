@@ -61,8 +61,11 @@ struct SJob {
   const float* bs[kMaxSegs];  // this CTA's weight rows (shared or global)
   const float* bsrc[kMaxSegs];  // the same rows in global memory (cache source)
   int k[kMaxSegs];
-  int pad[kMaxSegs];
+  int ldb[kMaxSegs];  // row stride of bs: round4(K) + 4 in the cache (conflict-free float4 rows), K in global
+  int boff[kMaxSegs];  // offset of bs in the shared weight cache (floats)
 };
+
+__host__ __device__ __forceinline__ int round4(int k) { return (k + 3) & ~3; }
 
 struct Slot {
   int off;      // byte offset of the pointer field inside the template arena
@@ -153,6 +156,11 @@ struct Builder {
   bool ok;
   OpRec* recs;
   int nrec, step, nchain;
+  short* writer;  // per buffer: rec * 5 + store slot of its only writer, -1 none, -2 several
+  __device__ void wrote(int b, int x) {
+    if (b < 0 || b >= kMaxBufBits || nrec > kMaxRecs) return;
+    writer[b] = writer[b] == -1 ? (short)((nrec - 1) * 5 + x) : (short)-2;
+  }
 
   template <class T>
   __device__ T* alloc(int count, int& off) {
@@ -186,6 +194,7 @@ struct Builder {
     o.out = nullptr;
     slot(&o.out, out, 0, 0, SL_WRITE);
     R.wb[0] = (short)out;
+    wrote(out, 0);
     o.out_is_ring = bufs[out].kind == 0;
     o.nterm = w[pos++];
     for (int i = 0; i < o.nterm; ++i, pos += 2) {
@@ -224,6 +233,7 @@ struct Builder {
       if (w[pos] >= 0) {
         slot(&o.eps[i], w[pos], 0, 0, SL_WRITE);
         R.wb[1 + i] = (short)w[pos];
+        wrote(w[pos], 1 + i);
       }
   }
   __device__ void chain(const SccCtx& c, const SccBuf* bufs, const SccW* wts, EwChain& ch, ChainCode& cc) {
@@ -266,6 +276,42 @@ __device__ __forceinline__ void sync_ctas(const SccCtx& c, unsigned& my_gen) {
   }
 }
 
+// Rows [rg, rg + nr) (nr <= RB) of one output column `col` of job J over the
+// ks-th of KS slices of every K segment: float4 shared-memory reads (A rows
+// broadcast across the warp, padded B rows conflict-free), RB accumulators in
+// registers; partial sums go to outp[r * QT].
+template <int RB>
+__device__ __forceinline__ void dots_rows(const SJob& J, const float* wcache, const float* ablk, int nrow, int rg,
+                                          int nr, int col, int ks, int KS, float* outp, int QT) {
+  float acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0f;
+  for (int s = 0; s < J.nseg; ++s) {
+    const int K4 = round4(J.k[s]) / 4;
+    const int kb = (int)((long long)ks * K4 / KS), ke = (int)((long long)(ks + 1) * K4 / KS);
+    const float4* b4 = reinterpret_cast<const float4*>(wcache + J.boff[s] + col * J.ldb[s]);
+    const float4* a4 = reinterpret_cast<const float4*>(ablk + rg * K4 * 4);
+    ablk += nrow * K4 * 4;
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const float4 bv = b4[k];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (RB == 1 || r < nr) {
+          const float4 av = a4[r * K4 + k];
+          acc[r] = fmaf(av.x, bv.x, acc[r]);
+          acc[r] = fmaf(av.y, bv.y, acc[r]);
+          acc[r] = fmaf(av.z, bv.z, acc[r]);
+          acc[r] = fmaf(av.w, bv.w, acc[r]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+    if (r < nr) outp[(long long)r * QT] = acc[r];
+}
+
 __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_constant__ SccCtx c) {
   extern __shared__ __align__(16) unsigned char sm[];
   // layout: [tables][weight cache][accumulators][A stage][forwarded values][template arena][slots]
@@ -283,21 +329,28 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   __shared__ unsigned s_wbits[kMaxBufBits / 32];
   __shared__ OpRec s_recs[kMaxRecs];
   __shared__ short s_pend[kMaxRecs * 10];
+  __shared__ short s_writer[kMaxBufBits];
   __shared__ int s_nrec, s_next;
   __shared__ ExtRow s_ext[kMaxExt];
 
   SCC_PRO(0)
   for (int i = threadIdx.x; i < c.nbufs; i += blockDim.x) sbufs[i] = c.bufs[i];
+  for (int i = threadIdx.x; i < kMaxBufBits; i += blockDim.x) s_writer[i] = -1;
   for (int i = threadIdx.x; i < c.nwts; i += blockDim.x) swts[i] = c.wts[i];
+  // CTA (rb, cb): streams [r0, r1) x units [j0, j1).  Streams never exchange
+  // data, so only the ncb CTAs of one row block synchronise (one cluster each).
   const int W = c.width;
-  const int j0 = (int)((long long)blockIdx.x * W / gridDim.x);
-  const int j1 = (int)((long long)(blockIdx.x + 1) * W / gridDim.x);
+  const int cb = blockIdx.x % c.ncb, rb = blockIdx.x / c.ncb;
+  const int j0 = (int)((long long)cb * W / c.ncb);
+  const int j1 = (int)((long long)(cb + 1) * W / c.ncb);
   const int ncol = j1 - j0;
+  const int r0 = (int)((long long)rb * c.S / c.nrb), r1 = (int)((long long)(rb + 1) * c.S / c.nrb);
+  const int nrow = r1 - r0;
   __syncthreads();
 
   // ---- build the templates once (thread 0), preload W_rec rows (all threads)
   if (threadIdx.x == 0) {
-    Builder B{c.body, 0, arena, 0, slots, 0, true, s_recs, 0, 0, 0};
+    Builder B{c.body, 0, arena, 0, slots, 0, true, s_recs, 0, 0, 0, s_writer};
     int nsteps = 0, woff = 0;
     while (B.pos < c.body_len && nsteps < kMaxSteps) {
       Step& st = steps[nsteps++];
@@ -322,9 +375,12 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
             J.bsrc[s] = (trans ? c.wt : c.w) + wd.off + (long long)j0 * K;
             if (c.use_cache) {
               J.bs[s] = wcache + woff;
-              woff += ncol * K;
+              J.boff[s] = woff;
+              J.ldb[s] = round4(K) + 4;
+              woff += ncol * J.ldb[s];
             } else {
               J.bs[s] = J.bsrc[s];
+              J.ldb[s] = K;
             }
           }
           B.chain(c, sbufs, swts, chains[jb], codes[jb]);
@@ -373,12 +429,10 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       const OpRec& R = s_recs[q / 10];
       const int sl = q % 10;
       short found = -1;
-      if (R.rb[sl] >= 0 && (R.rs[sl] == 0 || R.rs[sl] == prev)) {
-        int writers = 0, wr = -1, wsl = -1;
-        for (int g = 0; g < nrec; ++g)
-          for (int x = 0; x < 5; ++x)
-            if (s_recs[g].wb[x] == R.rb[sl]) ++writers, wr = g, wsl = x;
-        if (writers == 1) {
+      const int b = R.rb[sl];
+      if (b >= 0 && b < kMaxBufBits && s_writer[b] >= 0 && (R.rs[sl] == 0 || R.rs[sl] == prev)) {
+        const int wr = s_writer[b] / 5, wsl = s_writer[b] % 5;
+        {
           const OpRec& Wr = s_recs[wr];
           const bool ok = R.rs[sl] == 0 ? (Wr.step < R.step || (Wr.chain == R.chain && Wr.k < R.k))
                                         : (Wr.step > R.step || (Wr.chain == R.chain && Wr.k >= R.k));
@@ -390,29 +444,33 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     __syncthreads();
     if (threadIdx.x == 0) {
       int nv = 0, next = 0;
-      for (int q = 0; q < nrec * 10; ++q) {
-        const int b = s_recs[q / 10].rb[q % 10], sh = s_recs[q / 10].rs[q % 10];
-        if (b < 0) continue;
-        if (s_pend[q] < 0) {
-          // never written by the body: staged into a row at every frame start
-          if (b >= kMaxBufBits || (s_wbits[b >> 5] >> (b & 31) & 1)) continue;
-          int row = -1;
-          for (int x = 0; x < next; ++x)
-            if (s_ext[x].buf == b && s_ext[x].shift == sh) row = s_ext[x].row;
-          if (row < 0) {
-            if (nv >= c.vals_cap || next >= kMaxExt) continue;
-            row = nv++;
-            s_ext[next++] = ExtRow{(short)b, (short)sh, (short)row};
+      for (int r = 0; r < nrec; ++r) {
+        OpRec& R = s_recs[r];
+        for (int sl = 0; sl < 10; ++sl) {
+          const int b = R.rb[sl];
+          if (b < 0) continue;
+          const int sh = R.rs[sl], pend = s_pend[r * 10 + sl];
+          if (pend < 0) {
+            // never written by the body: staged into a row at every frame start
+            if (b >= kMaxBufBits || (s_wbits[b >> 5] >> (b & 31) & 1)) continue;
+            int row = -1;
+            for (int x = 0; x < next; ++x)
+              if (s_ext[x].buf == b && s_ext[x].shift == sh) row = s_ext[x].row;
+            if (row < 0) {
+              if (nv >= c.vals_cap || next >= kMaxExt) continue;
+              row = nv++;
+              s_ext[next++] = ExtRow{(short)b, (short)sh, (short)row};
+            }
+            R.code[sl] = (unsigned char)row;
+            continue;
           }
-          s_recs[q / 10].code[q % 10] = (unsigned char)row;
-          continue;
+          unsigned char& dst = s_recs[pend / 5].code[10 + pend % 5];
+          if (dst == kMem) {
+            if (nv >= c.vals_cap) continue;
+            dst = (unsigned char)nv++;
+          }
+          R.code[sl] = (unsigned char)(dst | (sh == 0 ? 0 : kPrev));
         }
-        unsigned char& dst = s_recs[s_pend[q] / 5].code[10 + s_pend[q] % 5];
-        if (dst == kMem) {
-          if (nv >= c.vals_cap) continue;
-          dst = (unsigned char)nv++;
-        }
-        s_recs[q / 10].code[q % 10] = (unsigned char)(dst | (sh == 0 ? 0 : kPrev));
       }
       s_next = next;
     }
@@ -426,10 +484,13 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       const SJob* jobs = reinterpret_cast<const SJob*>(arena + steps[si].jobs_off);
       for (int jb = 0; jb < steps[si].n; ++jb)
         for (int s = 0; s < jobs[jb].nseg; ++s) {
-          const int K = jobs[jb].k[s];
+          const int K = jobs[jb].k[s], ld = jobs[jb].ldb[s];
           const float* src = jobs[jb].bsrc[s];
-          for (int i = threadIdx.x; i < ncol * K; i += blockDim.x) wcache[off + i] = src[i];
-          off += ncol * K;
+          for (int i = threadIdx.x; i < ncol * ld; i += blockDim.x) {
+            const int cc = i / ld, kk = i - cc * ld;
+            wcache[off + i] = kk < K ? src[(long long)cc * K + kk] : 0.0f;
+          }
+          off += ncol * ld;
         }
     }
   }
@@ -455,11 +516,11 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     const bool g0 = steps[0].kind == S_GEMM;
     if (g0 && c.cluster) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     {
-      const int nel = c.S * ncol;
+      const int nel = nrow * ncol;
       for (int q = threadIdx.x; q < s_next * nel; q += blockDim.x) {
         const int x = q / nel, el = q - x * nel;
         const ExtRow er = s_ext[x];
-        const int srow = el / ncol, col = el - srow * ncol;
+        const int srow = r0 + el / ncol, col = el - (el / ncol) * ncol;
         const float* base = resolve(c, sbufs, fi, er.buf, er.shift);
         vals[er.row * c.vals_stride + el] = base[(long long)srow * sbufs[er.buf].width + j0 + col];
       }
@@ -490,79 +551,136 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       SccVals m{nullptr, vals, 0, c.vals_stride, f == 0};
       if (st.kind == S_GEMM) {
         const SJob* jobs = reinterpret_cast<const SJob*>(arena + st.jobs_off);
-        // stage the (small) A operands in shared memory once: every CTA reads
-        // the whole state vector(s) written by its peers in the previous phase
+        // stage the A rows of this row block once (rows padded to round4(K),
+        // zero tail): every CTA reads the state its peers wrote last phase
         const float* a_src[kMaxJobs][kMaxSegs];
+        int lda[kMaxJobs][kMaxSegs];
+        // (one stream row: the warp-per-column-chunk loop below is faster)
+        const bool fast = c.stage_floats > 0 && c.use_cache && nrow >= 2;
         if (c.stage_floats > 0) {
           int off = 0;
           for (int jb = 0; jb < st.n; ++jb)
             for (int s = 0; s < jobs[jb].nseg; ++s) {
-              const int n = c.S * jobs[jb].k[s];
-              const float* src = jobs[jb].a[s];
-              for (int i = threadIdx.x; i < n; i += blockDim.x) astage[off + i] = src[i];
+              const int K = jobs[jb].k[s], ld = round4(K);
+              const float* src = jobs[jb].a[s] + (long long)r0 * K;
+              if ((K & 3) == 0 && ((reinterpret_cast<size_t>(src) & 15) == 0)) {
+                const int n4 = nrow * K / 4;
+                for (int i = threadIdx.x; i < n4; i += blockDim.x)
+                  reinterpret_cast<float4*>(astage + off)[i] = reinterpret_cast<const float4*>(src)[i];
+              } else {
+                for (int i = threadIdx.x; i < nrow * ld; i += blockDim.x) {
+                  const int r = i / ld, k = i - r * ld;
+                  astage[off + i] = k < K ? src[(long long)r * K + k] : 0.0f;
+                }
+              }
               a_src[jb][s] = astage + off;
-              off += n;
+              lda[jb][s] = ld;
+              off += nrow * ld;
             }
           __syncthreads();
         } else {
           for (int jb = 0; jb < st.n; ++jb)
-            for (int s = 0; s < jobs[jb].nseg; ++s) a_src[jb][s] = jobs[jb].a[s];
+            for (int s = 0; s < jobs[jb].nseg; ++s) {
+              a_src[jb][s] = jobs[jb].a[s] + (long long)r0 * jobs[jb].k[s];
+              lda[jb][s] = jobs[jb].k[s];
+            }
         }
         SCC_MARK(f, 3 + si * 5)
-        // phase 1: one warp per (job, stream row, chunk of owned columns)
-        const int nchunks = (ncol + kColChunk - 1) / kColChunk;
-        const int items1 = st.n * c.S * nchunks;
-        for (int it = warp; it < items1; it += nwarps) {
-          const int jb = it / (c.S * nchunks), rem = it - jb * (c.S * nchunks);
-          const int srow = rem / nchunks, c0 = (rem - srow * nchunks) * kColChunk;
-          const SJob& J = jobs[jb];
-          float part[kColChunk];
-#pragma unroll
-          for (int q = 0; q < kColChunk; ++q) part[q] = 0.f;
-          for (int s = 0; s < J.nseg; ++s) {
-            const float* a = a_src[jb][s] + (long long)srow * J.k[s];
-            const float* b = J.bs[s] + (long long)c0 * J.k[s];
-            const int K = J.k[s];
-#pragma unroll 4
-            for (int k = lane; k < K; k += 32) {
-              const float av = a[k];
-#pragma unroll
-              for (int q = 0; q < kColChunk; ++q)
-                if (c0 + q < ncol) part[q] = fmaf(av, b[(long long)q * K + k], part[q]);
+        // accs: [row][q], q = job * ncol + unit (QT columns in all)
+        const int QT = st.n * ncol;
+        if (fast) {
+          // register-blocked SIMT dots: thread (q, ks) owns output column q
+          // for up to 8 rows over the ks-th K slice of every segment; float4
+          // smem reads (A broadcast across the warp, padded B rows
+          // conflict-free); the KS partials are summed through smem
+          int NQ = 1;
+          while (NQ < QT && NQ < (int)blockDim.x) NQ <<= 1;
+          const int KS = blockDim.x / NQ;
+          const int tq = threadIdx.x % NQ, ks = threadIdx.x / NQ;
+          for (int q = tq; q < QT; q += NQ) {
+            const int jb = q / ncol, col = q - jb * ncol;
+            const SJob& J = jobs[jb];
+            int aoff0 = 0;  // this job's first A block in astage (offsets, not pointers:
+            for (int x = 0; x < jb; ++x)  // keeps the loads in the shared window, LDS.128)
+              for (int s = 0; s < jobs[x].nseg; ++s) aoff0 += nrow * round4(jobs[x].k[s]);
+            for (int rg = 0; rg < nrow; rg += 8) {
+              const int nr = min(8, nrow - rg);
+              float* outp = accs + ((long long)ks * nrow + rg) * QT + q;
+              if (nr == 1)
+                dots_rows<1>(J, wcache, astage + aoff0, nrow, rg, 1, col, ks, KS, outp, QT);
+              else if (nr == 2)
+                dots_rows<2>(J, wcache, astage + aoff0, nrow, rg, 2, col, ks, KS, outp, QT);
+              else if (nr <= 4)
+                dots_rows<4>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
+              else
+                dots_rows<8>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
             }
           }
-#pragma unroll
-          for (int q = 0; q < kColChunk; ++q) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+          __syncthreads();
+          if (KS > 1) {
+            for (int o = threadIdx.x; o < nrow * QT; o += blockDim.x) {
+              float v = accs[o];
+              for (int x = 1; x < KS; ++x) v += accs[(long long)x * nrow * QT + o];
+              accs[o] = v;
+            }
+            __syncthreads();
           }
-          if (lane == 0) {
+        } else {
+          // generic: one warp per (job, row, chunk of owned columns), lanes over K
+          const int nchunks = (ncol + kColChunk - 1) / kColChunk;
+          const int items1 = st.n * nrow * nchunks;
+          for (int it = warp; it < items1; it += nwarps) {
+            const int jb = it / (nrow * nchunks), rem = it - jb * (nrow * nchunks);
+            const int r = rem / nchunks, c0 = (rem - r * nchunks) * kColChunk;
+            const SJob& J = jobs[jb];
+            float part[kColChunk];
 #pragma unroll
-            for (int q = 0; q < kColChunk; ++q)
-              if (c0 + q < ncol) accs[(jb * c.S + srow) * ncol + c0 + q] = part[q];
+            for (int q = 0; q < kColChunk; ++q) part[q] = 0.f;
+            for (int s = 0; s < J.nseg; ++s) {
+              const float* a = a_src[jb][s] + (long long)r * lda[jb][s];
+              const float* b = J.bs[s] + (long long)c0 * J.ldb[s];
+              const int K = J.k[s], ldb = J.ldb[s];
+#pragma unroll 4
+              for (int k = lane; k < K; k += 32) {
+                const float av = a[k];
+#pragma unroll
+                for (int q = 0; q < kColChunk; ++q)
+                  if (c0 + q < ncol) part[q] = fmaf(av, b[(long long)q * ldb + k], part[q]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < kColChunk; ++q) {
+#pragma unroll
+              for (int o = 16; o; o >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+            }
+            if (lane == 0) {
+#pragma unroll
+              for (int q = 0; q < kColChunk; ++q)
+                if (c0 + q < ncol) accs[(long long)r * QT + jb * ncol + c0 + q] = part[q];
+            }
           }
+          __syncthreads();
         }
-        __syncthreads();
         SCC_MARK(f, 4 + si * 5)
-        const int items = st.n * c.S * ncol;
+        const int items = nrow * QT;
         for (int it = threadIdx.x; it < items; it += blockDim.x) {
-          const int jb = it / (c.S * ncol), rem = it - jb * (c.S * ncol);
-          const int srow = rem / ncol, col = rem - srow * ncol;
+          const int r = it / QT, q = it - r * QT;
+          const int jb = q / ncol, col = q - jb * ncol;
           const EwChain& ch = chains[jb];
           const float acc = accs[it];
-          m.el = rem;
+          m.el = r * ncol + col;
           for (int k = 0; k < ch.nops; ++k) {
             m.code = codes[jb].c[k];
-            ew_apply_variant(m.code[15], m, ch.op[k], ch.width, srow, j0 + col, ring, k == 0, acc);
+            ew_apply_variant(m.code[15], m, ch.op[k], ch.width, r0 + r, j0 + col, ring, k == 0, acc);
             SCC_MARK(f, 6 + k + si * 5)
           }
         }
       } else {
-        const int items = c.S * ncol;
+        const int items = nrow * ncol;
         for (int i = 0; i < st.n; ++i) {
           const EwChain& ch = chains[i];
           for (int e = threadIdx.x; e < items; e += blockDim.x) {
-            const int srow = e / ncol, col = j0 + (e - (e / ncol) * ncol);
+            const int srow = r0 + e / ncol, col = j0 + (e - (e / ncol) * ncol);
             m.el = e;
             for (int k = 0; k < ch.nops; ++k) {
               m.code = codes[i].c[k];
@@ -606,6 +724,28 @@ int scc_max_blocks(size_t smem) {
   return per_sm * sms;
 }
 
+int scc_max_clusters(int ncb, size_t smem) {
+  cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncb);
+  cfg.blockDim = dim3(kSccThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ncb;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, scc_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n < 1 ? 1 : n;
+}
+
 cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s) {
   // the attribute is per function, not per launch: (re)set it for this size
   cudaError_t e = cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -620,7 +760,7 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = blocks;
+    attr[0].val.clusterDim.x = c.ncb;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

@@ -33,7 +33,8 @@ struct SccCtx {
   long long t1, t0, chunk_base;
   int S, cap, hmax, maxd;
   int inj_buf, use_cache;
-  int cluster;              // 1: one thread-block cluster, hardware cluster barrier
+  int cluster;              // 1: one thread-block cluster per row block, hardware cluster barrier
+  int ncb, nrb;             // CTAs per row block (column split of W) x row blocks (stream split of S)
   long long wcache_floats;  // per-CTA shared-memory weight cache (0 = read W from global)
   long long acc_floats;     // per-CTA accumulator staging
   long long stage_floats;   // per-CTA A-operand staging (0 = read A from global)
@@ -46,6 +47,7 @@ struct SccCtx {
 size_t scc_smem_bytes(const SccCtx& c);
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total);
 int scc_max_blocks(size_t smem);  // co-resident CTAs for a cooperative launch
+int scc_max_clusters(int ncb, size_t smem);  // co-resident clusters of ncb CTAs
 cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s);
 
 }  // namespace rgb
