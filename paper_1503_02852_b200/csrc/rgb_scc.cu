@@ -486,9 +486,27 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
         for (int s = 0; s < jobs[jb].nseg; ++s) {
           const int K = jobs[jb].k[s], ld = jobs[jb].ldb[s];
           const float* src = jobs[jb].bsrc[s];
-          for (int i = threadIdx.x; i < ncol * ld; i += blockDim.x) {
-            const int cc = i / ld, kk = i - cc * ld;
-            wcache[off + i] = kk < K ? src[(long long)cc * K + kk] : 0.0f;
+          if ((K & 3) == 0 && (reinterpret_cast<size_t>(src) & 15) == 0) {
+            // float4 rows, 8 loads in flight per thread before the stores
+            const int k4 = K / 4, l4 = ld / 4, n4 = ncol * k4;
+            for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * blockDim.x) {
+              float4 v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (i0 + u * (int)blockDim.x < n4) v[u] = reinterpret_cast<const float4*>(src)[i0 + u * blockDim.x];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < n4) reinterpret_cast<float4*>(wcache + off)[(i / k4) * l4 + i % k4] = v[u];
+              }
+            }
+            for (int i = threadIdx.x; i < ncol; i += blockDim.x)  // zero row pads
+              reinterpret_cast<float4*>(wcache + off)[i * l4 + k4] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            for (int i = threadIdx.x; i < ncol * ld; i += blockDim.x) {
+              const int cc = i / ld, kk = i - cc * ld;
+              wcache[off + i] = kk < K ? src[(long long)cc * K + kk] : 0.0f;
+            }
           }
           off += ncol * ld;
         }
@@ -517,12 +535,36 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     if (g0 && c.cluster) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     {
       const int nel = nrow * ncol;
-      for (int q = threadIdx.x; q < s_next * nel; q += blockDim.x) {
-        const int x = q / nel, el = q - x * nel;
-        const ExtRow er = s_ext[x];
-        const int srow = r0 + el / ncol, col = el - (el / ncol) * ncol;
-        const float* base = resolve(c, sbufs, fi, er.buf, er.shift);
-        vals[er.row * c.vals_stride + el] = base[(long long)srow * sbufs[er.buf].width + j0 + col];
+      const int nq = s_next * nel;
+      if (nq <= (int)blockDim.x) {  // one element per thread (single stream rows)
+        const int q = threadIdx.x;
+        if (q < nq) {
+          const int x = q / nel, el = q - x * nel;
+          const ExtRow er = s_ext[x];
+          const int srow = r0 + el / ncol, col = el - (el / ncol) * ncol;
+          const float* base = resolve(c, sbufs, fi, er.buf, er.shift);
+          vals[er.row * c.vals_stride + el] = base[(long long)srow * sbufs[er.buf].width + j0 + col];
+        }
+      } else
+      for (int q0 = threadIdx.x; q0 < nq; q0 += 8 * blockDim.x) {
+        float v[8];  // all loads in flight before the stores
+        int dst[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * blockDim.x;
+          dst[u] = -1;
+          if (q < nq) {
+            const int x = q / nel, el = q - x * nel;
+            const ExtRow er = s_ext[x];
+            const int srow = r0 + el / ncol, col = el - (el / ncol) * ncol;
+            const float* base = resolve(c, sbufs, fi, er.buf, er.shift);
+            v[u] = base[(long long)srow * sbufs[er.buf].width + j0 + col];
+            dst[u] = er.row * c.vals_stride + el;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dst[u] >= 0) vals[dst[u]] = v[u];
       }
     }
     if (g0) {
@@ -565,8 +607,15 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
               const float* src = jobs[jb].a[s] + (long long)r0 * K;
               if ((K & 3) == 0 && ((reinterpret_cast<size_t>(src) & 15) == 0)) {
                 const int n4 = nrow * K / 4;
-                for (int i = threadIdx.x; i < n4; i += blockDim.x)
-                  reinterpret_cast<float4*>(astage + off)[i] = reinterpret_cast<const float4*>(src)[i];
+                for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * blockDim.x) {
+                  float4 v[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (i0 + u * (int)blockDim.x < n4) v[u] = reinterpret_cast<const float4*>(src)[i0 + u * blockDim.x];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (i0 + u * (int)blockDim.x < n4) reinterpret_cast<float4*>(astage + off)[i0 + u * blockDim.x] = v[u];
+                }
               } else {
                 for (int i = threadIdx.x; i < nrow * ld; i += blockDim.x) {
                   const int r = i / ld, k = i - r * ld;
@@ -603,8 +652,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
             int aoff0 = 0;  // this job's first A block in astage (offsets, not pointers:
             for (int x = 0; x < jb; ++x)  // keeps the loads in the shared window, LDS.128)
               for (int s = 0; s < jobs[x].nseg; ++s) aoff0 += nrow * round4(jobs[x].k[s]);
-            for (int rg = 0; rg < nrow; rg += 8) {
-              const int nr = min(8, nrow - rg);
+            for (int rg = 0; rg < nrow; rg += 16) {
+              const int nr = min(16, nrow - rg);
               float* outp = accs + ((long long)ks * nrow + rg) * QT + q;
               if (nr == 1)
                 dots_rows<1>(J, wcache, astage + aoff0, nrow, rg, 1, col, ks, KS, outp, QT);
@@ -612,8 +661,10 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
                 dots_rows<2>(J, wcache, astage + aoff0, nrow, rg, 2, col, ks, KS, outp, QT);
               else if (nr <= 4)
                 dots_rows<4>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
-              else
+              else if (nr <= 8)
                 dots_rows<8>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
+              else
+                dots_rows<16>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
             }
           }
           __syncthreads();

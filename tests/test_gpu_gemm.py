@@ -108,6 +108,27 @@ def test_persistent_scc_matches_per_frame_launches():
     assert run_pair(P.build_custom_graph(16, 512, 16), 1, 32, 16, 3, 1e-3, 8) < 1e-4
 
 
+@pytest.mark.parametrize("n_hidden,S", [(64, 24), (1024, 2), (42, 40)])
+def test_persistent_scc_layouts(n_hidden, S):
+    """Persistent SCC kernel layouts: several stream rows per CTA (register-
+    blocked float4 dots), a W_rec too large for one cluster (grid-barrier
+    fallback over many CTAs), an odd width (K not a multiple of 4, uneven
+    column split).  The persistent kernel must actually run."""
+    import ctypes
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    L.rgb_profile_reset()
+    L.rgb_profile_enable(1)
+    try:
+        assert run_pair(P.build_lstm(8, n_hidden, 6), S, 8, 4, 2, 0.05, 31) < 1e-4
+        L.rgb_profile_collect()
+    finally:
+        L.rgb_profile_enable(0)
+    ms, n, fl, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+    L.rgb_profile_read(9, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl), ctypes.byref(by))
+    assert n.value > 0, "persistent SCC kernel did not run"
+
+
 def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
