@@ -25,6 +25,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 
 #include "rgb_ew.cuh"
 #include "rgb_kernels.cuh"
@@ -477,6 +478,9 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   }
   __syncthreads();
   SCC_PRO(2)
+  // everything above reads only the plan's own tables: with programmatic
+  // dependent launch it overlaps the tail of the preceding kernel
+  pdl_wait();
   if (c.use_cache) {
     int off = 0;
     for (int si = 0; si < s_nsteps; ++si) {
@@ -775,6 +779,11 @@ int scc_max_blocks(size_t smem) {
   return per_sm * sms;
 }
 
+static int g_scc_pdl = [] {
+  const char* e = getenv("RGB_SCC_PDL");
+  return e ? atoi(e) : 1;
+}();
+
 int scc_max_clusters(int ncb, size_t smem) {
   cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(scc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -809,13 +818,15 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
     cfg.blockDim = dim3(kSccThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = c.ncb;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = g_scc_pdl;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, scc_kernel, c);
   }
   void* args[] = {const_cast<SccCtx*>(&c)};
