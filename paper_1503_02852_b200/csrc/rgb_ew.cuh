@@ -400,15 +400,135 @@ __device__ __forceinline__ void ew_apply_vec(const EwOp& op, int width, const in
   }
 }
 
+// Specialised vector op (KIND, NT terms, NF factors fixed at compile time,
+// ew_variant ids 2-12): every operand of the op -- terms, base, y, injection
+// and the co-factors -- is loaded before its first store (the co-factors
+// belong to other layers, never to this op's out / eps), so the op costs one
+// memory latency; with the counts known the register arrays hold only what
+// the op uses.  Arithmetic per element is exactly ew_apply's.
+template <int R, int KIND, int NT, int NF>
+__device__ __forceinline__ void ew_apply_vec_t(const EwOp& op, int width, const int64_t (&r)[R], int j,
+                                               const bool (&ok)[R], const RingWrite& ring, bool has_acc,
+                                               const float4 (&acc)[R]) {
+  int64_t e[R];
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f), one = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+  for (int u = 0; u < R; ++u) e[u] = r[u] * width + j;
+  if constexpr (KIND == EW_CONST1) {
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, one);
+    return;
+  } else {
+    constexpr bool kBwd = KIND == EW_BWD, kMul = KIND == EW_FWD_MUL;
+    // bx: the base (FWD_ADD without accumulator) or the stored y for f' (BWD);
+    // BWD ops with a base or an injection take the generic path (dispatcher)
+    float4 tt[NT > 0 ? NT : 1][R], ff[NF > 0 ? NF : 1][R], bx[R];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) tt[i][u] = ok[u] ? ld4(op.term[i], e[u]) : zero;
+    }
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) ff[i][u] = ok[u] ? ld4(op.fac[i], e[u]) : one;
+    }
+    const bool has_base = KIND == EW_FWD_ADD && !has_acc && op.base;
+    const bool fprime = kBwd && (op.act == ACT_SIGMOID || op.act == ACT_TANH);
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      bx[u] = (has_base && ok[u]) ? ld4(op.base, e[u]) : ((fprime && ok[u]) ? ld4(op.y, e[u]) : zero);
+    float4 v[R];
+    if constexpr (kMul) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        v[u] = ff[0][u];
+#pragma unroll
+        for (int i = 1; i < NF; ++i) v[u] = mul4(v[u], ff[i][u]);
+        if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
+      }
+      return;
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        v[u] = has_acc ? acc[u] : (kBwd ? zero : bx[u]);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) v[u] = add4(v[u], tt[i][u]);
+      }
+      if constexpr (KIND == EW_FWD_ADD) {
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const float4 a = make_float4(act_apply(op.act, v[u].x), act_apply(op.act, v[u].y),
+                                       act_apply(op.act, v[u].z), act_apply(op.act, v[u].w));
+          if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, a);
+        }
+        return;
+      } else {
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          if (fprime)
+            v[u] = mul4(v[u], make_float4(act_deriv(op.act, bx[u].x), act_deriv(op.act, bx[u].y),
+                                          act_deriv(op.act, bx[u].z), act_deriv(op.act, bx[u].w)));
+          if (ok[u]) st4(op.out, e[u], v[u]);
+        }
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {  // eps_m = delta * prod_{other} z (engine.py:558-566)
+          if (!op.eps[i]) continue;
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            float4 p = v[u];
+#pragma unroll
+            for (int k = 0; k < NF; ++k)
+              if (k != i) p = mul4(p, ff[k][u]);
+            if (ok[u]) st4(op.eps[i], e[u], p);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void ew_apply_vec_variant(const EwOp& op, int width, const int64_t (&r)[R], int j,
+                                                     const bool (&ok)[R], const RingWrite& ring, bool has_acc,
+                                                     const float4 (&acc)[R]) {
+  int var = ew_variant(op.kind, op.nterm, op.nfac, op.nrank1);
+  if (op.kind == EW_BWD && (op.inj || (op.base && !has_acc))) var = 0;
+  switch (var) {
+    case 1: ew_apply_vec_t<R, EW_CONST1, 0, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 2: ew_apply_vec_t<R, EW_FWD_ADD, 0, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 3: ew_apply_vec_t<R, EW_FWD_ADD, 1, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 4: ew_apply_vec_t<R, EW_FWD_ADD, 2, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 5: ew_apply_vec_t<R, EW_FWD_MUL, 0, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 6: ew_apply_vec_t<R, EW_FWD_MUL, 0, 3>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 7: ew_apply_vec_t<R, EW_BWD, 0, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 8: ew_apply_vec_t<R, EW_BWD, 1, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 9: ew_apply_vec_t<R, EW_BWD, 2, 0>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 10: ew_apply_vec_t<R, EW_BWD, 0, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 11: ew_apply_vec_t<R, EW_BWD, 1, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
+    case 12: ew_apply_vec_t<R, EW_BWD, 2, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
+    default: ew_apply_vec<R>(op, width, r, j, ok, ring, has_acc, acc); break;
+  }
+}
+
 // the whole chain on R rows x 4 units; op 0 takes `acc` (GEMM epilogues).
 // Latency note: every op waits for its own operand loads, so the callers
 // give each thread as many rows (R) as registers allow -- one memory latency
 // per op covers all of them.
-template <int R>
+template <int R, bool SPEC = true>
 __device__ __forceinline__ void ew_chain_vec(const EwChain& ch, int width, const int64_t (&r)[R], int j,
                                              const bool (&ok)[R], const RingWrite& ring, bool has_acc,
                                              const float4 (&acc)[R]) {
-  for (int k = 0; k < ch.nops; ++k) ew_apply_vec<R>(ch.op[k], width, r, j, ok, ring, has_acc && k == 0, acc);
+  // SPEC: specialised single-latency ops (latency-bound per-frame epilogues);
+  // the persistent GEMM's epilogue overlaps other tiles and keeps the lean
+  // generic form (no spills at its 136-register budget)
+  for (int k = 0; k < ch.nops; ++k) {
+    if constexpr (SPEC)
+      ew_apply_vec_variant<R>(ch.op[k], width, r, j, ok, ring, has_acc && k == 0, acc);
+    else
+      ew_apply_vec<R>(ch.op[k], width, r, j, ok, ring, has_acc && k == 0, acc);
+  }
 }
 
 }  // namespace rgb

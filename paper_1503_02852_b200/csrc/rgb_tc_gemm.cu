@@ -365,7 +365,7 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
 #ifdef RGB_EXP_TRACE
           if (threadIdx.x == 0) { TRACE(3, 16) }
           for (int k = 0; k < epi.nops; ++k) {
-            ew_apply_vec<R>(epi.op[k], N, rr, n0 + cl, ok, ring, k == 0, acc);
+            ew_apply_vec_variant<R>(epi.op[k], N, rr, n0 + cl, ok, ring, k == 0, acc);
             if (threadIdx.x == 0) { TRACE(3, 17 + k) }
           }
 #else
@@ -1346,7 +1346,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
                         make_float4(p.alpha * a4[u].x, p.alpha * a4[u].y, p.alpha * a4[u].z, p.alpha * a4[u].w));
               } else {
                 const RingWrite ring = p.ring;
-                ew_chain_vec<RE>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
+                ew_chain_vec<RE, false>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
               }
             }
           }
