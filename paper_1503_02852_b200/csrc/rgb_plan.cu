@@ -373,7 +373,7 @@ struct rgb_plan {
       pr = SccCtx{};
       pr.nbufs = (int)bufs.size();
       pr.nwts = (int)wts.size();
-      pr.acc_floats = (long long)std::max(256, max_jobs * ncol_) * nrow_;
+      pr.acc_floats = (long long)std::max(kSccThreads, max_jobs * ncol_) * nrow_;
       pr.arena_bytes = (long long)scc_arena_bytes(njobs_total, nchains_total);
       pr.wcache_floats = 0;
       for (int K : ks) pr.wcache_floats += (long long)ncol_ * (((K + 3) & ~3) + 4);
@@ -862,6 +862,9 @@ struct rgb_plan {
             sc.vals_cap = sp.vals_cap;
             sc.ncb = sp.ncb;
             sc.nrb = sp.nrb;
+            // one chain element per thread: 256 threads unless a CTA owns more
+            // (single-stream loops pay for every extra warp at each __syncthreads)
+            sc.threads = (long long)sp.vals_stride > 256 ? kSccThreads : 256;
             sc.vals_stride = sp.vals_stride;
             sc.bar = bar_dev;
             const int slot = prof_start(st);

@@ -48,7 +48,6 @@ __device__ long long g_scc_pro[8];
 
 namespace {
 
-constexpr int kSccThreads = 256;
 constexpr int kColChunk = 4;   // owned weight rows dotted per pass over an A row
 constexpr int kMaxSteps = 8;
 constexpr int kMaxSlots = 512;
@@ -647,7 +646,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
           // smem reads (A broadcast across the warp, padded B rows
           // conflict-free); the KS partials are summed through smem
           int NQ = 1;
-          while (NQ < QT && NQ < (int)blockDim.x) NQ <<= 1;
+          while (NQ < QT && NQ < 128) NQ <<= 1;  // kSccThreads = 3 * 128
           const int KS = blockDim.x / NQ;
           const int tq = threadIdx.x % NQ, ks = threadIdx.x / NQ;
           for (int q = tq; q < QT; q += NQ) {
@@ -656,8 +655,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
             int aoff0 = 0;  // this job's first A block in astage (offsets, not pointers:
             for (int x = 0; x < jb; ++x)  // keeps the loads in the shared window, LDS.128)
               for (int s = 0; s < jobs[x].nseg; ++s) aoff0 += nrow * round4(jobs[x].k[s]);
-            for (int rg = 0; rg < nrow; rg += 16) {
-              const int nr = min(16, nrow - rg);
+            for (int rg = 0; rg < nrow; rg += 12) {
+              const int nr = min(12, nrow - rg);
               float* outp = accs + ((long long)ks * nrow + rg) * QT + q;
               if (nr == 1)
                 dots_rows<1>(J, wcache, astage + aoff0, nrow, rg, 1, col, ks, KS, outp, QT);
@@ -668,7 +667,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
               else if (nr <= 8)
                 dots_rows<8>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
               else
-                dots_rows<16>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
+                dots_rows<12>(J, wcache, astage + aoff0, nrow, rg, nr, col, ks, KS, outp, QT);
             }
           }
           __syncthreads();
@@ -815,7 +814,7 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(kSccThreads);
+    cfg.blockDim = dim3(c.threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -830,7 +829,7 @@ cudaError_t launch_scc(const SccCtx& c, int blocks, size_t smem, cudaStream_t s)
     return cudaLaunchKernelEx(&cfg, scc_kernel, c);
   }
   void* args[] = {const_cast<SccCtx*>(&c)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scc_kernel), dim3(blocks), dim3(kSccThreads), args,
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scc_kernel), dim3(blocks), dim3(c.threads), args,
                                      smem, s);
 }
 

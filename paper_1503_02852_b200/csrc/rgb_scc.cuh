@@ -9,6 +9,10 @@
 
 namespace rgb {
 
+// threads per CTA of the persistent SCC kernel (12 warps: one chain element
+// per thread for up to 384 (stream row, unit) pairs per CTA)
+constexpr int kSccThreads = 384;
+
 struct SccBuf {
   int kind, width;
   long long off;
@@ -35,6 +39,7 @@ struct SccCtx {
   int inj_buf, use_cache;
   int cluster;              // 1: one thread-block cluster per row block, hardware cluster barrier
   int ncb, nrb;             // CTAs per row block (column split of W) x row blocks (stream split of S)
+  int threads;              // CTA size: 256, or kSccThreads when a CTA owns more than 256 elements
   long long wcache_floats;  // per-CTA shared-memory weight cache (0 = read W from global)
   long long acc_floats;     // per-CTA accumulator staging
   long long stage_floats;   // per-CTA A-operand staging (0 = read A from global)
