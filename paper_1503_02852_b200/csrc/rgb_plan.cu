@@ -13,6 +13,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -74,6 +75,11 @@ struct Ctx {
 
 // persistent SCC kernel switch (1 = use it for eligible loops)
 int g_scc_mode = 1;
+// SCC template images reused across launches (RGB_SCC_TCACHE=0 rebuilds every launch)
+int g_scc_tcache = [] {
+  const char* e = getenv("RGB_SCC_TCACHE");
+  return e ? atoi(e) : 1;
+}();
 
 // algorithmic bytes of one elementwise chain over `rows` rows (reads + one
 // write per output; the ring mirror copy is an implementation cost, not counted)
@@ -175,12 +181,18 @@ struct rgb_plan {
   SccBuf* bufs_dev = nullptr;
   SccW* wts_dev = nullptr;
   unsigned* bar_dev = nullptr;
+  // template images of the persistent SCC loops (one 64-KB slot per loop body,
+  // zeroed at plan creation; the first launch of a body fills its slot)
+  static constexpr int kTcacheSlots = 32;
+  unsigned char* tcache_pool = nullptr;
+  int tcache_next = 0;
   struct SccPlan {
     bool ok = false;
     int width = 0, blocks = 0, use_cache = 0, cluster = 0;
     long long cache_floats = 0, acc_floats = 0, stage_floats = 0, arena_bytes = 0;
     int vals_cap = 0, vals_stride = 0, ncb = 1, nrb = 1;
     size_t smem = 0;
+    unsigned char* tcache = nullptr;
     double flops_per_frame = 0;
   };
   std::map<std::pair<int, int64_t>, SccPlan> scc_plans;
@@ -264,6 +276,7 @@ struct rgb_plan {
     if (bufs_dev) cudaFree(bufs_dev);
     if (wts_dev) cudaFree(wts_dev);
     if (bar_dev) cudaFree(bar_dev);
+    if (tcache_pool) cudaFree(tcache_pool);
   }
 
   int upload_scc_tables() {
@@ -282,11 +295,13 @@ struct rgb_plan {
       if (hw.empty()) hw.push_back(SccW{});
       if (cudaMalloc(&bufs_dev, hb.size() * sizeof(SccBuf)) != cudaSuccess ||
           cudaMalloc(&wts_dev, hw.size() * sizeof(SccW)) != cudaSuccess ||
-          cudaMalloc(&bar_dev, 2 * sizeof(unsigned)) != cudaSuccess)
+          cudaMalloc(&bar_dev, 2 * sizeof(unsigned)) != cudaSuccess ||
+          cudaMalloc(&tcache_pool, (size_t)kTcacheSlots * kSccTcacheBytes) != cudaSuccess)
         return fail(RGB_ERR_CUDA, "SCC table allocation failed");
       if (cudaMemcpy(bufs_dev, hb.data(), hb.size() * sizeof(SccBuf), cudaMemcpyHostToDevice) != cudaSuccess ||
           cudaMemcpy(wts_dev, hw.data(), hw.size() * sizeof(SccW), cudaMemcpyHostToDevice) != cudaSuccess ||
-          cudaMemset(bar_dev, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+          cudaMemset(bar_dev, 0, 2 * sizeof(unsigned)) != cudaSuccess ||
+          cudaMemset(tcache_pool, 0, (size_t)kTcacheSlots * kSccTcacheBytes) != cudaSuccess)
         return fail(RGB_ERR_CUDA, "SCC table upload failed");
     }
     return RGB_OK;
@@ -827,7 +842,12 @@ struct rgb_plan {
         if (g_scc_mode && g_gemm_mode != 2 && !id_mode && c.section >= 0 && c.frames >= 2 && prog_dev[c.section]) {
           const std::pair<int, int64_t> key{c.section, (int64_t)(body - c.sec_base)};
           auto found = scc_plans.find(key);
-          if (found == scc_plans.end()) found = scc_plans.emplace(key, plan_scc(body, len)).first;
+          if (found == scc_plans.end()) {
+            found = scc_plans.emplace(key, plan_scc(body, len)).first;
+            SccPlan& np = found->second;
+            if (np.ok && tcache_pool && tcache_next < kTcacheSlots && scc_tcache_fits(np.arena_bytes))
+              np.tcache = tcache_pool + (size_t)(tcache_next++) * kSccTcacheBytes;
+          }
           const SccPlan& sp = found->second;
           if (sp.ok) {
             SccCtx sc{};
@@ -867,6 +887,7 @@ struct rgb_plan {
             sc.threads = (long long)sp.vals_stride > 256 ? kSccThreads : 256;
             sc.vals_stride = sp.vals_stride;
             sc.bar = bar_dev;
+            sc.tcache = g_scc_tcache ? sp.tcache : nullptr;
             const int slot = prof_start(st);
             cudaError_t e = launch_scc(sc, sp.blocks, sp.smem, st);
             note_launch();

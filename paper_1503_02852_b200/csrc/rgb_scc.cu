@@ -63,6 +63,7 @@ struct SJob {
   int k[kMaxSegs];
   int ldb[kMaxSegs];  // row stride of bs: round4(K) + 4 in the cache (conflict-free float4 rows), K in global
   int boff[kMaxSegs];  // offset of bs in the shared weight cache (floats)
+  short cid[kMaxSegs], trans[kMaxSegs];
 };
 
 __host__ __device__ __forceinline__ int round4(int k) { return (k + 3) & ~3; }
@@ -85,6 +86,7 @@ constexpr int kMaxBufBits = 2048;
 constexpr unsigned char kMem = 0xFF, kPrev = 0x40;
 constexpr int kMaxRecs = 64;
 constexpr int kMaxExt = 32;
+constexpr int kTcacheMagic = 0x5cc7e301;
 struct ExtRow {  // an operand the body reads but never writes: staged per frame into vals row `row`
   short buf, shift, row;
 };
@@ -157,6 +159,7 @@ struct Builder {
   OpRec* recs;
   int nrec, step, nchain;
   short* writer;  // per buffer: rec * 5 + store slot of its only writer, -1 none, -2 several
+  bool has_r1;    // an op holds frame-independent rank-1 weight pointers (no template caching)
   __device__ void wrote(int b, int x) {
     if (b < 0 || b >= kMaxBufBits || nrec > kMaxRecs) return;
     writer[b] = writer[b] == -1 ? (short)((nrec - 1) * 5 + x) : (short)-2;
@@ -202,6 +205,7 @@ struct Builder {
       R.rb[i] = (short)w[pos], R.rs[i] = (short)w[pos + 1];
     }
     o.nrank1 = w[pos++];
+    if (o.nrank1 > 0) has_r1 = true;
     for (int i = 0; i < o.nrank1; ++i, pos += 3) {
       slot(&o.r1src[i], w[pos], w[pos + 1], 0, SL_ROW);
       o.r1w[i] = c.w + wts[w[pos + 2]].off;  // frame-independent
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   __shared__ short s_writer[kMaxBufBits];
   __shared__ int s_nrec, s_next;
   __shared__ ExtRow s_ext[kMaxExt];
+  __shared__ int s_cached, s_nslots, s_cacheable;
 
   SCC_PRO(0)
   for (int i = threadIdx.x; i < c.nbufs; i += blockDim.x) sbufs[i] = c.bufs[i];
@@ -348,9 +353,53 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
   const int nrow = r1 - r0;
   __syncthreads();
 
+  // ---- template image: [header 16 B][arena][slots][steps][read-only rows]
+  const long long img_arena = 16, img_slots = img_arena + ((c.arena_bytes + 15) & ~15LL);
+  const long long img_steps = img_slots + ((sizeof(Slot) * kMaxSlots + 15) & ~size_t(15));
+  const long long img_ext = img_steps + ((sizeof(Step) * kMaxSteps + 15) & ~size_t(15));
+  if (threadIdx.x == 0) s_cached = c.tcache && *reinterpret_cast<volatile int*>(c.tcache) == kTcacheMagic;
+  __syncthreads();
+  if (s_cached) {
+    // a previous launch of this body built the templates: copy them in
+    const int* hdr = reinterpret_cast<const int*>(c.tcache);
+    for (long long i = threadIdx.x; i < c.arena_bytes / 4; i += blockDim.x)
+      reinterpret_cast<int*>(arena)[i] = reinterpret_cast<const int*>(c.tcache + img_arena)[i];
+    for (int i = threadIdx.x; i < hdr[3] * (int)(sizeof(Slot) / 4); i += blockDim.x)
+      reinterpret_cast<int*>(slots)[i] = reinterpret_cast<const int*>(c.tcache + img_slots)[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(Step) * kMaxSteps / 4); i += blockDim.x)
+      reinterpret_cast<int*>(steps)[i] = reinterpret_cast<const int*>(c.tcache + img_steps)[i];
+    for (int i = threadIdx.x; i < kMaxExt; i += blockDim.x)
+      s_ext[i] = reinterpret_cast<const ExtRow*>(c.tcache + img_ext)[i];
+    if (threadIdx.x == 0) {
+      s_nsteps = hdr[1];
+      s_next = hdr[2];
+    }
+    __syncthreads();
+    // per-CTA / per-launch fields: this CTA's weight rows and their place in
+    // the shared cache (ncol differs between CTAs when ncb does not divide W)
+    if (threadIdx.x == 0) {
+      int woff = 0;
+      for (int si = 0; si < s_nsteps; ++si) {
+        if (steps[si].kind != S_GEMM) continue;
+        SJob* jobs = reinterpret_cast<SJob*>(arena + steps[si].jobs_off);
+        for (int jb = 0; jb < steps[si].n; ++jb)
+          for (int s = 0; s < jobs[jb].nseg; ++s) {
+            SJob& J = jobs[jb];
+            J.bsrc[s] = (J.trans[s] ? c.wt : c.w) + swts[J.cid[s]].off + (long long)j0 * J.k[s];
+            if (c.use_cache) {
+              J.boff[s] = woff;
+              J.bs[s] = wcache + woff;
+              woff += ncol * J.ldb[s];
+            } else {
+              J.bs[s] = J.bsrc[s];
+            }
+          }
+      }
+    }
+  } else {
   // ---- build the templates once (thread 0), preload W_rec rows (all threads)
   if (threadIdx.x == 0) {
-    Builder B{c.body, 0, arena, 0, slots, 0, true, s_recs, 0, 0, 0, s_writer};
+    Builder B{c.body, 0, arena, 0, slots, 0, true, s_recs, 0, 0, 0, s_writer, false};
     int nsteps = 0, woff = 0;
     while (B.pos < c.body_len && nsteps < kMaxSteps) {
       Step& st = steps[nsteps++];
@@ -373,6 +422,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
             J.a[s] = nullptr;
             B.slot(&J.a[s], ab, ash);
             J.bsrc[s] = (trans ? c.wt : c.w) + wd.off + (long long)j0 * K;
+            J.cid[s] = (short)cid;
+            J.trans[s] = (short)trans;
             if (c.use_cache) {
               J.bs[s] = wcache + woff;
               J.boff[s] = woff;
@@ -411,6 +462,8 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
     }
     s_nrec = B.nrec;
     s_next = 0;
+    s_nslots = B.nslots;
+    s_cacheable = B.ok && !B.has_r1;
   }
   __syncthreads();
   SCC_PRO(1)
@@ -475,6 +528,28 @@ __global__ void __launch_bounds__(kSccThreads, 1) scc_kernel(const __grid_consta
       s_next = next;
     }
   }
+  __syncthreads();
+  if (c.tcache && blockIdx.x == 0 && s_cacheable) {
+    // publish the templates for the next launches of this body
+    for (long long i = threadIdx.x; i < c.arena_bytes / 4; i += blockDim.x)
+      reinterpret_cast<int*>(c.tcache + img_arena)[i] = reinterpret_cast<const int*>(arena)[i];
+    for (int i = threadIdx.x; i < s_nslots * (int)(sizeof(Slot) / 4); i += blockDim.x)
+      reinterpret_cast<int*>(c.tcache + img_slots)[i] = reinterpret_cast<const int*>(slots)[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(Step) * kMaxSteps / 4); i += blockDim.x)
+      reinterpret_cast<int*>(c.tcache + img_steps)[i] = reinterpret_cast<const int*>(steps)[i];
+    for (int i = threadIdx.x; i < kMaxExt; i += blockDim.x)
+      reinterpret_cast<ExtRow*>(c.tcache + img_ext)[i] = s_ext[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* hdr = reinterpret_cast<int*>(c.tcache);
+      hdr[1] = s_nsteps;
+      hdr[2] = s_next;
+      hdr[3] = s_nslots;
+      __threadfence();
+      atomicExch(hdr, kTcacheMagic);
+    }
+  }
+  }  // built here
   __syncthreads();
   SCC_PRO(2)
   // everything above reads only the plan's own tables: with programmatic
@@ -758,6 +833,12 @@ size_t scc_smem_bytes(const SccCtx& c) {
   return ((sizeof(SccBuf) * c.nbufs + sizeof(SccW) * c.nwts + 15) & ~size_t(15)) +
          (size_t)((c.wcache_floats + 3) & ~3LL) * 4 + (size_t)((c.acc_floats + 3) & ~3LL) * 4 +
          (size_t)((c.stage_floats + 3) & ~3LL) * 4 + (size_t)((c.vals_floats + 3) & ~3LL) * 4 + c.arena_bytes + sizeof(Slot) * kMaxSlots + 64;
+}
+
+bool scc_tcache_fits(long long arena_bytes) {
+  return 16 + ((arena_bytes + 15) & ~15LL) + (long long)((sizeof(Slot) * kMaxSlots + 15) & ~size_t(15)) +
+             (long long)((sizeof(Step) * kMaxSteps + 15) & ~size_t(15)) + (long long)sizeof(ExtRow) * kMaxExt <=
+         kSccTcacheBytes;
 }
 
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total) {

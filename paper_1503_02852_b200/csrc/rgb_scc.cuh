@@ -40,6 +40,7 @@ struct SccCtx {
   int cluster;              // 1: one thread-block cluster per row block, hardware cluster barrier
   int ncb, nrb;             // CTAs per row block (column split of W) x row blocks (stream split of S)
   int threads;              // CTA size: 256, or kSccThreads when a CTA owns more than 256 elements
+  unsigned char* tcache;    // this loop body's template image (built by the first launch), or null
   long long wcache_floats;  // per-CTA shared-memory weight cache (0 = read W from global)
   long long acc_floats;     // per-CTA accumulator staging
   long long stage_floats;   // per-CTA A-operand staging (0 = read A from global)
@@ -49,6 +50,8 @@ struct SccCtx {
   unsigned* bar;            // [count, generation] of the grid barrier
 };
 
+constexpr int kSccTcacheBytes = 64 * 1024;  // per loop body
+bool scc_tcache_fits(long long arena_bytes);
 size_t scc_smem_bytes(const SccCtx& c);
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total);
 int scc_max_blocks(size_t smem);  // co-resident CTAs for a cooperative launch
