@@ -508,7 +508,23 @@ __device__ __forceinline__ void ew_apply_vec_variant(const EwOp& op, int width, 
     case 10: ew_apply_vec_t<R, EW_BWD, 0, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
     case 11: ew_apply_vec_t<R, EW_BWD, 1, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
     case 12: ew_apply_vec_t<R, EW_BWD, 2, 2>(op, width, r, j, ok, ring, has_acc, acc); break;
-    default: ew_apply_vec<R>(op, width, r, j, ok, ring, has_acc, acc); break;
+    default:
+      if constexpr (R > 4 && R % 4 == 0) {
+        // generic ops in quarters of 4 rows: the generic form's operand arrays at
+        // R = 8 would spill
+#pragma unroll 1
+        for (int h = 0; h < R; h += 4) {
+          int64_t rh[4];
+          bool okh[4];
+          float4 acch[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rh[u] = r[h + u], okh[u] = ok[h + u], acch[u] = acc[h + u];
+          ew_apply_vec<4>(op, width, rh, j, okh, ring, has_acc, acch);
+        }
+      } else {
+        ew_apply_vec<R>(op, width, r, j, ok, ring, has_acc, acc);
+      }
+      break;
   }
 }
 

@@ -336,7 +336,10 @@ __device__ __forceinline__ void epilogue(const P& p, int jid, int m0, int n0, in
     constexpr int LPR = BN >= 128 ? 32 : BN / 4;  // lanes per row
     constexpr int RPW = 32 / LPR;                  // rows per warp access
     constexpr int CG = BN / 4 / LPR;               // float4 groups per lane per row
-    constexpr int R = 4;  // rows per thread and pass: one operand latency per op covers 4 rows
+#ifndef RGB_EPI_R
+#define RGB_EPI_R 4
+#endif
+    constexpr int R = RGB_EPI_R;  // rows per thread and pass: one operand latency per op covers R rows
     const int sub = lane / LPR, lc = lane % LPR;
 #pragma unroll 1
     for (int rb = r_lo + warp * RPW + sub; rb < nrows; rb += 8 * RPW * R) {
