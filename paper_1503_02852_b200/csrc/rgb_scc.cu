@@ -842,8 +842,9 @@ bool scc_tcache_fits(long long arena_bytes) {
 }
 
 size_t scc_arena_bytes(int max_jobs_total, int max_chains_total) {
-  return (size_t)max_jobs_total * (sizeof(SJob) + 16) +
-         (size_t)max_chains_total * (sizeof(EwChain) + sizeof(ChainCode) + 32) + 64;
+  const size_t b = (size_t)max_jobs_total * (sizeof(SJob) + 16) +
+                   (size_t)max_chains_total * (sizeof(EwChain) + sizeof(ChainCode) + 32) + 64;
+  return (b + 15) & ~size_t(15);  // the slot table follows the arena
 }
 
 int scc_max_blocks(size_t smem) {
