@@ -139,6 +139,11 @@ int rgb_set_gemm_mode(int mode);
  * with W_rec resident in shared memory and a grid barrier per dense
  * dependency; 0 launches the loop body once per frame. */
 int rgb_set_scc_mode(int on);
+/* Cross-layer wavefront: the stages between persistent SCC
+ * loops of a forward / backward section run on their own streams over frame
+ * blocks (default on; env RGB_WAVEFRONT=0 or rgb_set_wavefront(0) disables).
+ * No reference counterpart (schedule switch; results equal within fp32). */
+int rgb_set_wavefront(int on);
 /* Stand-alone GEMM forms (kernel-level parity tests): C[m,n] = A[m,k] . B[n,k]
  * (both row-major) and G[m,n] = alpha * sum_r E[r,m] Y[r,n]; mode 1 SIMT,
  * 2 tcgen05. */

@@ -100,7 +100,60 @@ double ew_bytes(const EwChain& ch, int64_t rows) {
 int g_gemm_mode = 0;
 constexpr double kTcMinFlops = 32.0 * 1024 * 1024;
 
+int cuda_rc(cudaError_t e, const char* what);
+
+// set while a wavefront runs stages on several streams: tensor-core GEMMs
+// that would need the plan's shared split-K scratch run on the SIMT kernels
+bool g_wavefront_active = false;
 bool use_tc(double flops) { return g_gemm_mode == 2 || (g_gemm_mode == 0 && flops >= kTcMinFlops); }
+
+// cross-layer wavefront of the forward section; 1 = on
+int g_wavefront = [] {
+  const char* e = getenv("RGB_WAVEFRONT");
+  return e ? atoi(e) : 1;
+}();
+
+// words of the step at p[i] (kind word included), without running it; -1: unknown
+int64_t step_words(const int32_t* p, int64_t i, int64_t n) {
+  const int64_t i0 = i;
+  auto skip_op = [&](int64_t q) {
+    q += 3;
+    q += 1 + 2 * (int64_t)p[q];
+    q += 1 + 3 * (int64_t)p[q];
+    q += 1 + 2 * (int64_t)p[q];
+    q += 5;
+    q += 1 + (int64_t)p[q];
+    return q;
+  };
+  auto skip_chain = [&](int64_t q) {
+    const int nops = p[q + 1];
+    q += 2;
+    for (int k = 0; k < nops; ++k) q = skip_op(q);
+    return q;
+  };
+  const int kind = p[i++];
+  if (kind == STEP_EW) {
+    const int nc = p[i++];
+    for (int k = 0; k < nc; ++k) i = skip_chain(i);
+  } else if (kind == STEP_GEMM) {
+    const int nj = p[i++];
+    for (int j = 0; j < nj; ++j) {
+      const int ns = p[i++];
+      i = skip_chain(i + 4 * (int64_t)ns);
+    }
+  } else if (kind == STEP_SOFTMAX) {
+    i += 1;
+  } else if (kind == STEP_LOOP) {
+    const int len = p[i + 1];
+    i += 2 + len;
+  } else if (kind == STEP_DW) {
+    const int nj = p[i++];
+    i += 5 * (int64_t)nj;
+  } else {
+    return -1;
+  }
+  return i <= n ? i - i0 : -1;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -184,6 +237,10 @@ struct rgb_plan {
   // template images of the persistent SCC loops (one 64-KB slot per loop body,
   // zeroed at plan creation; the first launch of a body fills its slot)
   static constexpr int kTcacheSlots = 32;
+  // wavefront: extra streams (one per stage after the first) and events
+  std::vector<cudaStream_t> wf_streams;
+  std::vector<cudaEvent_t> wf_events;
+  int wf_ok[4] = {-1, -1, -1, -1};  // per section: structure eligible (cached after the first look)
   unsigned char* tcache_pool = nullptr;
   int tcache_next = 0;
   struct SccPlan {
@@ -277,6 +334,8 @@ struct rgb_plan {
     if (wts_dev) cudaFree(wts_dev);
     if (bar_dev) cudaFree(bar_dev);
     if (tcache_pool) cudaFree(tcache_pool);
+    for (auto e : wf_events) cudaEventDestroy(e);
+    for (auto q : wf_streams) cudaStreamDestroy(q);
   }
 
   int upload_scc_tables() {
@@ -727,6 +786,101 @@ struct rgb_plan {
     return RGB_OK;
   }
 
+  // Cross-layer wavefront of a forward or backward section.  The
+  // section's top-level steps are cut after every loop into stages (stage k =
+  // the hoisted steps feeding SCC loop k, then the loop); the chunk's frames
+  // are cut into blocks.  Stage k runs on its own stream, block after block
+  // (the loop's recurrence continues across blocks), and block b of stage k
+  // waits only for block b of stage k-1: layer l+1's loop over block b runs
+  // beside layer l's loop over block b+1.  Every step of a forward section is
+  // causal (reads frames <= its own, delays >= 0); a backward section reads
+  // errors of frames >= its own (engine.py:519-531), so its blocks run from
+  // the newest frames down and its whole-window dW runs after the join.
+  // Used for >= 2 persistent-kernel loops; otherwise *done = false and the
+  // caller runs the section as usual.
+  int run_wavefront(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st, bool* done) {
+    *done = false;
+    const bool bwd = c.section == 1;  // backward: blocks from the newest frames down, dW after the join
+    if (!g_wavefront || !g_scc_mode || id_mode || g_gemm_mode == 2 || (c.section != 0 && !bwd) ||
+        !prog_dev[c.section] || wf_ok[c.section] == 0)
+      return RGB_OK;
+    // blocks of >= 16 frames, >= 4 of them (fewer blocks overlap too little to pay)
+    const int B = std::max(16, (c.frames + 7) / 8);
+    const int nb = (c.frames + B - 1) / B;
+    if (nb < 4) return RGB_OK;
+    wf_ok[c.section] = 0;  // until the structure checks below pass
+    std::vector<int64_t> starts;
+    std::vector<int> kinds;
+    for (int64_t i = 0; i < n;) {
+      const int64_t w = step_words(p, i, n);
+      if (w <= 0) return RGB_OK;
+      starts.push_back(i);
+      kinds.push_back(p[i]);
+      i += w;
+    }
+    starts.push_back(n);
+    // trailing dW steps (whole window) run after the join
+    int nsteps = (int)kinds.size();
+    while (nsteps > 0 && kinds[nsteps - 1] == STEP_DW) --nsteps;
+    std::vector<std::pair<int, int>> stages;
+    int first = 0, nloops = 0;
+    for (int s = 0; s < nsteps; ++s) {
+      if (kinds[s] == STEP_DW) return RGB_OK;
+      if (kinds[s] != STEP_LOOP) continue;
+      const int32_t* body = p + starts[s] + 3;
+      const int len = p[starts[s] + 2];
+      const std::pair<int, int64_t> key{c.section, (int64_t)(body - c.sec_base)};
+      auto found = scc_plans.find(key);
+      if (found == scc_plans.end()) found = scc_plans.emplace(key, plan_scc(body, len)).first;
+      if (!found->second.ok) return RGB_OK;
+      stages.push_back({first, s});
+      first = s + 1;
+      ++nloops;
+    }
+    if (first < nsteps) stages.push_back({first, nsteps - 1});
+    if (nloops < 2) return RGB_OK;
+    wf_ok[c.section] = 1;
+    const int ns = (int)stages.size();
+    const size_t need_ev = (size_t)ns * nb + 1;
+    if ((int)wf_streams.size() < ns - 1 || wf_events.size() < need_ev) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return RGB_OK;  // size it in an eager step first
+      while ((int)wf_streams.size() < ns - 1) {
+        cudaStream_t q;
+        if (cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) != cudaSuccess)
+          return fail(RGB_ERR_CUDA, "wavefront stream");
+        wf_streams.push_back(q);
+      }
+      while (wf_events.size() < need_ev) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+          return fail(RGB_ERR_CUDA, "wavefront event");
+        wf_events.push_back(e);
+      }
+    }
+    *done = true;
+    auto ev = [&](int k, int b) { return wf_events[1 + (size_t)k * nb + b]; };
+    int rc = cuda_rc(cudaEventRecord(wf_events[0], st), "wavefront fork");
+    for (int k = 1; k < ns && !rc; ++k) rc = cuda_rc(cudaStreamWaitEvent(wf_streams[k - 1], wf_events[0], 0), "fork");
+    g_wavefront_active = true;
+    for (int b = 0; b < nb && !rc; ++b)
+      for (int k = 0; k < ns && !rc; ++k) {
+        cudaStream_t sk = k == 0 ? st : wf_streams[k - 1];
+        if (k > 0 && (rc = cuda_rc(cudaStreamWaitEvent(sk, ev(k - 1, b), 0), "wavefront wait"))) break;
+        Ctx cb = c;
+        cb.frames = std::min(B, c.frames - b * B);
+        cb.t_a = bwd ? c.t_a + c.frames - (int64_t)b * B - cb.frames : c.t_a + (int64_t)b * B;
+        const int64_t a0 = starts[stages[k].first], a1 = starts[stages[k].second + 1];
+        if ((rc = run(p + a0, a1 - a0, cb, sk))) break;
+        rc = cuda_rc(cudaEventRecord(ev(k, b), sk), "wavefront record");
+      }
+    g_wavefront_active = false;
+    for (int k = 1; k < ns && !rc; ++k) rc = cuda_rc(cudaStreamWaitEvent(st, ev(k, nb - 1), 0), "wavefront join");
+    if (!rc && nsteps < (int)kinds.size()) rc = run(p + starts[nsteps], n - starts[nsteps], c, st);
+    return rc;
+  }
+
   int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) {
     Reader rd{p, n};
     while (rd.i < n) {
@@ -818,7 +972,8 @@ struct rgb_plan {
           flops += 2.0 * G.rows * G.job[j].n * (double)ksum;
           bytes += 4.0 * ((double)G.rows * ksum + (double)G.job[j].n * ksum) + ew_bytes(G.job[j].epi, G.rows);
         }
-        const bool tc = use_tc(flops);
+        bool tc = use_tc(flops);
+        if (tc && g_wavefront_active && (!G.tma || tc_gemm_nt_scratch(G) > 0)) tc = false;
         if (tc && G.tma && (rc = splitk_scratch(G, st))) return rc;
         const int slot = prof_start(st);
         int nl = 1;
@@ -1037,6 +1192,11 @@ int rgb_abi_version(void) { return RGB_ABI_VERSION; }
 
 int rgb_set_scc_mode(int on) {
   g_scc_mode = on ? 1 : 0;
+  return RGB_OK;
+}
+
+int rgb_set_wavefront(int on) {
+  g_wavefront = on ? 1 : 0;
   return RGB_OK;
 }
 
@@ -1268,6 +1428,8 @@ int rgb_forward_chunk(rgb_plan* p, const float* w, const float* x, int x_on_host
   c.section = sequential ? 2 : 0;
   const auto& prog = p->prog[c.section];
   c.sec_base = prog.data();
+  bool wf = false;
+  if ((rc = p->run_wavefront(prog.data(), (int64_t)prog.size(), c, st, &wf)) || wf) return rc;
   return p->run(prog.data(), (int64_t)prog.size(), c, st);
 }
 
@@ -1307,6 +1469,8 @@ int rgb_forward_chunk_ids(rgb_plan* p, const float* w, const float* wt, const in
   c.section = sequential ? 2 : 0;
   const auto& prog = p->prog[c.section];
   c.sec_base = prog.data();
+  bool wf = false;
+  if ((rc = p->run_wavefront(prog.data(), (int64_t)prog.size(), c, st, &wf)) || wf) return rc;
   return p->run(prog.data(), (int64_t)prog.size(), c, st);
 }
 
@@ -1393,6 +1557,9 @@ int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_pri
   c.section = sequential ? 3 : 1;
   const auto& prog = p->prog[c.section];
   c.sec_base = prog.data();
+  bool wf = false;
+  int rc = p->run_wavefront(prog.data(), (int64_t)prog.size(), c, as_stream(stream), &wf);
+  if (rc || wf) return rc;
   return p->run(prog.data(), (int64_t)prog.size(), c, as_stream(stream));
 }
 

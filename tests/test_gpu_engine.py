@@ -276,6 +276,27 @@ def test_graph_replay_equals_eager(net_fn, S):
     assert len(tb._graphs) == tb._cap // 4
 
 
+def test_graph_replay_with_wavefront():
+    """The cross-layer wavefront (extra streams forked and joined inside the
+    capture) replays from CUDA graphs bit for bit like the eager steps."""
+    net = P.build_stacked_lstm(24, [48, 48], 16)
+    cfg = P.TrainConfig(h=96, h_prime=64, lr=0.02, iterations=1)
+    wa, wb = P.Weights.init(net, 5), P.Weights.init(net, 5)
+    ta, tb = P.Trainer(net, wa, 1, cfg), P.Trainer(net, wb, 1, cfg)
+    tb.enable_graphs()
+    gx, gt = tb.graph_inputs()
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        x = torch.tensor(rng.uniform(-1, 1, size=(64, 24)), dtype=torch.float32, device="cuda")
+        t = torch.tensor(rng.integers(0, 16, size=64), device="cuda")
+        ta.step(x, t)
+        gx.copy_(x)
+        gt.copy_(t)
+        tb.step_graphed()
+        assert abs(ta.loss() - tb.loss()) == 0.0
+    assert torch.equal(wa.flat, wb.flat)
+
+
 def test_staged_inputs_and_async_loss_equal_eager():
     """Host inputs staged on the copy stream one iteration ahead and losses read
     back one iteration late (the e2e loop of bench.py) give the eager results."""

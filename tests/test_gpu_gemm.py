@@ -129,6 +129,21 @@ def test_persistent_scc_layouts(n_hidden, S):
     assert n.value > 0, "persistent SCC kernel did not run"
 
 
+@pytest.mark.parametrize("wavefront", [1, 0])
+def test_wavefront_matches_oracle(wavefront):
+    """Cross-layer wavefront (default on): the stages between
+    persistent SCC loops of the forward and backward sections run on their
+    own streams over frame blocks; both schedules match the oracle."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_wavefront(wavefront))
+    try:
+        assert run_pair(P.build_stacked_lstm(24, [64, 64, 48], 20), 1, 96, 64, 3, 1e-2, 13) < 1e-4
+        assert run_pair(P.build_stacked_lstm(16, [32, 32], 16), 3, 64, 48, 3, 1e-2, 14) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_wavefront(1))
+
+
 def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
