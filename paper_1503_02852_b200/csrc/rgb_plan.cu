@@ -804,10 +804,14 @@ struct rgb_plan {
     if (!g_wavefront || !g_scc_mode || id_mode || g_gemm_mode == 2 || (c.section != 0 && !bwd) ||
         !prog_dev[c.section] || wf_ok[c.section] == 0)
       return RGB_OK;
-    // blocks of >= 16 frames, >= 4 of them (fewer blocks overlap too little to pay)
-    const int B = std::max(16, (c.frames + 7) / 8);
-    const int nb = (c.frames + B - 1) / B;
-    if (nb < 4) return RGB_OK;
+    // Loops on the persistent kernel: blocks of >= 16 frames, >= 4 of them
+    // (cfg2; fewer overlap too little to pay for the extra launches).  Loops
+    // of per-frame launches: only while one frame's GEMM leaves most of the
+    // GPU idle (S <= 128), blocks of >= 8 frames, >= 2 of them (cfg4 layers at
+    // S = 64 / 128 per GPU: 1.33x / 1.22x measured; at S >= 256 a frame
+    // already fills the GPU and the split hoisted GEMMs lose).
+    constexpr int kWfMaxRows = 128;
+    const bool frame_loops_ok = S <= kWfMaxRows;
     wf_ok[c.section] = 0;  // until the structure checks below pass
     std::vector<int64_t> starts;
     std::vector<int> kinds;
@@ -824,6 +828,7 @@ struct rgb_plan {
     while (nsteps > 0 && kinds[nsteps - 1] == STEP_DW) --nsteps;
     std::vector<std::pair<int, int>> stages;
     int first = 0, nloops = 0;
+    bool any_frame_loop = false;
     for (int s = 0; s < nsteps; ++s) {
       if (kinds[s] == STEP_DW) return RGB_OK;
       if (kinds[s] != STEP_LOOP) continue;
@@ -832,7 +837,10 @@ struct rgb_plan {
       const std::pair<int, int64_t> key{c.section, (int64_t)(body - c.sec_base)};
       auto found = scc_plans.find(key);
       if (found == scc_plans.end()) found = scc_plans.emplace(key, plan_scc(body, len)).first;
-      if (!found->second.ok) return RGB_OK;
+      if (!found->second.ok) {
+        if (!frame_loops_ok) return RGB_OK;
+        any_frame_loop = true;
+      }
       stages.push_back({first, s});
       first = s + 1;
       ++nloops;
@@ -840,6 +848,9 @@ struct rgb_plan {
     if (first < nsteps) stages.push_back({first, nsteps - 1});
     if (nloops < 2) return RGB_OK;
     wf_ok[c.section] = 1;
+    const int B = any_frame_loop ? std::max(8, (c.frames + 7) / 8) : std::max(16, (c.frames + 7) / 8);
+    const int nb = (c.frames + B - 1) / B;
+    if (nb < (any_frame_loop ? 2 : 4)) return RGB_OK;
     const int ns = (int)stages.size();
     const size_t need_ev = (size_t)ns * nb + 1;
     if ((int)wf_streams.size() < ns - 1 || wf_events.size() < need_ev) {

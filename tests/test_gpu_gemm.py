@@ -144,6 +144,18 @@ def test_wavefront_matches_oracle(wavefront):
         _lib.check(L.rgb_set_wavefront(1))
 
 
+def test_wavefront_with_per_frame_tensor_core_loops():
+    """The wavefront over loops of per-frame launches (no persistent kernel,
+    S <= 128): tcgen05 per-frame GEMMs of two layers run on two streams."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_scc_mode(0))
+    try:
+        assert run_pair(P.build_stacked_lstm(64, [512, 512], 32), 64, 32, 16, 2, 1e-3, 21) < 1e-4
+    finally:
+        _lib.check(L.rgb_set_scc_mode(1))
+
+
 def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
