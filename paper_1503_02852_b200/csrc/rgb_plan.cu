@@ -810,7 +810,10 @@ struct rgb_plan {
     // GPU idle (S <= 128), blocks of >= 8 frames, >= 2 of them (cfg4 layers at
     // S = 64 / 128 per GPU: 1.33x / 1.22x measured; at S >= 256 a frame
     // already fills the GPU and the split hoisted GEMMs lose).
-    constexpr int kWfMaxRows = 128;
+    static const int kWfMaxRows = [] {
+      const char* e = getenv("RGB_WF_MAXROWS");
+      return e ? atoi(e) : 128;
+    }();
     const bool frame_loops_ok = S <= kWfMaxRows;
     wf_ok[c.section] = 0;  // until the structure checks below pass
     std::vector<int64_t> starts;
