@@ -851,7 +851,11 @@ struct rgb_plan {
     if (first < nsteps) stages.push_back({first, nsteps - 1});
     if (nloops < 2) return RGB_OK;
     wf_ok[c.section] = 1;
-    const int B = any_frame_loop ? std::max(8, (c.frames + 7) / 8) : std::max(16, (c.frames + 7) / 8);
+    static const int nblk = [] {  // target block count (experiments: RGB_WF_NBLK)
+      const char* e = getenv("RGB_WF_NBLK");
+      return e ? std::max(2, atoi(e)) : 8;
+    }();
+    const int B = std::max(any_frame_loop ? 8 : 16, (c.frames + nblk - 1) / nblk);
     const int nb = (c.frames + B - 1) / B;
     if (nb < (any_frame_loop ? 2 : 4)) return RGB_OK;
     const int ns = (int)stages.size();
