@@ -156,6 +156,17 @@ def test_wavefront_with_per_frame_tensor_core_loops():
         _lib.check(L.rgb_set_scc_mode(1))
 
 
+@pytest.mark.parametrize("S,widths,h,hp", [(1, [40, 56, 24], 96, 64), (5, [64, 64], 80, 64), (40, [96, 96], 64, 32)])
+def test_stacked_default_schedule_sweep(S, widths, h, hp):
+    """Default engine (persistent SCC row blocks, forwarded chain values,
+    template images, cross-layer wavefront) on stacked LSTMs of odd widths,
+    several stream counts and window shapes, against the oracle."""
+    from test_gpu_engine import run_pair
+    # lr / S: gradients are raw sums over streams and frames (README.md:84-89),
+    # a fixed lr diverges at 40 streams within three iterations
+    assert run_pair(P.build_stacked_lstm(12, widths, 10), S, h, hp, 3, 1e-2 / S, 31 + S) < 1e-4
+
+
 def test_engine_parity_large_auto():
     """cfg3-like shapes, where auto mode routes the big GEMMs to tcgen05."""
     from test_gpu_engine import run_pair
