@@ -155,6 +155,13 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
 /* Tensor-core kernel variants for A/B tests (1 on, 0 off, -1 unchanged): CTA
  * pairs (cta_group::2), persistent multi-wave kernels, cluster split-K. */
 int rgb_set_tc_config(int pair, int persist, int csplit);
+/* Tensor-core GEMM precision (the north_star's separately bounded TF32 mode;
+ * the reference is float64 throughout, kernels.py:84-103): 3 (default) =
+ * 3xTF32, fp32-exact (hi*hi + hi*lo + lo*hi per k-step); 1 = plain TF32
+ * (hi*hi only, ~1e-3 relative per product; bound in tests/test_gpu_engine.py).
+ * Affects only the tcgen05 GEMMs; SIMT and SCC kernels stay fp32.  Read at
+ * launch time, so CUDA graphs captured before a change keep the old mode. */
+int rgb_set_tc_precision(int terms);
 
 /* Instrumentation (no reference counterpart; the reference times whole
  * iterations with perf_counter, engine.py:733-758).  rgb_launch_count: kernel

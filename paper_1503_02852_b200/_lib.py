@@ -52,6 +52,7 @@ _SIGS = {
     "rgb_onehot_rows": ([_P, _I, _I, _P, _P], _I),
     "rgb_tape_gather": ([_P, _P, _P, _P, _I, _I, _P], _I),
     "rgb_set_gemm_mode": ([_I], _I),
+    "rgb_set_tc_precision": ([_I], _I),
     "rgb_set_scc_mode": ([_I], _I),
     "rgb_set_wavefront": ([_I], _I),
     "rgb_gemm_nt": ([_P, _P, _P, _I, _I, _I, _I, _P], _I),

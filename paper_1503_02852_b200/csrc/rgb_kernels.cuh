@@ -52,6 +52,9 @@ long long tc_gemm_nt_scratch(const GemmGroup& p);
 // tensor-core kernel variants (1 on, 0 off, -1 unchanged): CTA pairs,
 // persistent multi-wave kernels, cluster (DSMEM) split-K
 void set_tc_config(int pair, int persist, int csplit);
+// tensor-core products per k-step: 3 (3xTF32, fp32-exact) or 1 (plain TF32)
+void set_tc_terms(int terms);
+int get_tc_terms();
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s);
 void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.

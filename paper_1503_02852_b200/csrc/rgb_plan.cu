@@ -1300,6 +1300,12 @@ int rgb_gemm_nt_tma(const float* a, const float* b, const float* b_lo, float* c,
   return e == cudaSuccess ? RGB_OK : fail(RGB_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
 }
 
+int rgb_set_tc_precision(int terms) {
+  if (terms != 1 && terms != 3) return fail(RGB_ERR_KERNEL, "tensor-core precision must be 3 (3xTF32) or 1 (TF32)");
+  set_tc_terms(terms);
+  return RGB_OK;
+}
+
 int rgb_set_tc_config(int pair, int persist, int csplit) {
   set_tc_config(pair, persist, csplit);
   return RGB_OK;

@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ---------------- MMA issuer (warp 8) ----------------
     const int n_inst = (N - n0) >= BN ? BN : (((N - n0) + 15) / 16) * 16;
     const uint32_t idesc = idesc_tf32(BM, n_inst, 0, 0);  // both operands K-major in smem
+    const bool split = p.terms != 1;
     for (int it = 0; it < nstages; ++it) {
       const int s = it % C::STAGES;
       mbar_wait(&full[s], (it / C::STAGES) & 1);
@@ -515,9 +516,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const uint64_t dah = smem_desc(a_hi + off, 16, 1024), dal = smem_desc(a_lo + off, 16, 1024);
         const uint64_t dbh = smem_desc(b_hi + off, 16, 1024), dbl = smem_desc(b_lo + off, 16, 1024);
         const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
-        mma_tf32(tmem, dal, dbh, idesc, acc0);  // small terms first
-        mma_tf32(tmem, dah, dbl, idesc, 1u);
-        mma_tf32(tmem, dah, dbh, idesc, 1u);
+        if (split) {
+          mma_tf32(tmem, dal, dbh, idesc, acc0);  // small terms first
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+        }
+        mma_tf32(tmem, dah, dbh, idesc, split ? 1u : acc0);
       }
       mma_commit(&empty[s]);
     }
@@ -826,6 +829,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       // epilogue skips those columns) so that each CTA's half is BN/2 rows
       const int n_inst = (PAIR || (N - n0) >= BN) ? BN : (((N - n0) + 15) / 16) * 16;
       const uint32_t idesc = idesc_tf32(BM * NCTA, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+      const bool split = p.terms != 1;  // 3xTF32 lo terms (plain TF32 issues only hi*hi)
       for (int it = 0; it < nstages; ++it) {
         const int s = it % C::STAGES;
         if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (it / C::STAGES) & 1);
@@ -861,27 +865,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
           const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
           if constexpr (TA) {
             // A hi/lo from tensor memory: 8 columns per k-step
+            const uint32_t acch = split ? 1u : acc0;
             if constexpr (PAIR) {
-              mma_tf32_ta_pair(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
-              mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
-              mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbh, idesc, 1u);
+              if (split) {
+                mma_tf32_ta_pair(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
+                mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
+              }
+              mma_tf32_ta_pair(tmem, ta_hi + 8 * j, dbh, idesc, acch);
             } else {
-              mma_tf32_ta(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
-              mma_tf32_ta(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
-              mma_tf32_ta(tmem, ta_hi + 8 * j, dbh, idesc, 1u);
+              if (split) {
+                mma_tf32_ta(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
+                mma_tf32_ta(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
+              }
+              mma_tf32_ta(tmem, ta_hi + 8 * j, dbh, idesc, acch);
             }
           } else if constexpr (PAIR) {
-            mma_tf32_pair(tmem, dal, dbh, idesc, acc0);
-            mma_tf32_pair(tmem, dah, dbl, idesc, 1u);
-            mma_tf32_pair(tmem, dah, dbh, idesc, 1u);
+            if (split) {
+              mma_tf32_pair(tmem, dal, dbh, idesc, acc0);
+              mma_tf32_pair(tmem, dah, dbl, idesc, 1u);
+            }
+            mma_tf32_pair(tmem, dah, dbh, idesc, split ? 1u : acc0);
           } else {
-#ifndef RGB_EXP_ONEMMA
-            mma_tf32(tmem, dal, dbh, idesc, acc0);
-            mma_tf32(tmem, dah, dbl, idesc, 1u);
-            mma_tf32(tmem, dah, dbh, idesc, 1u);
-#else
-            mma_tf32(tmem, dah, dbh, idesc, acc0);
-#endif
+            if (split) {
+              mma_tf32(tmem, dal, dbh, idesc, acc0);
+              mma_tf32(tmem, dah, dbl, idesc, 1u);
+            }
+            mma_tf32(tmem, dah, dbh, idesc, split ? 1u : acc0);
           }
         }
         if constexpr (PAIR) mma_commit_pair(&empty[s], leader);
@@ -915,10 +924,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
         const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + 64 * s + 16 * kh;
         tmem_st16(ta, hi);
-        tmem_st16(ta + 32, lo);
+        if (p.terms != 1) tmem_st16(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      } else {
+      } else if (p.terms != 1) {
         const float4* a_hi = reinterpret_cast<const float4*>(base);
         float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
@@ -928,7 +937,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
           a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
       }
-      {  // B residual (weights for the NT form, activations for dW)
+      if (p.terms != 1) {  // B residual (weights for the NT form, activations for dW)
         const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
         float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
         for (int q = threadIdx.x; q < C::B_BYTES / 16; q += kProducers) {
@@ -1181,6 +1190,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     if (lane == 0 && rank == 0) {
       // ---------------- MMA issuer ----------------
       const uint32_t idesc = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+      const bool split = p.terms != 1;
       int g = 0, ti = 0;
       for (int t = first; t < ntiles; t += stride, ++ti) {
         const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
@@ -1215,13 +1225,17 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
             }
             const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
             if constexpr (PAIR) {
-              mma_tf32_pair(acc, dal, dbh, idesc, acc0);
-              mma_tf32_pair(acc, dah, dbl, idesc, 1u);
-              mma_tf32_pair(acc, dah, dbh, idesc, 1u);
+              if (split) {
+                mma_tf32_pair(acc, dal, dbh, idesc, acc0);
+                mma_tf32_pair(acc, dah, dbl, idesc, 1u);
+              }
+              mma_tf32_pair(acc, dah, dbh, idesc, split ? 1u : acc0);
             } else {
-              mma_tf32(acc, dal, dbh, idesc, acc0);
-              mma_tf32(acc, dah, dbl, idesc, 1u);
-              mma_tf32(acc, dah, dbh, idesc, 1u);
+              if (split) {
+                mma_tf32(acc, dal, dbh, idesc, acc0);
+                mma_tf32(acc, dah, dbl, idesc, 1u);
+              }
+              mma_tf32(acc, dah, dbh, idesc, split ? 1u : acc0);
             }
           }
           if constexpr (PAIR) mma_commit_pair(&empty[s]);
@@ -1240,6 +1254,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         const int s = g % C::STAGES;
         mbar_wait(&tma_full[s], (g / C::STAGES) & 1);
         uint8_t* base = smem + s * C::STAGE_BYTES;
+        if (p.terms != 1) {
         const float4* a_hi = reinterpret_cast<const float4*>(base);
         float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
@@ -1255,6 +1270,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           const int q = threadIdx.x + i * kPersConv;
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+        }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if constexpr (PAIR) {
@@ -1532,6 +1548,7 @@ int pick_bn(F tiles_for) {
 
 namespace {
 
+int g_tc_terms = 3;  // 3: 3xTF32 (fp32-exact, default); 1: plain TF32 (rgb_set_tc_precision)
 int g_tc_opt[3] = {-1, -1, -1};  // pair, persistent, cluster split-K (-1: from the environment)
 
 bool pair_enabled() {  // RGB_TC_PAIR=0 disables the CTA-pair kernels (tuning experiments); rgb_set_tc_config overrides
@@ -1681,6 +1698,7 @@ long long tc_gemm_nt_scratch(const GemmGroup& p) {
 }
 
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
+  p.terms = g_tc_terms;
   NtConfig c = nt_config(p);
   p.csplit = c.splits > 1 && csplit_enabled() ? 1 : 0;
   if (c.pair && c.splits > 1 && !p.csplit) c.splits = 1;  // pairs split only through the cluster
@@ -1726,6 +1744,7 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
 }
 
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
+  p.terms = g_tc_terms;
   const bool pair = p.tma && pair_enabled() && !getenv("RGB_TC_BN");
   const int bm = tc::BM * (pair ? 2 : 1);
   auto tiles_for = [&](int bn) {
@@ -1772,6 +1791,8 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
 }  // namespace rgb
 
 namespace rgb {
+void set_tc_terms(int terms) { g_tc_terms = terms; }
+int get_tc_terms() { return g_tc_terms; }
 void set_tc_config(int pair, int persist, int csplit) {
   if (pair >= 0) g_tc_opt[0] = pair != 0;
   if (persist >= 0) g_tc_opt[1] = persist != 0;

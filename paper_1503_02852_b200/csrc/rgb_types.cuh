@@ -96,6 +96,7 @@ struct GemmGroup {
   int splits;          // set by launch_tc_gemm_nt
   int pair;            // 1: CTA-pair (cta_group::2) tiles of 256 rows
   int csplit;          // 1: the splits of a tile form a cluster and reduce through DSMEM
+  int terms;           // tcgen05 products per k-step: 3 = 3xTF32 (fp32-exact), 1 = plain TF32
 };
 
 struct EwLaunch {
@@ -119,6 +120,7 @@ struct DwGroup {
   int njobs, k;
   float alpha;
   int tma;             // 1: every job has TMA maps
+  int terms;           // 3 = 3xTF32 (fp32-exact), 1 = plain TF32
   int tile_start[kMaxDw + 1];
   int tiles_n[kMaxDw];
   DwJob job[kMaxDw];

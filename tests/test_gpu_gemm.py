@@ -313,3 +313,69 @@ def test_id_inputs_with_tensor_cores_forced():
         assert run_pair(P.build_lstm(300, 32, 16), 3, 8, 4, 3, 0.05, 21, ids=True) < 1e-4
     finally:
         _lib.check(L.rgb_set_gemm_mode(0))
+
+
+# ---- plain-TF32 tensor-core mode (rgb_set_tc_precision(1)) ------------------
+# The north_star allows a TF32 GEMM mode "to a separately stated bound".  One
+# tcgen05 kind::tf32 product per k-step truncates both fp32 operands to a
+# 10-bit mantissa (relative step 2^-10); for U(-1,1) operands the normwise GEMM
+# error is ~4e-4.  Stated bounds: GEMM 2e-3, full training step (outputs,
+# weight gradients, weights after SGD) 2e-2 normwise, loss 1e-2 relative.
+TF32_GEMM_BOUND = 2e-3
+TF32_STEP_BOUND = 2e-2
+
+
+@pytest.fixture
+def _tf32():
+    L = _lib.lib()
+    _lib.check(L.rgb_set_tc_precision(1))
+    try:
+        yield L
+    finally:
+        _lib.check(L.rgb_set_tc_precision(3))
+
+
+def test_tc_precision_rejects_bad_values():
+    L = _lib.lib()
+    assert L.rgb_set_tc_precision(2) == _lib.RGB_ERR_KERNEL
+    assert L.rgb_set_tc_precision(0) == _lib.RGB_ERR_KERNEL
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 512, 1024), (1024, 2048, 1024), (200, 300, 70)])
+def test_gemm_tf32_mode(_tf32, m, n, k):
+    """Both tcgen05 forms (NT and dW, incl. the TMA-fed dW) in plain TF32:
+    inside the stated bound, and measurably less exact than 3xTF32 (the mode
+    switch is real)."""
+    rng = np.random.default_rng(m + 5 * n + k)
+    a, b = rng.uniform(-1, 1, size=(m, k)), rng.uniform(-1, 1, size=(n, k))
+    ta = torch.tensor(a, dtype=torch.float32, device="cuda")
+    tb = torch.tensor(b, dtype=torch.float32, device="cuda")
+    tc = torch.full((m, n), float("nan"), device="cuda")
+    _lib.check(_tf32.rgb_gemm_nt(ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()),
+                                 ctypes.c_void_p(tc.data_ptr()), m, n, k, 2, _stream()))
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    err = normwise(tc.cpu().numpy(), ref)
+    assert 1e-5 < err < TF32_GEMM_BOUND, err
+    e, y = rng.uniform(-1, 1, size=(k, m)), rng.uniform(-1, 1, size=(k, n))
+    te = torch.tensor(e, dtype=torch.float32, device="cuda")
+    ty = torch.tensor(y, dtype=torch.float32, device="cuda")
+    ref = -(e.astype(np.float32).astype(np.float64).T @ y.astype(np.float32).astype(np.float64))
+    for mode in ([2, 3] if m % 32 == 0 and n % 32 == 0 else [2]):
+        tg = torch.full((m, n), float("nan"), device="cuda")
+        _lib.check(_tf32.rgb_gemm_dw(ctypes.c_void_p(te.data_ptr()), ctypes.c_void_p(ty.data_ptr()),
+                                     ctypes.c_void_p(tg.data_ptr()), m, n, k, ctypes.c_float(-1.0), mode, _stream()))
+        err = normwise(tg.cpu().numpy(), ref)
+        assert 1e-5 < err < TF32_GEMM_BOUND, (mode, err)
+
+
+def test_engine_parity_tf32_mode(_tf32):
+    """Whole training steps with every GEMM on tcgen05 in plain TF32 against
+    the float64 oracle, at the TF32 bound."""
+    from test_gpu_engine import run_pair
+    _lib.check(_tf32.rgb_set_gemm_mode(2))
+    try:
+        assert run_pair(P.build_lstm(39, 128, 39), 2, 32, 16, 3, 1e-3, 0, loss_tol=1e-2) < TF32_STEP_BOUND
+        assert run_pair(P.build_stacked_lstm(256, [256, 256], 256), 64, 8, 4, 2, 1e-3, 4,
+                        loss_tol=1e-2) < TF32_STEP_BOUND
+    finally:
+        _lib.check(_tf32.rgb_set_gemm_mode(0))

@@ -1,6 +1,7 @@
 """Time the tcgen05 TMA GEMM on raw shapes (tuning aid).
 
     python tools/gemm_bench.py 512x2048x1024 512x1024x2048 8192x4096x1024
+    python tools/gemm_bench.py --tf32 dw:4096x1024x16384   # plain-TF32 mode, dW form
 """
 from __future__ import annotations
 
@@ -28,9 +29,33 @@ def main():
         _lib.LIB_PATH = args.pop(0).split("=", 1)[1]
         print("library:", _lib.LIB_PATH)
     L = _lib.lib()
+    if args and args[0] == "--tf32":
+        args.pop(0)
+        _lib.check(L.rgb_set_tc_precision(1))
+        print("tensor-core precision: plain TF32")
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     for shape in args:
+        if shape.startswith("dw:"):  # G[m,n] = -E^T Y over k rows (the TMA-fed dW form)
+            m, n, k = (int(v) for v in shape[3:].split("x"))
+            e = torch.rand(k, m, device="cuda") * 2 - 1
+            y = torch.rand(k, n, device="cuda") * 2 - 1
+            g = torch.empty(m, n, device="cuda")
+            run = lambda: L.rgb_gemm_dw(P(e), P(y), P(g), m, n, k, ctypes.c_float(-1.0), 3, st)  # noqa: E731
+            for _ in range(3):
+                _lib.check(run())
+            torch.cuda.synchronize()
+            ref = -(e.double().T @ y.double())
+            err = ((g.double() - ref).abs().max() / ref.abs().max()).item()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                run()
+            e1.record()
+            torch.cuda.synchronize()
+            us = 1000 * e0.elapsed_time(e1) / 20
+            print(f"{shape}: {us:8.1f} us  {2 * m * n * k / us / 1e6:7.1f} TFLOP/s  err {err:.1e}")
+            continue
         m, n, k = (int(v) for v in shape.split("x"))
         a = torch.rand(m, k, device="cuda") * 2 - 1
         b = torch.rand(n, k, device="cuda") * 2 - 1
