@@ -1560,6 +1560,12 @@ bool pair_enabled() {  // RGB_TC_PAIR=0 disables the CTA-pair kernels (tuning ex
   return on == 1;
 }
 
+// Full-machine pair tiles pay in 3xTF32 only (they halve the B residual
+// conversion per CTA).  Plain TF32 has no conversion and the pair's cross-CTA
+// handshake becomes the bound: single CTAs measured 1.5-1.7x faster on the
+// hoisted / dW shapes (profiles/r01_tf32_mode.md).
+bool wide_pair_enabled() { return pair_enabled() && g_tc_terms == 3; }
+
 // output tiles of a launch: 128-row tiles, or 256-row pair tiles
 int nt_tiles(const GemmGroup& p, int bn, bool pair) {
   const int bm = tc::BM * (pair ? 2 : 1);
@@ -1616,7 +1622,7 @@ NtConfig nt_config(const GemmGroup& p) {
     }
     for (int bn : {256, 128}) {
       if (pair_bn && bn != pair_bn) continue;
-      if (2 * nt_tiles(p, bn, true) >= 120) {
+      if (wide_pair_enabled() && 2 * nt_tiles(p, bn, true) >= 120) {
         c.bn = bn;
         c.pair = true;
         return c;
@@ -1745,7 +1751,7 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
 
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   p.terms = g_tc_terms;
-  const bool pair = p.tma && pair_enabled() && !getenv("RGB_TC_BN");
+  const bool pair = p.tma && wide_pair_enabled() && !getenv("RGB_TC_BN");
   const int bm = tc::BM * (pair ? 2 : 1);
   auto tiles_for = [&](int bn) {
     int t = 0;
