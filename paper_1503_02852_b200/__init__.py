@@ -14,7 +14,8 @@ from .builders import build_custom_graph, build_elman, build_lstm, build_stacked
 from .schedule import EngineError, build_program
 from .engine import (Batch, BpttWindow, CheckpointError, Criterion, GradStore, IterationMetrics, StreamState,
                      TrainConfig, Trainer, Weights, backward_window, forward_chunk, inject_output_error,
-                     load_checkpoint, loss_value, save_checkpoint, sgd_update, structure_hash, train_loop)
+                     load_checkpoint, loss_value, save_checkpoint, set_tc_precision, sgd_update, structure_hash,
+                     train_loop)
 
 from .tapes import DeviceStreamSet, TapePlanner
 

@@ -527,6 +527,20 @@ def sgd_update(weights: Weights, grads: GradStore, lr: float) -> None:
 # move between the two implementations)
 
 
+_TC_TERMS = {"3xtf32": 3, "tf32": 1}
+
+
+def set_tc_precision(mode: str) -> None:
+    """Tensor-core GEMM precision for subsequently launched (and captured)
+    steps: ``"3xtf32"`` (default, fp32-exact) or ``"tf32"`` (the separately
+    bounded mode: 2e-2 normwise per training step, tests/test_gpu_gemm.py).
+    No reference counterpart -- the reference computes in float64
+    (kernels.py:84-103).  CUDA graphs captured earlier keep their mode."""
+    if mode not in _TC_TERMS:
+        raise ValueError(f"tensor-core precision must be one of {sorted(_TC_TERMS)}, got {mode!r}")
+    _lib.check(_lib.lib().rgb_set_tc_precision(_TC_TERMS[mode]))
+
+
 class CheckpointError(EngineError):
     """Mirror of the reference ``CheckpointError`` (engine.py:90)."""
 

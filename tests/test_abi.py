@@ -60,3 +60,9 @@ def test_sass_is_sm100(lib):
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_set_tc_precision_validates_mode_without_gpu():
+    import paper_1503_02852_b200 as P
+    with pytest.raises(ValueError):
+        P.set_tc_precision("fp16")

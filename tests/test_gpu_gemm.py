@@ -339,6 +339,10 @@ def test_tc_precision_rejects_bad_values():
     L = _lib.lib()
     assert L.rgb_set_tc_precision(2) == _lib.RGB_ERR_KERNEL
     assert L.rgb_set_tc_precision(0) == _lib.RGB_ERR_KERNEL
+    with pytest.raises(ValueError):
+        P.set_tc_precision("bf16")
+    P.set_tc_precision("tf32")
+    P.set_tc_precision("3xtf32")
 
 
 @pytest.mark.parametrize("m,n,k", [(256, 512, 1024), (1024, 2048, 1024), (200, 300, 70)])
