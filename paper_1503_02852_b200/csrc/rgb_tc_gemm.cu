@@ -1113,10 +1113,18 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   constexpr int kBoxIdx = box_idx<BNL>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // Plain TF32 (p.terms == 1, single CTAs) needs no residual halves: each
+  // physical [A][A_lo][B][B_lo] slot holds two logical [A][B] stages, so the
+  // pipeline is twice as deep (2 -> 4 stages at BN = 256).
+  const bool one = !PAIR && p.terms == 1;
+  const int NST = one ? 2 * C::STAGES : C::STAGES;
+  const int SB = one ? C::STAGE_BYTES / 2 : C::STAGE_BYTES;
+  const int BOFF = one ? C::A_BYTES : C::B_OFF;
+  static_assert(6 * C::STAGES * 8 + 40 <= 512, "barrier region");
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* conv_full = tma_full + C::STAGES;
-  uint64_t* empty = conv_full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;   // [2]
+  uint64_t* conv_full = tma_full + 2 * C::STAGES;
+  uint64_t* empty = conv_full + 2 * C::STAGES;
+  uint64_t* tmem_full = empty + 2 * C::STAGES;   // [2]
   uint64_t* tmem_empty = tmem_full + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 512);
@@ -1127,7 +1135,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   const int first = blockIdx.x / NCTA, stride = gridDim.x / NCTA;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&tma_full[s], 2);
       mbar_init(&conv_full[s], PAIR ? 2 : kPersConv);
       mbar_init(&empty[s], 1);
@@ -1165,18 +1173,18 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         const auto& job = p.job[T.jid];
         int seg = 0, k0 = 0;
         for (int it = 0; it < T.nstages; ++it, ++g) {
-          const int s = g % C::STAGES;
-          mbar_wait(&empty[s], ((g / C::STAGES) & 1) ^ 1);
-          uint8_t* base = smem + s * C::STAGE_BYTES;
+          const int s = g % NST;
+          mbar_wait(&empty[s], ((g / NST) & 1) ^ 1);
+          uint8_t* base = smem + s * SB;
           mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
           if constexpr (IS_DW) {
             if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, T.m0 / 32, &tma_full[s]);
-            else tma_load_3d(base + C::B_OFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, T.nb0 / 32, &tma_full[s]);
+            else tma_load_3d(base + BOFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, T.nb0 / 32, &tma_full[s]);
             k0 += BK;
           } else {
             const Seg& sg = job.seg[seg];
             if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + T.m0, &tma_full[s]);
-            else tma_load_2d(base + C::B_OFF, map_at(sg.tb, kBoxIdx), k0, T.nb0, &tma_full[s]);
+            else tma_load_2d(base + BOFF, map_at(sg.tb, kBoxIdx), k0, T.nb0, &tma_full[s]);
             k0 += BK;
             if (k0 >= sg.k) {
               k0 = 0;
@@ -1200,13 +1208,13 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + b * BN;
         for (int it = 0; it < T.nstages; ++it, ++g) {
-          const int s = g % C::STAGES;
-          if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (g / C::STAGES) & 1);
-          else mbar_wait(&conv_full[s], (g / C::STAGES) & 1);
+          const int s = g % NST;
+          if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (g / NST) & 1);
+          else mbar_wait(&conv_full[s], (g / NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t base = smem_u32(smem + s * SB);
           const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
-          const uint32_t b_hi = base + C::B_OFF, b_lo = b_hi + C::B_BYTES;
+          const uint32_t b_hi = base + BOFF, b_lo = b_hi + C::B_BYTES;
 #pragma unroll
           for (int j = 0; j < BK / 8; ++j) {
             uint64_t dah, dal, dbh, dbl;
@@ -1251,9 +1259,9 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     for (int t = first; t < ntiles; t += stride) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
       for (int it = 0; it < T.nstages; ++it, ++g) {
-        const int s = g % C::STAGES;
-        mbar_wait(&tma_full[s], (g / C::STAGES) & 1);
-        uint8_t* base = smem + s * C::STAGE_BYTES;
+        const int s = g % NST;
+        mbar_wait(&tma_full[s], (g / NST) & 1);
+        uint8_t* base = smem + s * SB;
         if (p.terms != 1) {
         const float4* a_hi = reinterpret_cast<const float4*>(base);
         float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
@@ -1263,8 +1271,8 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           const float4 x = a_hi[q];
           a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
-        const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
-        float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
+        const float4* b_hi = reinterpret_cast<const float4*>(base + BOFF);
+        float4* b_lo = reinterpret_cast<float4*>(base + BOFF + C::B_BYTES);
 #pragma unroll
         for (int i = 0; i < C::B_BYTES / 16 / kPersConv; ++i) {
           const int q = threadIdx.x + i * kPersConv;
