@@ -695,10 +695,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   // Both CTAs of a pair get the same layout (the leader's MMA descriptors
   // address the peer's operands at the same offsets).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // Plain TF32 (p.terms == 1, single CTAs): no residual halves, so the same
+  // shared memory holds more logical stages of [A][B] (TA: 32 instead of 64
+  // TMEM columns per A stage); the barrier arrays are sized for 8 stages.
+  constexpr int kMaxSt = 8;
+  static_assert(C::STAGES <= kMaxSt && 3 * kMaxSt * 8 + 12 <= 256, "barrier region");
+  const bool one = !PAIR && p.terms == 1;
+  const int SB = one ? C::A_BYTES + C::B_BYTES : C::STAGE_BYTES;
+  const int BOFF = one ? C::A_BYTES : C::B_OFF;
+  const int TST = one ? 32 : 64;  // TMEM columns per TA stage
+  int NST = C::STAGES;
+  if (one) {
+    NST = (C::STAGES * C::STAGE_BYTES) / SB;
+    if (TA && NST > (512 - BN) / 32) NST = (512 - BN) / 32;
+    if (NST > kMaxSt) NST = kMaxSt;
+  }
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* conv_full = tma_full + C::STAGES;
-  uint64_t* empty = conv_full + C::STAGES;
-  uint64_t* done = empty + C::STAGES;
+  uint64_t* conv_full = tma_full + kMaxSt;
+  uint64_t* empty = conv_full + kMaxSt;
+  uint64_t* done = empty + kMaxSt;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 256);
 
@@ -741,7 +756,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   nstages = (int)((long long)(split + 1) * nstages / splits) - s_begin;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&tma_full[s], 2);  // one expect_tx arrival per producer warp
       // pair: one arrival per converter warp of both CTAs (on the leader's copy)
       mbar_init(&conv_full[s], PAIR ? 2 : kProducers);
@@ -798,22 +813,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         }
       }
       for (int it = 0; it < nstages; ++it) {
-        const int s = it % C::STAGES;
-        mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+        const int s = it % NST;
+        mbar_wait(&empty[s], ((it / NST) & 1) ^ 1);
         if (load_a) { TRACE(0, it) }
-        uint8_t* base = smem + s * C::STAGE_BYTES;
+        uint8_t* base = smem + s * SB;
         mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
         if constexpr (IS_DW) {
           // MN-contiguous E [K x M] and Y [K x N]: one 3-D box of 4 (BNL/32)
           // 4-KB atoms {32 mn, 32 k} per operand (rgb_plan.cu encode_map_mn)
           if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, m0 / 32, &tma_full[s]);
-          else tma_load_3d(base + C::B_OFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, nb0 / 32, &tma_full[s]);
+          else tma_load_3d(base + BOFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, nb0 / 32, &tma_full[s]);
           k0 += BK;
         } else {
           const Seg& sg = job.seg[seg];
           if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + m0, &tma_full[s]);
           // weight maps come in 32/64/128/256-row box variants: one load per stage
-          else tma_load_2d(base + C::B_OFF, map_at(sg.tb, kBoxIdx), k0, nb0, &tma_full[s]);
+          else tma_load_2d(base + BOFF, map_at(sg.tb, kBoxIdx), k0, nb0, &tma_full[s]);
           k0 += BK;
           if (k0 >= sg.k) {
             k0 = 0;
@@ -831,15 +846,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       const uint32_t idesc = idesc_tf32(BM * NCTA, n_inst, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       const bool split = p.terms != 1;  // 3xTF32 lo terms (plain TF32 issues only hi*hi)
       for (int it = 0; it < nstages; ++it) {
-        const int s = it % C::STAGES;
-        if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (it / C::STAGES) & 1);
-        else mbar_wait(&conv_full[s], (it / C::STAGES) & 1);
+        const int s = it % NST;
+        if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (it / NST) & 1);
+        else mbar_wait(&conv_full[s], (it / NST) & 1);
         TRACE(2, it)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+        const uint32_t base = smem_u32(smem + s * SB);
         const uint32_t a_hi = base, a_lo = base + C::A_BYTES;
-        const uint32_t b_hi = base + C::B_OFF, b_lo = b_hi + C::B_BYTES;
-        const uint32_t ta_hi = tmem + BN + 64 * s, ta_lo = ta_hi + 32;  // TA: A stage in TMEM
+        const uint32_t b_hi = base + BOFF, b_lo = b_hi + C::B_BYTES;
+        const uint32_t ta_hi = tmem + BN + TST * s, ta_lo = ta_hi + 32;  // TA: A stage in TMEM
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           uint64_t dah, dal, dbh, dbl;
@@ -902,10 +917,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
   } else {
     // ---------------- converters: x_lo = x - trunc(x), same byte offsets ----------------
     for (int it = 0; it < nstages; ++it) {
-      const int s = it % C::STAGES;
-      mbar_wait(&tma_full[s], (it / C::STAGES) & 1);
+      const int s = it % NST;
+      mbar_wait(&tma_full[s], (it / NST) & 1);
       if (threadIdx.x == 0) { TRACE(1, it) }
-      uint8_t* base = smem + s * C::STAGE_BYTES;
+      uint8_t* base = smem + s * SB;
 #ifndef RGB_EXP_NOCONV
       if constexpr (TA) {
         // A row r = 32*(warp%4) + lane (the TMEM lane quarter this warp may
@@ -922,7 +937,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
-        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + 64 * s + 16 * kh;
+        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + TST * s + 16 * kh;
         tmem_st16(ta, hi);
         if (p.terms != 1) tmem_st16(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -938,8 +953,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
         }
       }
       if (p.terms != 1) {  // B residual (weights for the NT form, activations for dW)
-        const float4* b_hi = reinterpret_cast<const float4*>(base + C::B_OFF);
-        float4* b_lo = reinterpret_cast<float4*>(base + C::B_OFF + C::B_BYTES);
+        const float4* b_hi = reinterpret_cast<const float4*>(base + BOFF);
+        float4* b_lo = reinterpret_cast<float4*>(base + BOFF + C::B_BYTES);
         for (int q = threadIdx.x; q < C::B_BYTES / 16; q += kProducers) {
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
