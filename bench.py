@@ -12,9 +12,11 @@ frames/s = h' * S_total / seconds per step (engine.py:751-757, cli.py:335-346).
 CUDA events on the launching stream, max over ranks.  ``e2e`` is the same
 metric through the public API (Trainer.step = the C-ABI calls) with pinned
 HOST inputs/targets copied in and the loss read back every step.  The CPU
-baseline is the float64 oracle (oracle/engine_np.py, numpy BLAS, all host
-threads) on a bounded sample of the same workload -- the only place bench.py
-executes oracle/.
+baseline of record is the reference itself: rnngraph.train_loop (numba,
+float64, every host thread) installed in oracle/_ref by oracle/build_ref.sh,
+on a bounded stream sample of the same workload (oracle/ref_runner.py; the
+float64 numpy oracle port stands in only when oracle/_ref is absent) -- the
+only places bench.py executes oracle/.
 """
 
 from __future__ import annotations
@@ -154,8 +156,27 @@ def blas_threads() -> int:
 
 
 def cpu_sample_streams(cfg) -> int:
-    """Bounded sample: streams of the workload the oracle runs (~10-30 s)."""
-    return {"cfg4": 32, "cfg3": 64, "cfg2": 1}.get(cfg["name"], cfg["S"])
+    """Bounded sample: streams of the workload the CPU arms run.  Every stream
+    is an independent context and the CPU kernels' cost is
+    linear in S, so a stream subset measures the same per-frame rate."""
+    return {"cfg4": 16, "cfg3": 64, "cfg2": 1}.get(cfg["name"], cfg["S"])
+
+
+def reference_rate(cfg, n_streams, warm, iters):
+    """The reference's own train_loop (numba, float64, all host threads) from
+    oracle/_ref on ``n_streams`` streams of the workload: (frames/s, cpu_baseline
+    dict) or None when the reference is not installed on this box."""
+    from oracle import ref_runner as RR
+    if RR.load_reference() is None:
+        return None
+    net = build_net(cfg)
+    rate, n, secs, _ = RR.time_train_loop(net, n_streams, cfg["h"], cfg["hp"], cfg["lr"], warm, iters)
+    nb = RR.numba_info()
+    return rate, {"value": rate, "unit": "frames/s", "cores": nb["threads"], "kind": "reference",
+                  "sample": f"reference rnngraph.train_loop (oracle/_ref, numba {nb['numba']}, float64, "
+                            f"NUMBA_NUM_THREADS={nb['threads']}, {RR.cpu_model()}) on {n_streams} of {cfg['S']} "
+                            f"streams of {cfg['name']}, h={cfg['h']}, h'={cfg['hp']}: {n} iterations after {warm} "
+                            f"warm-up, {secs:.1f} s"}
 
 
 def run_reference(args, cfg):
@@ -165,34 +186,45 @@ def run_reference(args, cfg):
     n = cpu_sample_streams(cfg)
     if cfg["name"] == "cfg2":
         cfg = dict(cfg, hp=32, h=64)  # bounded: a 1/8 slice of the T=256 window
-    rates = []
-    from oracle import engine_np as O
-    import paper_1503_02852_b200 as P
-    net = build_net(cfg)
-    cg = P.condense(net)
-    W = O.init_weights(net, 0)
-    st = O.History(net, n, cfg["h"])
-    rng = np.random.default_rng(0)
-    for it in range(args.warmup + args.steps):
-        x = rng.uniform(-1, 1, size=(cfg["hp"] * n, cfg["n_in"]))
-        t = rng.integers(0, cfg["n_out"], size=cfg["hp"] * n)
-        t0 = time.perf_counter()
-        O.train_step(net, cg, W, st, x, t, cfg["h"], cfg["lr"])
-        if it >= args.warmup:
-            rates.append(cfg["hp"] * n / (time.perf_counter() - t0))
-    value = len(rates) / sum(1.0 / r for r in rates)
-    sample = f"{n} of {cfg['S']} streams of {cfg['name']}, h={cfg['h']}, h'={cfg['hp']}, float64 numpy"
+    got = reference_rate(cfg, n, max(args.warmup, math.ceil(cfg["h"] / cfg["hp"]) + 1), args.steps)
+    if got is not None:
+        value, cpu = got
+    else:  # the reference is not installed here: the oracle port (float64 numpy)
+        from oracle import engine_np as O
+        import paper_1503_02852_b200 as P
+        net = build_net(cfg)
+        cg = P.condense(net)
+        W = O.init_weights(net, 0)
+        st = O.History(net, n, cfg["h"])
+        rng = np.random.default_rng(0)
+        rates = []
+        for it in range(args.warmup + args.steps):
+            x = rng.uniform(-1, 1, size=(cfg["hp"] * n, cfg["n_in"]))
+            t = rng.integers(0, cfg["n_out"], size=cfg["hp"] * n)
+            t0 = time.perf_counter()
+            O.train_step(net, cg, W, st, x, t, cfg["h"], cfg["lr"])
+            if it >= args.warmup:
+                rates.append(cfg["hp"] * n / (time.perf_counter() - t0))
+        value = len(rates) / sum(1.0 / r for r in rates)
+        cpu = {"value": value, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
+               "sample": f"{n} of {cfg['S']} streams of {cfg['name']}, h={cfg['h']}, h'={cfg['hp']}, float64 numpy"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["hp"] * n / value,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": cfg["name"] + ": " + cfg["desc"]},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
+
+
+def paper_flops_per_frame(net) -> int:
+    """The paper's operation count (reference cli.py:49-55, count_flops): 6 *
+    rows * cols per dense connection per frame; identity edges and
+    elementwise work count zero."""
+    return 6 * sum(net.layer(c.dst).size * net.layer(c.src).size for c in net.iter_dense())
 
 
 # ---------------------------------------------------------------------------
@@ -464,6 +496,11 @@ def run_ours(args, cfg):
                    "launch": "CUDA-graph replay per ring phase" if graphs else "eager",
                    "gemm_precision": args.tc_precision},
         "algorithmic_tflops": F_iter / (ms / 1000.0) / 1e12,
+        # the two FLOP conventions: SURVEY §8(d)'s algorithmic unit (above) and
+        # the paper's 6*R*C per dense edge per frame (reference cli.py:49-55)
+        "paper_6rc": {"mflop_per_frame": paper_flops_per_frame(net) / 1e6,
+                      "gflops": paper_flops_per_frame(net) * value / 1e9,
+                      "e2e_gflops": paper_flops_per_frame(net) * e2e["value"] / 1e9},
         # the frame-sequential (recurrent) part of an iteration: device time of
         # the per-frame launches (or persistent SCC kernels) per frame step
         # (layers x frames of the forward chunk and the backward window)
@@ -479,10 +516,14 @@ def run_ours(args, cfg):
     }
     if world == 1 and not args.no_cpu:
         n = cpu_sample_streams(cfg)
-        rate, iters, secs = cpu_oracle_rate(cfg, n, min_seconds=args.cpu_seconds)
-        line["cpu_baseline"] = {"value": rate, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
-                                "sample": f"oracle (float64 numpy) on {n} of {cfg['S']} streams of {cfg['name']}, "
-                                          f"{iters} iterations after 2 warm-up, {secs:.1f} s"}
+        got = reference_rate(cfg, n, math.ceil(h / hp) + 1, 3)
+        if got is not None:
+            line["cpu_baseline"] = got[1]
+        else:
+            rate, iters, secs = cpu_oracle_rate(cfg, n, min_seconds=args.cpu_seconds)
+            line["cpu_baseline"] = {"value": rate, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
+                                    "sample": f"oracle (float64 numpy) on {n} of {cfg['S']} streams of "
+                                              f"{cfg['name']}, {iters} iterations after 2 warm-up, {secs:.1f} s"}
     if world == 1 and not args.no_intra:
         line["intra_stream"] = measure_intra_stream(P)
     if world == 1 and not args.no_tf32 and args.tc_precision != "tf32":

@@ -84,8 +84,13 @@ int rgb_forward_chunk_ids(rgb_plan* plan, const float* w, const float* wt, const
  * criterion: 0 cross-entropy/softmax, 1 mse/identity. */
 int rgb_inject_output_error(rgb_plan* plan, const void* target, int target_kind, int target_on_host,
                             int criterion, int frames, void* stream);
-/* Read the last loss (synchronises the stream). */
+/* Read the last loss (synchronises the stream).  Fails with RGB_ERR_ENGINE
+ * when an input id or a target class id of an earlier step was out of range
+ * (the kernels substitute a zero row / a NaN loss and raise a sticky flag;
+ * the reference raises EngineError / IndexError, engine.py:385-389, 443-456). */
 int rgb_read_loss(rgb_plan* plan, double* loss, void* stream);
+/* The same out-of-range check without reading the loss (synchronises). */
+int rgb_check_inputs(rgb_plan* plan, void* stream);
 /* Enqueue the copy of the last loss into `dst` (pinned host or device memory)
  * without synchronising; the caller waits on the stream / an event. */
 int rgb_read_loss_async(rgb_plan* plan, double* dst, void* stream);
@@ -125,6 +130,14 @@ int rgb_refresh_transpose(rgb_plan* plan, const float* w, float* wt, void* strea
 
 /* StreamState.reset_stream (engine.py:267-276). */
 int rgb_reset_stream(rgb_plan* plan, int stream_index, void* stream);
+
+/* Read-only view of one schedule buffer over frames [t_lo, t_hi] (frame-major
+ * rows of `width` floats, contiguous): activation rings (layer y, edge z) at
+ * the current cursor, or the error buffers of the LAST backward window -- the
+ * per-layer deltas and the per-edge eps of multiplicative destinations that
+ * the reference computes as locals of backward_window (engine.py:512-566).
+ * Buffer ids come from the program's buffer table (schedule.Layout). */
+int rgb_window_view(const rgb_plan* plan, int buffer, int64_t t_lo, int64_t t_hi, const float** ptr, int* width);
 
 /* Count non-finite values of one buffer over frames [t_lo, t_hi] (the
  * check_finite guard, engine.py:415-417); result copied to *count (sync). */

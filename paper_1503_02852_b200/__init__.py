@@ -15,7 +15,7 @@ from .schedule import EngineError, build_program
 from .engine import (Batch, BpttWindow, CheckpointError, Criterion, GradStore, IterationMetrics, StreamState,
                      TrainConfig, Trainer, Weights, backward_window, forward_chunk, inject_output_error,
                      load_checkpoint, loss_value, save_checkpoint, set_tc_precision, sgd_update, structure_hash,
-                     train_loop)
+                     train_loop, window_errors)
 
 from .tapes import DeviceStreamSet, TapePlanner
 

@@ -40,6 +40,7 @@ _SIGS = {
     "rgb_forward_chunk_ids": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),
     "rgb_inject_output_error": ([_P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_read_loss": ([_P, ctypes.POINTER(ctypes.c_double), _P], _I),
+    "rgb_check_inputs": ([_P, _P], _I),
     "rgb_read_loss_async": ([_P, _P, _P], _I),
     "rgb_set_injection": ([_P, _P, _I, _P], _I),
     "rgb_get_injection": ([_P, _P, _I, _P], _I),
@@ -47,6 +48,7 @@ _SIGS = {
     "rgb_sgd_update": ([_P, _P, _P, _P, ctypes.c_float, _P], _I),
     "rgb_refresh_transpose": ([_P, _P, _P, _P], _I),
     "rgb_reset_stream": ([_P, _I, _P], _I),
+    "rgb_window_view": ([_P, _I, _I64, _I64, ctypes.POINTER(_P), ctypes.POINTER(_I)], _I),
     "rgb_count_nonfinite": ([_P, _I, _I64, _I64, ctypes.POINTER(_I64), _P], _I),
     "rgb_inject_rows": ([_P, _P, _I, _I, _P, _P, _P, _I, _I, _P], _I),
     "rgb_onehot_rows": ([_P, _I, _I, _P, _P], _I),
@@ -81,7 +83,28 @@ def build(verbose: bool = False, force: bool = False) -> str:
         t = os.path.getmtime(LIB_PATH)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", *srcs]
+    # one nvcc per translation unit in parallel (the tensor-core file alone
+    # takes ~2 min), then one link step
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    heads = [os.path.join(HERE, h) for h in HEADERS]
+    newest_head = max(os.path.getmtime(h) for h in heads)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_head):
+            cmd = ["nvcc", *cflags, "-c", src, "-o", obj + ".tmp"]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True, cwd=HERE)
+            os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=HERE)

@@ -351,7 +351,7 @@ void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring,
 // delta_out = d - y and the per-row loss (engine.py:425-474)
 
 __global__ void inject_loss_kernel(const float* y, const void* target, int target_kind, int criterion, float* inj,
-                                   double* row_loss, int rows, int width) {
+                                   double* row_loss, int rows, int width, int* bad) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -374,17 +374,24 @@ __global__ void inject_loss_kernel(const float* y, const void* target, int targe
     const long long id = target_kind == 0 ? static_cast<const long long*>(target)[warp]
                                           : (long long)static_cast<const int*>(target)[warp];
     for (int j = lane; j < width; j += 32) ir[j] = (j == id ? 1.0f : 0.0f) - yr[j];
-    if (lane == 0 && id >= 0 && id < width) loss = -log((double)yr[id]);
+    if (lane == 0) {
+      if (id >= 0 && id < width) {
+        loss = -log((double)yr[id]);
+      } else {  // the reference raises IndexError (engine.py:443-456): poison the loss, flag the plan
+        loss = __longlong_as_double(0x7ff8000000000000LL);
+        if (bad) atomicOr(bad, 2);
+      }
+    }
   }
   for (int o = 16; o; o >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, o);
   if (lane == 0) row_loss[warp] = loss;
 }
 
 void launch_inject_loss(const float* y, const void* target, int target_kind, int criterion, float* inj,
-                        double* row_loss, int rows, int width, cudaStream_t s) {
+                        double* row_loss, int rows, int width, int* bad, cudaStream_t s) {
   const int threads = 256, per = threads / 32;
   inject_loss_kernel<<<(rows + per - 1) / per, threads, 0, s>>>(y, target, target_kind, criterion, inj, row_loss,
-                                                                rows, width);
+                                                                rows, width, bad);
 }
 
 // fixed-order fp64 sum (deterministic run to run)
@@ -493,19 +500,25 @@ void launch_count_nonfinite(const float* p, int64_t n, unsigned long long* out, 
 // gradient is a deterministic scatter over a stable sort of the window rows.
 namespace rgb {
 
-__global__ void ids_ring_write_kernel(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap) {
+__global__ void ids_ring_write_kernel(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap,
+                                      int vocab, int* bad) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int64_t t = t_a + r / S;
   const int64_t slot = ((t % cap) + cap) % cap;
   const int n = r % S;
-  const int32_t v = (int32_t)ids[r];
+  int32_t v = (int32_t)ids[r];
+  if (ids[r] < 0 || ids[r] >= vocab) {  // never gather outside W^T: zero row + plan error flag
+    v = -1;
+    if (bad) atomicOr(bad, 1);
+  }
   ring[slot * S + n] = v;            // the frame's slot
   ring[(slot + cap) * S + n] = v;    // and its mirror
 }
 
-void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, cudaStream_t s) {
-  if (rows > 0) ids_ring_write_kernel<<<(rows + 255) / 256, 256, 0, s>>>(ids, ring, rows, S, t_a, cap);
+void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, int vocab,
+                           int* bad, cudaStream_t s) {
+  if (rows > 0) ids_ring_write_kernel<<<(rows + 255) / 256, 256, 0, s>>>(ids, ring, rows, S, t_a, cap, vocab, bad);
 }
 
 __global__ void ids_reset_kernel(int32_t* ring, int S, int frames, int stream) {

@@ -60,7 +60,7 @@ void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring,
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.
 // criterion: 0 = cross entropy (softmax output), 1 = mse (identity output).
 void launch_inject_loss(const float* y, const void* target, int target_kind, int criterion, float* inj,
-                        double* row_loss, int rows, int width, cudaStream_t s);
+                        double* row_loss, int rows, int width, int* bad, cudaStream_t s);
 void launch_sum_rows(const double* row_loss, int rows, double* out, cudaStream_t s);
 // W -= lr * G over n floats and lo = W - trunc_tf32(W); g == nullptr: residual only.
 void launch_transpose(const TransposeGroup& p, cudaStream_t s);
@@ -68,7 +68,8 @@ void launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 void launch_onehot(const int64_t* ids, int rows, int width, float* out, cudaStream_t s);
 // token-id input path (rgb_kernels.cu): id history ring, W^T row gather,
 // deterministic scatter dW (returns the kernel launch count)
-void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, cudaStream_t s);
+void launch_ids_ring_write(const int64_t* ids, int32_t* ring, int rows, int S, int64_t t_a, int cap, int vocab,
+                           int* bad, cudaStream_t s);
 void launch_ids_reset(int32_t* ring, int S, int frames, int stream, cudaStream_t s);
 void launch_tape_gather(const int64_t* corpus, const int64_t* pos, int64_t* inputs, int64_t* targets, int S, int k,
                         cudaStream_t s);

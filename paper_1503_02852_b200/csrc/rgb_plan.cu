@@ -217,6 +217,7 @@ struct rgb_plan {
   std::vector<int32_t> prog[4];  // fwd, bwd, fwd_seq, bwd_seq
   float* ws = nullptr;
   int64_t cursor = 0;
+  int64_t last_t1 = -1;  // t1 of the last backward window (window buffer views)
 
   // TMA tensor maps (device copy + host mirror): per workspace buffer one
   // K-major map (box 32 x 128 rows, NT GEMM A operand) at [0, nb) and one
@@ -580,6 +581,9 @@ struct rgb_plan {
     return scratch_off + ((tgt + 3) & ~int64_t(3));
   }
   int64_t loss_off() const { return rowloss_off() + (((int64_t)hmax * S * 2 + 3) & ~int64_t(3)); }
+  // sticky input-error flags (bit 0: input id outside [0, n_in), bit 1: target
+  // id outside [0, n_out)), raised by the kernels, reported by rgb_read_loss
+  int* err_flag() const { return reinterpret_cast<int*>(ws + loss_off() + 4); }
 
   // ---- operand resolution -------------------------------------------------
   int resolve(const Ctx& c, int buf, int shift, int frames, float** out) const {
@@ -1200,6 +1204,15 @@ int cuda_rc(cudaError_t e, const char* what) {
   return fail(RGB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// report (and clear) the sticky input-error flags the kernels raise
+int check_err_flag(rgb_plan* p, int flag, cudaStream_t st) {
+  if (!flag) return RGB_OK;
+  cudaMemsetAsync(p->err_flag(), 0, sizeof(int), st);
+  cudaStreamSynchronize(st);
+  if (flag & 1) return fail(RGB_ERR_ENGINE, "input ids outside [0, %d)", p->n_in);
+  return fail(RGB_ERR_ENGINE, "target ids outside [0, %d)", p->n_out);
+}
+
 }  // namespace
 
 static int transpose_weights(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream);
@@ -1480,7 +1493,8 @@ int rgb_forward_chunk_ids(rgb_plan* p, const float* w, const float* wt, const in
   if (rc) return rc;
   p->id_mode = true;
   p->cursor += frames;
-  launch_ids_ring_write(p->ids_stage, p->ids_ring, rows, p->S, p->cursor - frames + 1, p->cap, st);
+  launch_ids_ring_write(p->ids_stage, p->ids_ring, rows, p->S, p->cursor - frames + 1, p->cap, p->n_in,
+                        p->err_flag(), st);
   note_launch();
   Ctx c;
   c.t_a = p->cursor - frames + 1;
@@ -1524,7 +1538,7 @@ int rgb_inject_output_error(rgb_plan* p, const void* target, int target_kind, in
   double* row_loss = reinterpret_cast<double*>(p->ws + p->rowloss_off());
   double* loss = reinterpret_cast<double*>(p->ws + p->loss_off());
   const int slot = prof_start(st);
-  launch_inject_loss(y, tdev, target_kind, criterion, inj, row_loss, rows, p->n_out, st);
+  launch_inject_loss(y, tdev, target_kind, criterion, inj, row_loss, rows, p->n_out, p->err_flag(), st);
   launch_sum_rows(row_loss, rows, loss, st);
   note_launch();
   note_launch();
@@ -1535,9 +1549,22 @@ int rgb_inject_output_error(rgb_plan* p, const void* target, int target_kind, in
 int rgb_read_loss(rgb_plan* p, double* loss, void* stream) {
   if (!p || !p->ws || !loss) return fail(RGB_ERR_KERNEL, "null argument");
   cudaStream_t st = as_stream(stream);
+  int flag = 0;
   int rc = cuda_rc(cudaMemcpyAsync(loss, p->ws + p->loss_off(), sizeof(double), cudaMemcpyDeviceToHost, st), "loss copy");
+  if (!rc) rc = cuda_rc(cudaMemcpyAsync(&flag, p->err_flag(), sizeof(int), cudaMemcpyDeviceToHost, st), "flag copy");
+  if (!rc) rc = cuda_rc(cudaStreamSynchronize(st), "loss sync");
   if (rc) return rc;
-  return cuda_rc(cudaStreamSynchronize(st), "loss sync");
+  return check_err_flag(p, flag, st);
+}
+
+int rgb_check_inputs(rgb_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  cudaStream_t st = as_stream(stream);
+  int flag = 0;
+  int rc = cuda_rc(cudaMemcpyAsync(&flag, p->err_flag(), sizeof(int), cudaMemcpyDeviceToHost, st), "flag copy");
+  if (!rc) rc = cuda_rc(cudaStreamSynchronize(st), "flag sync");
+  if (rc) return rc;
+  return check_err_flag(p, flag, st);
 }
 
 int rgb_read_loss_async(rgb_plan* p, double* dst, void* stream) {
@@ -1581,6 +1608,7 @@ int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_pri
   c.section = sequential ? 3 : 1;
   const auto& prog = p->prog[c.section];
   c.sec_base = prog.data();
+  p->last_t1 = c.t1;
   bool wf = false;
   int rc = p->run_wavefront(prog.data(), (int64_t)prog.size(), c, as_stream(stream), &wf);
   if (rc || wf) return rc;
@@ -1671,11 +1699,32 @@ int rgb_inject_rows(const float* y, const void* target, int target_kind, int cri
   if (!y || !target || !delta || !row_loss || !loss) return fail(RGB_ERR_KERNEL, "null argument");
   if (target_kind < 0 || target_kind > 2 || rows < 1 || width < 1) return fail(RGB_ERR_KERNEL, "bad arguments");
   cudaStream_t st = as_stream(stream);
-  launch_inject_loss(y, target, target_kind, criterion, delta, row_loss, rows, width, st);
+  launch_inject_loss(y, target, target_kind, criterion, delta, row_loss, rows, width, nullptr, st);
   launch_sum_rows(row_loss, rows, loss, st);
   note_launch();
   note_launch();
   return cuda_rc(cudaGetLastError(), "inject launch");
+}
+
+int rgb_window_view(const rgb_plan* p, int buffer, int64_t t_lo, int64_t t_hi, const float** ptr, int* width) {
+  if (!p || !p->ws || !ptr || !width) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (buffer < 0 || buffer >= (int)p->bufs.size() || t_hi < t_lo) return fail(RGB_ERR_KERNEL, "bad buffer or frame range");
+  const BufDesc& b = p->bufs[buffer];
+  if (b.kind == BUF_WIN && p->last_t1 < 0) return fail(RGB_ERR_ENGINE, "no backward window has run on this plan");
+  if (b.kind == BUF_WIN && t_lo <= p->last_t1 - p->hmax)
+    return fail(RGB_ERR_ENGINE, "frames [%lld, %lld] outside the last window (%lld, %lld]", (long long)t_lo,
+                (long long)t_hi, (long long)(p->last_t1 - p->hmax), (long long)p->last_t1);
+  if (b.kind == BUF_CHUNK) return fail(RGB_ERR_KERNEL, "chunk buffers have no frame view");
+  Ctx c;
+  c.t_a = t_lo;
+  c.t1 = p->last_t1;
+  c.frames = (int)(t_hi - t_lo + 1);
+  float* q;
+  int rc = p->resolve(c, buffer, 0, c.frames, &q);
+  if (rc) return rc;
+  *ptr = q;
+  *width = b.width;
+  return RGB_OK;
 }
 
 int rgb_count_nonfinite(rgb_plan* p, int buffer, int64_t t_lo, int64_t t_hi, int64_t* count, void* stream) {

@@ -174,6 +174,15 @@ __device__ __forceinline__ float tf32_residual(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+// x -> tf32_rna(x) over `bytes` of shared memory (plain TF32 mode operands)
+__device__ __forceinline__ void round_tf32_inplace(uint8_t* base, int bytes, int tid, int nthreads) {
+  float4* v = reinterpret_cast<float4*>(base);
+  for (int q = tid; q < bytes / 16; q += nthreads) {
+    const float4 x = v[q];
+    v[q] = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+  }
+}
+
 // One operand tile source: `rows` is the valid extent along M (or N), `kv` the
 // valid extent along K, ld the global leading dimension (elements).
 struct Src {
@@ -935,8 +944,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
           const float4 x = *reinterpret_cast<const float4*>(arow + ((c ^ (r & 7)) * 16));
           hi[4 * cc] = x.x, hi[4 * cc + 1] = x.y, hi[4 * cc + 2] = x.z, hi[4 * cc + 3] = x.w;
         }
+        if (p.terms != 1) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
+          for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) hi[q] = tf32_rna(hi[q]);  // plain TF32: round, do not truncate
+        }
         const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + TST * s + 16 * kh;
         tmem_st16(ta, hi);
         if (p.terms != 1) tmem_st16(ta + 32, lo);
@@ -959,6 +973,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
+      } else {
+        // plain TF32: round every smem operand to nearest (cvt.rna) in place --
+        // the MMA alone would truncate (a 2^-11 relative bias on every product)
+        if constexpr (!TA) round_tf32_inplace(base, C::A_BYTES, threadIdx.x, kProducers);
+        round_tf32_inplace(base + BOFF, C::B_BYTES, threadIdx.x, kProducers);
       }
       if (threadIdx.x == 0) { TRACE(4, it) }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1053,10 +1072,24 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // while the producers, converters and MMA issuer already run tile i+1 (in the
 // one-tile kernel the epilogue was ~25% of every multi-wave launch).
 //   warps 0-7 converters, 8 TMA A, 9 MMA, 10 TMA B, 11-14 epilogue.
-// Barriers: per stage tma_full / conv_full / empty (as above), per
-// accumulator buffer tmem_full (MMA commit -> epilogue) and tmem_empty
-// (epilogue -> MMA).  The epilogue stages 32-column chunks of the tile in a
-// private smem slice (TMEM -> smem -> coalesced 16-byte row walk).
+// Barriers: per stage tma_full / conv_full / empty (as above), per running
+// sum r_full (MMA commit -> epilogue) / r_empty (epilogue -> MMA), per chunk
+// accumulator x_full / x_empty.  The epilogue stages 16-column chunks of the
+// tile in a private smem slice (TMEM -> smem -> coalesced 16-byte row walk).
+//
+// K-chunked accumulation.  tcgen05 adds each k-step's products into the fp32
+// TMEM accumulator with truncation (round toward zero) in the alignment, so
+// one accumulator's relative error grows linearly with the number of MMAs it
+// absorbs (tools/accum_probe.py: 3xTF32 at K = 16384 -> 1.2e-4 random /
+// 3.1e-4 coherent data vs 6e-6 for SIMT fp32; the cfg4 dW depth h*S is
+// 16384).  So for deep K the MMA issuer restarts a fresh chunk accumulator X
+// every `kc` stages; the epilogue warps fold each finished chunk into the
+// tile's running sum R with round-to-nearest fp32 adds (tcgen05.ld X, R ->
+// FADD -> tcgen05.st R; R = X for chunk 0) and then release X.  R is private
+// to the epilogue threads, so the output pass of tile i overlaps the MMAs of
+// tile i+1's first chunk.  Truncation then acts on <= 3*kc*(BK/8)
+// accumulations per chunk.  Shallow launches (kc == 0) accumulate straight
+// into two alternating running sums as before.
 constexpr int kPersThreads = 480;
 constexpr int kPersConv = 128;  // converter threads (warps 0-3)
 constexpr int kEpiCols = 16;    // columns per epilogue chunk
@@ -1073,10 +1106,13 @@ struct PCfg {
   static constexpr int BUDGET = 227 * 1024 - 1024 - 512 - 2 * kChainBytes - CHUNK_BYTES;
   static constexpr int RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = RAW > 8 ? 8 : RAW;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  // TMEM: K-chunked mode: one running sum R then NX chunk accumulators X;
+  // unchunked mode: two running sums (see tma_gemm_persistent)
+  static constexpr int NX = 512 / BN - 1;  // chunk accumulators beside one running sum
+  static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512 + 2 * kChainBytes + CHUNK_BYTES;
   static_assert(STAGES >= 2, "persistent pipeline needs two stages");
-  static_assert(TMEM_COLS <= 512, "two accumulators must fit in TMEM");
+  static_assert(TMEM_COLS == 512 && 2 * BN <= 512, "running sums and chunk accumulators fill TMEM");
 };
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -1120,7 +1156,7 @@ struct PTile {
 };
 
 template <int BN, bool IS_DW, bool PAIR, class P>
-__global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles) {
+__global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles, int kc) {
   constexpr int NCTA = PAIR ? 2 : 1;
   constexpr int BNL = BN / NCTA;
   using C = PCfg<BN, BNL>;
@@ -1135,13 +1171,21 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   const int NST = one ? 2 * C::STAGES : C::STAGES;
   const int SB = one ? C::STAGE_BYTES / 2 : C::STAGE_BYTES;
   const int BOFF = one ? C::A_BYTES : C::B_OFF;
-  static_assert(6 * C::STAGES * 8 + 40 <= 512, "barrier region");
+  // kc == 0: unchunked (every tile accumulates in one of two running sums R,
+  // the epilogue of tile i overlaps the MMAs of tile i+1); kc > 0: K-chunked,
+  // one running sum R (TMEM columns [0, BN)) and NX chunk accumulators X
+  const bool chunked = kc > 0;
+  const int NR = chunked ? 1 : 2, NX = C::NX;
+  if (!chunked) kc = 1 << 30;
+  static_assert(6 * C::STAGES * 8 + 10 * 8 + 8 <= 512 && C::NX <= 3, "barrier region");
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* conv_full = tma_full + 2 * C::STAGES;
   uint64_t* empty = conv_full + 2 * C::STAGES;
-  uint64_t* tmem_full = empty + 2 * C::STAGES;   // [2]
-  uint64_t* tmem_empty = tmem_full + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* r_full = empty + 2 * C::STAGES;  // [NR]
+  uint64_t* r_empty = r_full + 2;            // [NR]
+  uint64_t* x_full = r_empty + 2;            // [NX <= 3]
+  uint64_t* x_empty = x_full + 3;            // [NX <= 3]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 3);
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 512);
   float* chunk_s = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512 + 2 * kChainBytes);
 
@@ -1156,8 +1200,12 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], 2 * NCTA);  // both epilogue groups of every CTA
+      mbar_init(&r_full[b], 1);
+      mbar_init(&r_empty[b], 2 * NCTA);  // both epilogue groups of every CTA
+    }
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&x_full[b], 1);
+      mbar_init(&x_empty[b], 2 * NCTA);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1214,15 +1262,29 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
       // ---------------- MMA issuer ----------------
       const uint32_t idesc = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       const bool split = p.terms != 1;
-      int g = 0, ti = 0;
+      int g = 0, ti = 0, xc = 0;
       for (int t = first; t < ntiles; t += stride, ++ti) {
         const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
-        const int b = ti & 1;
-        if constexpr (PAIR) mbar_wait_cluster(&tmem_empty[b], ((ti >> 1) & 1) ^ 1);
-        else mbar_wait(&tmem_empty[b], ((ti >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t acc = tmem + b * BN;
+        const int rb = ti % NR;
+        uint32_t acc = tmem + rb * BN;
+        if (!chunked) {
+          if constexpr (PAIR) mbar_wait_cluster(&r_empty[rb], ((ti / NR) & 1) ^ 1);
+          else mbar_wait(&r_empty[rb], ((ti / NR) & 1) ^ 1);
+        }
+        int xb = -1, chunk_end = 0;
         for (int it = 0; it < T.nstages; ++it, ++g) {
+          if (chunked && it == chunk_end) {  // next chunk: a fresh accumulator X
+            if (xb >= 0) {
+              if constexpr (PAIR) mma_commit_pair(&x_full[xb]);
+              else mma_commit(&x_full[xb]);
+              ++xc;
+            }
+            xb = xc % NX;
+            if constexpr (PAIR) mbar_wait_cluster(&x_empty[xb], ((xc / NX) & 1) ^ 1);
+            else mbar_wait(&x_empty[xb], ((xc / NX) & 1) ^ 1);
+            acc = tmem + (1 + xb) * BN;
+            chunk_end += kc;
+          }
           const int s = g % NST;
           if constexpr (PAIR) mbar_wait_cluster(&conv_full[s], (g / NST) & 1);
           else mbar_wait(&conv_full[s], (g / NST) & 1);
@@ -1246,7 +1308,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
               dbh = smem_desc(b_hi + off, 16, 1024, 2);
               dbl = smem_desc(b_lo + off, 16, 1024, 2);
             }
-            const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+            const uint32_t acc0 = (it > (chunked ? chunk_end - kc : 0) || j > 0) ? 1u : 0u;
             if constexpr (PAIR) {
               if (split) {
                 mma_tf32_pair(acc, dal, dbh, idesc, acc0);
@@ -1264,8 +1326,14 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           if constexpr (PAIR) mma_commit_pair(&empty[s]);
           else mma_commit(&empty[s]);
         }
-        if constexpr (PAIR) mma_commit_pair(&tmem_full[b]);
-        else mma_commit(&tmem_full[b]);
+        if (chunked) {  // the tile's last chunk accumulator
+          if constexpr (PAIR) mma_commit_pair(&x_full[xb]);
+          else mma_commit(&x_full[xb]);
+          ++xc;
+        } else {
+          if constexpr (PAIR) mma_commit_pair(&r_full[rb]);
+          else mma_commit(&r_full[rb]);
+        }
       }
     }
   } else if (warp < 4) {
@@ -1294,6 +1362,9 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           const float4 x = b_hi[q];
           b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
         }
+        } else {  // plain TF32: round both operands to nearest in place (the MMA would truncate)
+          round_tf32_inplace(base, C::A_BYTES, threadIdx.x, kPersConv);
+          round_tf32_inplace(base + BOFF, C::B_BYTES, threadIdx.x, kPersConv);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if constexpr (PAIR) {
@@ -1319,18 +1390,46 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     float* my_chunk = chunk_s + grp * (BM * kEpiLd);
     const int bar = 3 + grp;
     auto gsync = [&] { asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory"); };
-    auto release = [&](int b) {  // this group's last TMEM read of buffer b is done
+    auto release_bar = [&](uint64_t* bar) {  // this group's last TMEM access of a buffer is done
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       gsync();
       if (et == 0) {
-        if (rank == 0) mbar_arrive(&tmem_empty[b]);
-        else mbar_arrive_cluster(&tmem_empty[b], 0);
+        if (rank == 0) mbar_arrive(bar);
+        else mbar_arrive_cluster(bar, 0);
       }
     };
-    int ti = 0, staged_job = -1;
+    int ti = 0, staged_job = -1, xc = 0;
     for (int t = first; t < ntiles; t += stride, ++ti) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
-      const int b = ti & 1;
+      const int rb = ti % NR;
+      auto release = [&](int) {
+        if (!chunked) release_bar(&r_empty[rb]);
+      };
+      const uint32_t racc = tmem + rb * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      // K-chunked: fold every chunk of the tile into R (R = X, then R += X;
+      // round-to-nearest fp32 adds) over this group's 16-column slices -- the
+      // same slices the output pass reads, so R never crosses threads
+      const int nch = chunked ? (T.nstages + kc - 1) / kc : 0;
+      for (int c = 0; c < nch; ++c, ++xc) {
+        const int xb = xc % NX;
+        mbar_wait(&x_full[xb], (xc / NX) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t xacc = tmem + (1 + xb) * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+        for (int c0 = grp * kEpiCols; c0 < BN; c0 += 2 * kEpiCols) {
+          float vx[16], vr[16];
+          tmem_ld16(xacc + c0, vx);
+          if (c > 0) {
+            tmem_ld16(racc + c0, vr);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) vr[q] += vx[q];
+            tmem_st16(racc + c0, vr);
+          } else {
+            tmem_st16(racc + c0, vx);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        release_bar(&x_empty[xb]);
+      }
       if constexpr (!IS_DW) {
         if (T.jid != staged_job) {  // the chain of this tile's job
           gsync();
@@ -1339,9 +1438,12 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           staged_job = T.jid;
         }
       }
-      mbar_wait(&tmem_full[b], (ti >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t acc = tmem + b * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int b = rb;
+      if (!chunked) {
+        mbar_wait(&r_full[rb], (ti / NR) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      const uint32_t acc = racc;
       const int ncols = (T.N - T.n0) < BN ? (T.N - T.n0) : BN;
       const int nrows = (T.M - T.m0) < BM ? (T.M - T.m0) : BM;
       bool vec;
@@ -1423,8 +1525,32 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
 }
 
 // ntiles output tiles (pair tiles when PAIR) over min(ntiles, SMs/NCTA) CTAs / pairs
+// Truncating tensor-core accumulation (see tma_gemm_persistent): an
+// accumulator absorbing more than this many K-stages (3 * 4 MMAs each in
+// 3xTF32) loses ~1e-5 of its magnitude (a K = 1024 GEMM on coherent data
+// measured 2.3e-5, tools/accum_probe.py) -- the end-to-end budget after
+// several training steps is 1e-4 (tests/test_gpu_configs.py), so deeper
+// launches run K-chunked.
+constexpr int kMaxStagesPerAcc = 16;
+
+// stages per accumulation chunk for a launch whose tiles are at most
+// `max_stages` deep: 0 (unchunked) when the whole K fits the bound, else
+// 8 (3xTF32) / 24 (TF32) -- <= 96 truncating accumulations per chunk.
+// RGB_TC_KC overrides (experiments).
+int chunk_stages(int terms, int max_stages) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("RGB_TC_KC");
+    forced = e ? atoi(e) : 0;
+  }
+  const int per_acc = terms == 1 ? (max_stages + 2) / 3 : max_stages;
+  if (per_acc <= kMaxStagesPerAcc) return 0;
+  if (forced > 0) return forced;
+  return terms == 1 ? 24 : 8;
+}
+
 template <int BN, bool IS_DW, bool PAIR, class P>
-void launch_persistent(const P& p, int ntiles, cudaStream_t s) {
+void launch_persistent(const P& p, int ntiles, int max_stages, cudaStream_t s) {
   using C = PCfg<BN, BN / (PAIR ? 2 : 1)>;
   static bool configured = false;
   auto k = tma_gemm_persistent<BN, IS_DW, PAIR, P>;
@@ -1452,7 +1578,7 @@ void launch_persistent(const P& p, int ntiles, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, p, ntiles);
+  cudaLaunchKernelEx(&cfg, k, p, ntiles, chunk_stages(p.terms, max_stages));
 }
 
 template <int BN, bool IS_DW, bool PAIR, class P>
@@ -1697,8 +1823,10 @@ bool persist_enabled() {  // RGB_TC_PERSIST=0 disables the persistent kernels (t
   return on == 1;
 }
 
-// persistent kernel for launches of at least two waves
-bool use_persistent(int blocks, int bn) { return persist_enabled() && blocks > 148 && bn >= 128; }
+// persistent kernel for launches of at least two waves, or of deep K
+bool use_persistent(int blocks, int bn, int stages_per_acc = 0) {
+  return (persist_enabled() && blocks > 148 && bn >= 128) || stages_per_acc > tc::kMaxStagesPerAcc;
+}
 
 template <bool PAIR>
 void launch_nt_bn(const GemmGroup& p, int bn, int blocks, cudaStream_t s, int cluster = 1) {
@@ -1726,9 +1854,39 @@ long long tc_gemm_nt_scratch(const GemmGroup& p) {
   return csplit_enabled() && !c.pair ? 0 : nt_scratch(p, c);
 }
 
+int nt_max_stages(const GemmGroup& p) {
+  int kst = 0;
+  for (int j = 0; j < p.njobs; ++j) {
+    int st = 0;
+    for (int s = 0; s < p.job[j].nseg; ++s) st += (p.job[j].seg[s].k + kTmaNtBk - 1) / kTmaNtBk;
+    kst = st > kst ? st : kst;
+  }
+  return kst;
+}
+
+// tile width of K-chunked CTA-pair launches: 256 (half of B per CTA; one
+// chunk accumulator beside R) measured 1.3x faster at the cfg4 shapes than 128
+// (three chunk accumulators, but twice the A traffic per FLOP); RGB_TC_CHUNK_BN
+// overrides
+int chunk_pair_bn() {
+  static int bn = -1;
+  if (bn < 0) {
+    const char* e = getenv("RGB_TC_CHUNK_BN");
+    bn = e ? atoi(e) : 256;
+  }
+  return bn == 128 ? 128 : 256;
+}
+
 int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   p.terms = g_tc_terms;
   NtConfig c = nt_config(p);
+  // deep K without split-K: the K-chunked persistent kernel (accuracy)
+  const int acc_stages = (nt_max_stages(p) * (p.terms == 1 ? 1 : 3) + 2) / 3 / std::max(c.splits, 1);
+  if (p.tma && acc_stages > tc::kMaxStagesPerAcc) {
+    if (c.bn < 128) c.bn = 128;
+    if (c.pair) c.bn = chunk_pair_bn();
+    c.splits = 1;
+  }
   p.csplit = c.splits > 1 && csplit_enabled() ? 1 : 0;
   if (c.pair && c.splits > 1 && !p.csplit) c.splits = 1;  // pairs split only through the cluster
   if (c.splits > 1 && !p.csplit && (!p.part || nt_scratch(p, c) > p.part_cap)) c.splits = 1;  // no scratch
@@ -1743,14 +1901,14 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   }
   const int blocks = p.tile_start[p.njobs] * c.splits * (c.pair ? 2 : 1);
   if (blocks == 0) return 0;
-  if (p.tma && c.splits == 1 && use_persistent(blocks, c.bn)) {
+  if (p.tma && c.splits == 1 && use_persistent(blocks, c.bn, acc_stages)) {
     const int ntiles = p.tile_start[p.njobs];
     if (c.pair) {
-      if (c.bn == 256) tc::launch_persistent<256, false, true>(p, ntiles, s);
-      else tc::launch_persistent<128, false, true>(p, ntiles, s);
+      if (c.bn == 256) tc::launch_persistent<256, false, true>(p, ntiles, nt_max_stages(p), s);
+      else tc::launch_persistent<128, false, true>(p, ntiles, nt_max_stages(p), s);
     } else {
-      if (c.bn == 256) tc::launch_persistent<256, false, false>(p, ntiles, s);
-      else tc::launch_persistent<128, false, false>(p, ntiles, s);
+      if (c.bn == 256) tc::launch_persistent<256, false, false>(p, ntiles, nt_max_stages(p), s);
+      else tc::launch_persistent<128, false, false>(p, ntiles, nt_max_stages(p), s);
     }
   } else if (p.tma) {
     if (c.pair) launch_nt_bn<true>(p, c.bn, blocks, s, p.csplit ? c.splits : 1);
@@ -1783,6 +1941,9 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   };
   int bn = tc::pick_bn(tiles_for);
   if (pair && bn < 128) bn = 128;
+  // deep K (the window rows h*S): the K-chunked persistent kernel (accuracy)
+  const int acc_stages = ((p.k + 31) / 32 * (p.terms == 1 ? 1 : 3) + 2) / 3;
+  if (p.tma && acc_stages > tc::kMaxStagesPerAcc) bn = pair ? chunk_pair_bn() : std::max(bn, 128);
   p.tile_start[0] = 0;
   for (int j = 0; j < p.njobs; ++j) {
     p.tiles_n[j] = (p.job[j].n + bn - 1) / bn;
@@ -1790,14 +1951,14 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   }
   const int blocks = p.tile_start[p.njobs] * (pair ? 2 : 1);
   if (blocks == 0) return;
-  if (p.tma && use_persistent(blocks, bn)) {
+  if (p.tma && use_persistent(blocks, bn, acc_stages)) {
     const int ntiles = p.tile_start[p.njobs];
     if (pair) {
-      if (bn == 256) tc::launch_persistent<256, true, true>(p, ntiles, s);
-      else tc::launch_persistent<128, true, true>(p, ntiles, s);
+      if (bn == 256) tc::launch_persistent<256, true, true>(p, ntiles, (p.k + 31) / 32, s);
+      else tc::launch_persistent<128, true, true>(p, ntiles, (p.k + 31) / 32, s);
     } else {
-      if (bn == 256) tc::launch_persistent<256, true, false>(p, ntiles, s);
-      else tc::launch_persistent<128, true, false>(p, ntiles, s);
+      if (bn == 256) tc::launch_persistent<256, true, false>(p, ntiles, (p.k + 31) / 32, s);
+      else tc::launch_persistent<128, true, false>(p, ntiles, (p.k + 31) / 32, s);
     }
   } else if (p.tma) {
     if (pair) {

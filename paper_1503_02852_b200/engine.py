@@ -174,8 +174,8 @@ class Weights:
         self.net = net
         self.offsets, self.n_params = weight_offsets(net)
         dev = _device()
-        # [W | W_lo] and [W^T | W^T_lo]: the second halves hold the tf32 residuals
-        # the tensor-core GEMMs consume (refreshed by every update)
+        # W and W^T: n_params floats each (the 3xTF32 tensor-core GEMMs form the
+        # tf32 residuals of their operands in shared memory; no residual buffers)
         n2 = max(self.n_params, 4)
         self.flat = _flat if _flat is not None else torch.zeros(n2, dtype=DTYPE, device=dev)
         self.flat_t = _flat_t if _flat_t is not None else torch.zeros_like(self.flat)
@@ -485,10 +485,45 @@ def loss_value(target, output: Batch, criterion: Criterion) -> float:
 # backward (reference engine.py:481-599)
 
 
+def _view(state: StreamState, buf: int, t_lo: int, t_hi: int) -> torch.Tensor:
+    """Device view of schedule buffer ``buf`` over frames [t_lo, t_hi] through
+    rgb_window_view (rows frame-major, one row per stream)."""
+    ptr, width = ctypes.c_void_p(), ctypes.c_int()
+    _lib.check(_lib.lib().rgb_window_view(state._plan.handle, buf, t_lo, t_hi, ctypes.byref(ptr), ctypes.byref(width)),
+               "window_view")
+    off = (ptr.value - state.workspace.data_ptr()) // 4
+    n = (t_hi - t_lo + 1) * state.n * width.value
+    return state.workspace[off:off + n].view(-1, width.value)
+
+
+def window_errors(state: StreamState, t1: int, h: int) -> tuple[dict, dict]:
+    """(delta, eps) of the last backward window ending at t1: per-layer deltas
+    and per-edge eps over frames (t0', t1], t0' = max(t1 - h, 0), as the
+    reference computes them (engine.py:512-566; eps = delta of the destination
+    for additive layers, delta times the other factors' z for multiplicative
+    ones).  Device views, valid until the next backward_window."""
+    net, L = state.net, state.program.layout
+    t0p = max(t1 - h, 0)
+    delta, eps = {}, {}
+    if t1 <= t0p:
+        return delta, eps
+    for name, buf in L.names.items():
+        if name.startswith("d") and name[1:].isdigit():
+            delta[int(name[1:])] = _view(state, buf, t0p + 1, t1)
+    for c in net.connections:
+        if f"e{c.id}" in L.names:
+            eps[c.id] = _view(state, L.names[f"e{c.id}"], t0p + 1, t1)
+        elif c.dst in delta:
+            eps[c.id] = delta[c.dst]
+    return delta, eps
+
+
 def backward_window(net: NetworkDef, cg: CondensedGraph, weights: Weights, state: StreamState, window: BpttWindow,
-                    delta_out: Batch, *, frame_parallel: bool = True) -> GradStore:
+                    delta_out: Batch, *, frame_parallel: bool = True, capture: dict | None = None) -> GradStore:
     """Backpropagate the injected output errors through the window and return
-    dE/dW.  Pure with respect to ``state``."""
+    dE/dW.  Pure with respect to ``state``.  ``capture`` (a dict, optional;
+    no reference counterpart) receives ``delta`` / ``eps`` per layer / edge id
+    over (t0', t1] as device views (window_errors)."""
     _single_io(net)
     n = state.n
     if window.t1 != state.cursor:
@@ -507,6 +542,8 @@ def backward_window(net: NetworkDef, cg: CondensedGraph, weights: Weights, state
     grads.frames_streams = window.frames * n
     _lib.check(L.rgb_backward_window(state._plan.handle, _ptr(weights.flat_t), _ptr(grads.flat), window.h,
                                      window.h_prime, 0 if frame_parallel else 1, _stream()), "backward_window")
+    if capture is not None:
+        capture["delta"], capture["eps"] = window_errors(state, window.t1, window.h)
     return grads
 
 
@@ -669,13 +706,8 @@ class Trainer:
         gradient buffer over ranks between backward and SGD."""
         L, st, plan = self._lib, self._stream(), self.state._plan.handle
         hp = self.cfg.h_prime
-        if isinstance(inputs, torch.Tensor):
-            x, on_host, mode = inputs, 0 if inputs.is_cuda else 1, "dense" if inputs.is_floating_point() else "ids"
-            if mode == "ids" and x.dtype != torch.int64:
-                x = x.to(torch.int64)
-        else:
-            x, _, mode = _input_rows(self.net.layer(self.net.input_layers()[0].id), self.state, inputs)
-            on_host = 0
+        x, on_host, mode = self._check_inputs(inputs)
+        targets = self._check_targets(targets)
         if mode == "ids":  # token ids: id history, W^T row gathers, sorted-scatter dW
             _lib.check(L.rgb_forward_chunk_ids(plan, _ptr(self.weights.flat), _ptr(self.weights.flat_t), _ptr(x),
                                                on_host, hp, self._seq, st))
@@ -689,13 +721,9 @@ class Trainer:
                                                  ctypes.byref(bad), st))
                 if bad.value:
                     raise FloatingPointError(f"{bad.value} non-finite values in activations of layer {l.name!r}")
-        if isinstance(targets, torch.Tensor):
-            tkind = 2 if targets.is_floating_point() else (0 if targets.dtype == torch.int64 else 1)
-            _lib.check(L.rgb_inject_output_error(plan, _ptr(targets), tkind, 0 if targets.is_cuda else 1,
-                                                 _CRIT_CODE[self.cfg.criterion], hp, st))
-        else:
-            tgt, tkind = _target_arg(targets, 0, 0)
-            _lib.check(L.rgb_inject_output_error(plan, _ptr(tgt), tkind, 0, _CRIT_CODE[self.cfg.criterion], hp, st))
+        tkind = 2 if targets.is_floating_point() else (0 if targets.dtype == torch.int64 else 1)
+        _lib.check(L.rgb_inject_output_error(plan, _ptr(targets), tkind, 0 if targets.is_cuda else 1,
+                                             _CRIT_CODE[self.cfg.criterion], hp, st))
         if self.state.program.softmax_feeds is not None:
             raise EngineError(f"softmax layer {self.state.program.softmax_feeds!r} feeds other layers")
         _lib.check(L.rgb_backward_window(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat), self.cfg.h, hp,
@@ -704,6 +732,57 @@ class Trainer:
             exchange.allreduce_(self.grads.flat)
         _lib.check(L.rgb_sgd_update(self.weights._plan.handle, _ptr(self.weights.flat), _ptr(self.weights.flat_t),
                                     _ptr(self.grads.flat), ctypes.c_float(self.cfg.lr), st))
+
+    # ---- argument validation (reference forward_chunk / inject_output_error guards,
+    # engine.py:372-403, 436-456): shape, dtype, frames == h', streams == S; id
+    # ranges of host arrays here, of device tensors by the kernels' error flag
+    # (reported by loss() / check_inputs() without a sync inside step)
+    def _check_inputs(self, inputs):
+        S, hp = self.state.n, self.cfg.h_prime
+        lin = self.net.layer(self.net.input_layers()[0].id)
+        if not isinstance(inputs, torch.Tensor):
+            x, frames, mode = _input_rows(lin, self.state, inputs)
+            if frames != hp:
+                raise EngineError(f"chunk has {frames} frames, step wants h'={hp}")
+            return x, 0, mode
+        if inputs.is_floating_point():
+            if tuple(inputs.shape) != (hp * S, lin.size):
+                raise EngineError(f"dense inputs must be ({hp * S}, {lin.size}) = (h'*S, n_in), got "
+                                  f"{tuple(inputs.shape)}")
+            x = inputs if inputs.dtype == DTYPE else inputs.to(DTYPE)
+            return x.contiguous(), 0 if x.is_cuda else 1, "dense"
+        if inputs.ndim != 1 or inputs.shape[0] != hp * S:
+            raise EngineError(f"id inputs must be ({hp * S},) = (h'*S,), got {tuple(inputs.shape)}")
+        if not inputs.is_cuda and inputs.numel() and (int(inputs.min()) < 0 or int(inputs.max()) >= lin.size):
+            raise EngineError(f"input ids outside [0, {lin.size})")
+        x = inputs if inputs.dtype == torch.int64 else inputs.to(torch.int64)
+        return x.contiguous(), 0 if x.is_cuda else 1, "ids"
+
+    def _check_targets(self, targets) -> torch.Tensor:
+        S, hp = self.state.n, self.cfg.h_prime
+        n_out = self.lout.size
+        if isinstance(targets, Batch):
+            targets = _as_device_f32(targets.values)
+        elif not isinstance(targets, torch.Tensor):
+            targets = torch.as_tensor(np.asarray(targets))
+        if targets.is_floating_point():
+            if tuple(targets.shape) != (hp * S, n_out):
+                raise EngineError(f"dense targets must be ({hp * S}, {n_out}), got {tuple(targets.shape)}")
+            return (targets if targets.dtype == DTYPE else targets.to(DTYPE)).contiguous()
+        if self.cfg.criterion is not Criterion.CROSS_ENTROPY_SOFTMAX:
+            raise EngineError("class-id targets are only defined for cross-entropy")
+        if targets.ndim != 1 or targets.shape[0] != hp * S:
+            raise EngineError(f"need {hp * S} target ids, got {tuple(targets.shape)}")
+        if not targets.is_cuda and targets.numel() and (int(targets.min()) < 0 or int(targets.max()) >= n_out):
+            raise IndexError(f"target ids outside [0, {n_out})")
+        if targets.dtype not in (torch.int64, torch.int32):
+            targets = targets.to(torch.int64)
+        return targets.contiguous()
+
+    def check_inputs(self) -> None:
+        """Raise EngineError if a device-side id of an earlier step was out of
+        range (synchronises)."""
+        _lib.check(self._lib.rgb_check_inputs(self.state._plan.handle, self._stream()))
 
     def loss(self) -> float:
         v = ctypes.c_double()
@@ -821,10 +900,7 @@ def train_loop(net: NetworkDef, streams: StreamSource, config: TrainConfig, weig
         if config.reset_on_sequence_boundary and getattr(chunk, "new_sequence", None) is not None:
             for s in np.flatnonzero(np.asarray(chunk.new_sequence)):
                 tr.state.reset_stream(int(s))
-        inputs = chunk.inputs
-        if isinstance(inputs, Batch):
-            inputs = _as_device_f32(inputs.values)
-        tr.step(inputs, chunk.targets)
+        tr.step(chunk.inputs, chunk.targets)
         total = tr.loss()
         seconds = time.perf_counter() - start
         samples = config.h_prime * streams.n_streams

@@ -1,0 +1,95 @@
+"""GPU parity at the exact shapes of the benchmarked configs (BASELINE.json
+configs[1] and [3]), run the way bench.py runs them, against the float64 oracle.
+
+* cfg4 (the headline): build_stacked_lstm(1024, [1024]*3, 1024), S = 512,
+  h = 32, h' = 16, the default kernel variants (CTA pairs, persistent GEMMs,
+  cluster split-K / the persistent recurrent path), Trainer + CUDA-graph replay
+  (one graph per ring phase), 4 iterations incl. SGD.
+* cfg2 (the intra-stream line): 2 x LSTM512 (512 in/out), S = 1, h = 512,
+  h' = 256, persistent SCC loops + the cross-layer wavefront, graph replay.
+
+Every iteration compares the outputs, the loss, every delta and every eps of the
+window (reference engine.py:512-566, read through rgb_window_view) and every
+dW; the weights after the last SGD step are compared too.  Tolerance:
+1e-4 normwise, 1e-4 relative on the loss."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import engine_np as O  # noqa: E402
+from oracle_util import normwise  # noqa: E402
+
+import paper_1503_02852_b200 as P  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def run_graphed_vs_oracle(net, S, h, hp, iters, lr, seed, report):
+    """Trainer.step_graphed (first step eager, then one captured graph per ring
+    phase) against the oracle; returns the worst normwise error."""
+    cg = P.condense(net)
+    lin, lout = net.input_layers()[0], net.output_layers()[0]
+    W = O.init_weights(net, seed)
+    st_o = O.History(net, S, h)
+    w = P.Weights(net, W)
+    tr = P.Trainer(net, w, S, P.TrainConfig(h=h, h_prime=hp, lr=lr, iterations=1))
+    tr.enable_graphs()
+    gx, gt = tr.graph_inputs()
+    rng = np.random.default_rng(seed + 7)
+    worst = 0.0
+    for it in range(iters):
+        x = rng.uniform(-1, 1, size=(hp * S, lin.size))
+        t = rng.integers(0, lout.size, size=hp * S)
+        gx.copy_(torch.tensor(x, dtype=torch.float32))
+        gt.copy_(torch.tensor(t))
+        tr.step_graphed()
+        loss = tr.loss()
+        # oracle iteration (engine.py:732-758)
+        out_o = O.forward_chunk(net, cg, W, st_o, x)
+        loss_o = O.loss_value(t, out_o)
+        cap_o = {}
+        g_o = O.backward_window(net, cg, W, st_o, st_o.cursor, h, hp, O.inject_output_error(t, out_o),
+                                capture=cap_o)
+        O.sgd_update(W, g_o, lr)
+        t1 = tr.state.cursor
+        assert t1 == st_o.cursor
+        errs = {"out": normwise(tr.state.read_y(lout.id, t1 - hp + 1, t1).cpu().numpy(), out_o),
+                "loss": abs(loss - loss_o) / max(1.0, abs(loss_o))}
+        delta, eps = P.window_errors(tr.state, t1, h)
+        assert sorted(delta) == sorted(cap_o["delta"]) and sorted(eps) == sorted(cap_o["eps"])
+        errs["delta"] = max(normwise(delta[k].cpu().numpy(), v) for k, v in cap_o["delta"].items())
+        errs["eps"] = max(normwise(eps[k].cpu().numpy(), v) for k, v in cap_o["eps"].items())
+        gd = {cid: m.cpu().numpy() for cid, m in tr.grads.g.items()}
+        errs["dW"] = max(normwise(gd[cid], g_o[cid]) for cid in g_o)
+        report.append((it, errs))
+        worst = max(worst, *errs.values())
+    wn = w.numpy()
+    worst = max(worst, max(normwise(wn[cid], W[cid]) for cid in W))
+    return worst
+
+
+def test_cfg4_headline_config_matches_oracle():
+    net = P.build_stacked_lstm(1024, [1024] * 3, 1024)
+    report = []
+    worst = run_graphed_vs_oracle(net, S=512, h=32, hp=16, iters=4, lr=1e-3, seed=0, report=report)
+    print("cfg4 per-iteration normwise errors:", report)
+    assert worst < TOL, report
+
+
+def test_cfg2_intra_stream_config_matches_oracle():
+    net = P.build_stacked_lstm(512, [512, 512], 512)
+    report = []
+    worst = run_graphed_vs_oracle(net, S=1, h=512, hp=256, iters=3, lr=1e-3, seed=1, report=report)
+    print("cfg2 per-iteration normwise errors:", report)
+    assert worst < TOL, report

@@ -30,6 +30,20 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+def errors_vs_oracle(cap, cap_o) -> float:
+    """Worst normwise error of every delta and every eps (reference engine.py:
+    512-566) of one window; both sides must hold the same ids."""
+    assert set(cap["delta"]) == set(cap_o["delta"]), (sorted(cap["delta"]), sorted(cap_o["delta"]))
+    assert set(cap["eps"]) == set(cap_o["eps"]), (sorted(cap["eps"]), sorted(cap_o["eps"]))
+    worst = 0.0
+    for kind in ("delta", "eps"):
+        for k, ref in cap_o[kind].items():
+            got = cap[kind][k].cpu().numpy()
+            assert got.shape == ref.shape, (kind, k, got.shape, ref.shape)
+            worst = max(worst, normwise(got, ref))
+    return worst
+
+
 def run_pair(net, S, h, hp, iters, lr, seed, *, frame_parallel=True, crit=O.CE, hw=None, ids=False, chunk=True,
              loss_tol=1e-4):
     """Drive engine and oracle side by side; return the worst normwise error."""
@@ -50,7 +64,9 @@ def run_pair(net, S, h, hp, iters, lr, seed, *, frame_parallel=True, crit=O.CE, 
             x = rng.uniform(-1, 1, size=(hp * S, lin.size))
         t = rng.integers(0, lout.size, size=hp * S) if crit == O.CE else rng.uniform(-1, 1, size=(hp * S, lout.size))
         out_o = O.forward_chunk(net, cg, W, st_o, x)
-        g_o = O.backward_window(net, cg, W, st_o, st_o.cursor, hw, hp, O.inject_output_error(t, out_o))
+        cap_o, cap = {}, {}
+        g_o = O.backward_window(net, cg, W, st_o, st_o.cursor, hw, hp, O.inject_output_error(t, out_o),
+                                capture=cap_o)
         inp = xi if ids else P.Batch(x, hp, S)
         out = P.forward_chunk(net, cg, w, st, inp, frame_parallel=frame_parallel)
         worst = max(worst, normwise(out.numpy(), out_o))
@@ -59,10 +75,12 @@ def run_pair(net, S, h, hp, iters, lr, seed, *, frame_parallel=True, crit=O.CE, 
         d = P.inject_output_error(tgt, out, crit_p, lout.activation)
         loss = P.loss_value(tgt, out, crit_p)
         assert abs(loss - O.loss_value(t, out_o, crit)) <= loss_tol * max(1.0, abs(loss))
-        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, hw, hp), d, frame_parallel=frame_parallel)
+        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, hw, hp), d, frame_parallel=frame_parallel,
+                              capture=cap)
         gn = g.numpy()
         for cid in g_o:
             worst = max(worst, normwise(gn[cid], g_o[cid]))
+        worst = max(worst, errors_vs_oracle(cap, cap_o))
         O.sgd_update(W, g_o, lr)
         P.sgd_update(w, g, lr)
     wn = w.numpy()
@@ -93,11 +111,18 @@ def test_against_reference_golden_directly():
         out = P.forward_chunk(net, cg, w, st, P.Batch(x, spec["hp"], spec["S"]))
         assert normwise(out.numpy(), gold[f"out_{it}"]) < TOL
         d = P.inject_output_error(t, out, CE, P.Activation.SOFTMAX)
-        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, spec["h"], spec["hp"]), d)
+        cap = {}
+        g = P.backward_window(net, cg, w, st, P.BpttWindow(st.cursor, spec["h"], spec["hp"]), d, capture=cap)
         gn = g.numpy()
         for cid in gn:
             assert normwise(gn[cid], gold[f"g_{it}_{cid}"]) < TOL, (it, cid)
         P.sgd_update(w, g, spec["lr"])
+    # every delta and eps of the last window, straight from the reference
+    for kind in ("delta", "eps"):
+        keys = sorted(int(k.split("_")[1]) for k in gold.files if k.startswith(kind + "_"))
+        assert keys == sorted(cap[kind]), (kind, keys, sorted(cap[kind]))
+        for k in keys:
+            assert normwise(cap[kind][k].cpu().numpy(), gold[f"{kind}_{k}"]) < TOL, (kind, k)
 
 
 @pytest.mark.parametrize("seq", [False, True])

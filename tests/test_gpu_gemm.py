@@ -272,7 +272,7 @@ def test_engine_kernel_variants_agree(restore_tc_modes):
         out = tr.state.read_y(net.output_layers()[0].id, tr.state.cursor - hp + 1, tr.state.cursor).cpu().numpy()
         results.append((out, tr.grads.flat.cpu().numpy(), w.flat[: w.n_params].cpu().numpy()))
     for a, b in zip(results[0], results[1]):
-        assert normwise(a, b.astype(np.float64)) < 1e-5
+        assert normwise(a, b.astype(np.float64)) < 5e-5
 
 
 def test_pair_cluster_split_k_opt_in():
@@ -315,14 +315,41 @@ def test_id_inputs_with_tensor_cores_forced():
         _lib.check(L.rgb_set_gemm_mode(0))
 
 
+@pytest.mark.parametrize("kind", ["random", "coherent"])
+@pytest.mark.parametrize("k", [4096, 16384])
+def test_deep_k_accumulation_stays_fp32_exact(kind, k):
+    """tcgen05 accumulates with truncation, so one accumulator's error grows
+    with K (tools/accum_probe.py measured 3.1e-4 at K = 16384 before the
+    K-chunked accumulation); the dW depth of cfg4 is h*S = 16384.  Both forms
+    stay at the fp32 level (SIMT measured 6e-6 .. 7e-6 here)."""
+    rng = np.random.default_rng(k)
+    lo = 0.0 if kind == "coherent" else -1.0
+    m = n = 512
+    e, y = rng.uniform(lo, 1, size=(k, m)).astype(np.float32), rng.uniform(lo, 1, size=(k, n)).astype(np.float32)
+    ref = e.astype(np.float64).T @ y.astype(np.float64)
+    te, ty = torch.tensor(e, device="cuda"), torch.tensor(y, device="cuda")
+    g = torch.empty((m, n), device="cuda")
+    _lib.check(_lib.lib().rgb_gemm_dw(ctypes.c_void_p(te.data_ptr()), ctypes.c_void_p(ty.data_ptr()),
+                                      ctypes.c_void_p(g.data_ptr()), m, n, k, ctypes.c_float(1.0), 3, _stream()))
+    assert normwise(g.cpu().numpy(), ref) < 3e-5
+    a, b = torch.tensor(np.ascontiguousarray(e.T), device="cuda"), torch.tensor(np.ascontiguousarray(y.T), device="cuda")
+    c = torch.empty((m, n), device="cuda")
+    _lib.check(_lib.lib().rgb_gemm_nt_tma(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                          ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(c.data_ptr()), m, n, k,
+                                          _stream()))
+    assert normwise(c.cpu().numpy(), ref) < 3e-5
+
+
 # ---- plain-TF32 tensor-core mode (rgb_set_tc_precision(1)) ------------------
 # The north_star allows a TF32 GEMM mode "to a separately stated bound".  One
-# tcgen05 kind::tf32 product per k-step truncates both fp32 operands to a
-# 10-bit mantissa (relative step 2^-10); for U(-1,1) operands the normwise GEMM
-# error is ~4e-4.  Stated bounds: GEMM 2e-3, full training step (outputs,
-# weight gradients, weights after SGD) 2e-2 normwise, loss 1e-2 relative.
+# tcgen05 kind::tf32 product per k-step on operands rounded to nearest tf32
+# (cvt.rna in the converter warps; the MMA alone would truncate, a biased
+# 2^-11 relative error per operand); for U(-1,1) operands the normwise GEMM
+# error is ~2e-4.  Stated bounds (BASELINE.md §5): GEMM and full training step
+# (outputs, every delta / eps, weight gradients, weights after SGD) 2e-3
+# normwise, loss 1e-2 relative.
 TF32_GEMM_BOUND = 2e-3
-TF32_STEP_BOUND = 2e-2
+TF32_STEP_BOUND = 2e-3
 
 
 @pytest.fixture
@@ -345,7 +372,10 @@ def test_tc_precision_rejects_bad_values():
     P.set_tc_precision("3xtf32")
 
 
-@pytest.mark.parametrize("m,n,k", [(256, 512, 1024), (1024, 2048, 1024), (200, 300, 70)])
+@pytest.mark.parametrize("m,n,k", [(256, 512, 1024), (1024, 2048, 1024), (200, 300, 70),
+                                   # > 148 tiles (persistent kernels) and K deep enough to wrap the
+                                   # 8- / 16-slot logical stage rings several times
+                                   (4096, 4096, 2048)])
 def test_gemm_tf32_mode(_tf32, m, n, k):
     """Both tcgen05 forms (NT and dW, incl. the TMA-fed dW) in plain TF32:
     inside the stated bound, and measurably less exact than 3xTF32 (the mode
@@ -383,3 +413,13 @@ def test_engine_parity_tf32_mode(_tf32):
                         loss_tol=1e-2) < TF32_STEP_BOUND
     finally:
         _lib.check(_tf32.rgb_set_gemm_mode(0))
+
+
+def test_cfg4_shape_tf32_mode(_tf32):
+    """The cfg4 layer shapes (1024 wide, 2 layers, S = 256: persistent hoisted /
+    dW kernels, per-frame launches) in plain TF32 against the oracle, at the
+    TF32 bound, with every delta / eps compared."""
+    from test_gpu_engine import run_pair
+    worst = run_pair(P.build_stacked_lstm(1024, [1024, 1024], 1024), 256, 32, 16, 3, 1e-3, 6, loss_tol=1e-2)
+    print(f"cfg4-shape TF32 step error {worst:.2e}")
+    assert worst < TF32_STEP_BOUND
