@@ -340,7 +340,7 @@ def run_ours(args, cfg):
 
     import paper_1503_02852_b200 as P
     from paper_1503_02852_b200 import _lib
-    from paper_1503_02852_b200.dist import GradientExchange, init_from_env, shard_streams
+    from paper_1503_02852_b200.dist import GradientExchange, NcclExchange, init_from_env, shard_streams
 
     rank, world, local = init_from_env("nccl")
     if world != args.gpus:
@@ -349,7 +349,10 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
     L = _lib.lib()
     _lib.check(L.rgb_set_tc_precision(1 if args.tc_precision == "tf32" else 3))
-    ex = GradientExchange()
+    ex = GradientExchange()  # timing max over ranks (torch.distributed plumbing)
+    # the gradient exchange itself: NCCL through the C ABI, bucketed and
+    # overlapped with the backward (rgb_backward_window_allreduce)
+    nex = NcclExchange() if world > 1 else None
     S_total = cfg["S"] * (world if args.scaling == "weak" else 1)
     lo, hi = shard_streams(S_total, world, rank)
     S = hi - lo
@@ -361,7 +364,7 @@ def run_ours(args, cfg):
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     xs = [torch.rand((hp * S, cfg["n_in"]), device=dev, generator=g) * 2 - 1 for _ in range(pool)]
     ts = [torch.randint(0, cfg["n_out"], (hp * S,), device=dev, generator=g) for _ in range(pool)]
-    exch = ex if world > 1 else None
+    exch = nex
 
     def barrier():
         if world > 1:
@@ -490,7 +493,8 @@ def run_ours(args, cfg):
                                                      "Weights.init seed 0)",
         "config": {"workload": cfg["name"] + ": " + cfg["desc"], "streams_total": S_total, "streams_per_gpu": S,
                    "h": h, "h_prime": hp, "global_batch_frames": hp * S_total,
-                   "parallelism": f"dp{world} (streams sharded, NCCL all-reduce of dW)",
+                   "parallelism": f"dp{world} (streams sharded; dW summed by NCCL through the C ABI in "
+                                  f"per-supernode buckets overlapped with the backward)" if world > 1 else "dp1",
                    "l2": "no flush: per-step working set (history + W + W^T + dW) exceeds the 126 MB L2",
                    "schedule": "hoisted (paper §3.1)",
                    "launch": "CUDA-graph replay per ring phase" if graphs else "eager",
@@ -529,9 +533,41 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_tf32 and args.tc_precision != "tf32":
         line["tf32_mode"] = measure_tf32(P, L, cfg, S, value)
     print(json.dumps(line))
+    if nex is not None:
+        torch.cuda.synchronize()
+        nex.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def dry_setup(args):
+    """Rank setup only (CPU tests of the launcher): join the process group with
+    gloo, shard the streams, print one JSON line per rank."""
+    import torch.distributed as dist
+
+    from paper_1503_02852_b200.dist import init_from_env, shard_streams
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    rank, world, local = init_from_env("gloo")
+    lo, hi = shard_streams(cfg["S"], world, rank)
+    print(json.dumps({"dry_setup": True, "rank": rank, "world": world, "local_rank": local, "streams": [lo, hi]}),
+          flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def relaunch(args, argv) -> int:
+    """--gpus N > 1 without a launcher: re-run this script under
+    torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1."""
+    import socket
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def main(argv=None):
@@ -549,9 +585,15 @@ def main(argv=None):
                     help="tensor-core GEMM precision for the whole run (tf32: the separately bounded mode)")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    args = ap.parse_args(argv)
+    ap.add_argument("--dry-setup", action="store_true", help="rank setup only (launcher test, CPU)")
+    raw = sys.argv[1:] if argv is None else list(argv)
+    args = ap.parse_args(raw)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args, raw)
+    if args.dry_setup:
+        return dry_setup(args)
     cfg = dict(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)

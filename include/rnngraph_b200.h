@@ -123,6 +123,31 @@ int rgb_onehot_rows(const int64_t* ids, int rows, int width, float* out, void* s
 int rgb_backward_window(rgb_plan* plan, const float* wt, float* g, int h, int h_prime, int sequential,
                         void* stream);
 
+/* ---- Multi-GPU: stream-sharded data parallelism -------
+ * One process per GPU, each owning a slice of the S streams; the only exchange
+ * is the SUM of the weight gradients over the GPUs (the reference folds the
+ * per-stream partials in one process, engine.py:593-598).  NCCL is loaded at
+ * run time (dlopen of libnccl.so.2, the copy PyTorch maps; RGB_NCCL_LIB
+ * overrides).  Rank 0 draws the 128-byte unique id, the caller ships it to
+ * the other ranks (e.g. through the torch.distributed store). */
+typedef struct rgb_comm rgb_comm;
+int rgb_comm_unique_id(void* id_out /* 128 bytes */);
+int rgb_comm_init(const void* id /* 128 bytes */, int nranks, int rank, rgb_comm** out);
+int rgb_comm_destroy(rgb_comm* comm);
+int rgb_comm_size(const rgb_comm* comm, int* nranks, int* rank);
+/* In-place SUM of n fp32 gradients over all ranks (one flat buffer). */
+int rgb_allreduce_grads(rgb_comm* comm, float* g, int64_t n, void* stream);
+/* In-place SUM (op_max = 0) or MAX (op_max = 1) of n doubles (loss, timings). */
+int rgb_allreduce_f64(rgb_comm* comm, double* v, int64_t n, int op_max, void* stream);
+/* backward_window with the gradient exchange overlapped: the dW of the edges
+ * into each supernode is computed right after that supernode's backward
+ * (reverse topological order) and summed over the ranks on a communication
+ * stream while the supernodes below are backpropagated; the call's stream
+ * waits for every bucket before returning control of G.  comm == NULL runs
+ * the same bucketed schedule without communication. */
+int rgb_backward_window_allreduce(rgb_plan* plan, const float* wt, float* g, int h, int h_prime, rgb_comm* comm,
+                                  void* stream);
+
 /* sgd_update (engine.py:606-612): W -= lr*G fused with the WT = W^T refresh. */
 int rgb_sgd_update(rgb_plan* plan, float* w, float* wt, const float* g, float lr, void* stream);
 /* Weights.refresh (engine.py:138-139): WT = W^T. */

@@ -15,9 +15,10 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "librnngraph_b200.so")
-SOURCES = ["csrc/rgb_kernels.cu", "csrc/rgb_tc_gemm.cu", "csrc/rgb_scc.cu", "csrc/rgb_plan.cu", "csrc/rgb_prof.cu"]
+SOURCES = ["csrc/rgb_kernels.cu", "csrc/rgb_tc_gemm.cu", "csrc/rgb_scc.cu", "csrc/rgb_plan.cu", "csrc/rgb_prof.cu",
+           "csrc/rgb_comm.cu"]
 HEADERS = ["csrc/rgb_types.cuh", "csrc/rgb_kernels.cuh", "csrc/rgb_ew.cuh", "csrc/rgb_prof.cuh", "csrc/rgb_scc.cuh",
-           "../include/rnngraph_b200.h"]
+           "csrc/rgb_comm.cuh", "../include/rnngraph_b200.h"]
 PROF_CATEGORIES = ("ew", "gemm", "gemm_frame", "ew_frame", "dw", "softmax", "inject", "sgd", "transpose", "scc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -45,6 +46,13 @@ _SIGS = {
     "rgb_set_injection": ([_P, _P, _I, _P], _I),
     "rgb_get_injection": ([_P, _P, _I, _P], _I),
     "rgb_backward_window": ([_P, _P, _P, _I, _I, _I, _P], _I),
+    "rgb_comm_unique_id": ([_P], _I),
+    "rgb_comm_init": ([_P, _I, _I, ctypes.POINTER(_P)], _I),
+    "rgb_comm_destroy": ([_P], _I),
+    "rgb_comm_size": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "rgb_allreduce_grads": ([_P, _P, _I64, _P], _I),
+    "rgb_allreduce_f64": ([_P, _P, _I64, _I, _P], _I),
+    "rgb_backward_window_allreduce": ([_P, _P, _P, _I, _I, _P, _P], _I),
     "rgb_sgd_update": ([_P, _P, _P, _P, ctypes.c_float, _P], _I),
     "rgb_refresh_transpose": ([_P, _P, _P, _P], _I),
     "rgb_reset_stream": ([_P, _I, _P], _I),
@@ -104,7 +112,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH + ".tmp", *objs]
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH + ".tmp", *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=HERE)

@@ -23,6 +23,7 @@
 #include "rgb_kernels.cuh"
 #include "rgb_prof.cuh"
 #include "rgb_scc.cuh"
+#include "rgb_comm.cuh"
 
 #include <map>
 
@@ -45,7 +46,8 @@ int fail(int code, const char* fmt, ...) {
 constexpr int32_t kMagic = 0x52474231;
 constexpr int kHeader = 32;
 enum BufKind { BUF_RING = 0, BUF_WIN = 1, BUF_CHUNK = 2 };
-enum Step { STEP_EW = 1, STEP_GEMM = 2, STEP_SOFTMAX = 3, STEP_LOOP = 4, STEP_DW = 5 };
+enum Step { STEP_EW = 1, STEP_GEMM = 2, STEP_SOFTMAX = 3, STEP_LOOP = 4, STEP_DW = 5, STEP_AR = 6 };
+constexpr int kSections = 5;  // fwd, bwd, fwd_seq, bwd_seq, bwd_bucketed
 
 struct BufDesc {
   int kind, width;
@@ -149,6 +151,9 @@ int64_t step_words(const int32_t* p, int64_t i, int64_t n) {
   } else if (kind == STEP_DW) {
     const int nj = p[i++];
     i += 5 * (int64_t)nj;
+  } else if (kind == STEP_AR) {
+    const int nr = p[i++];
+    i += 4 * (int64_t)nr;
   } else {
     return -1;
   }
@@ -214,7 +219,7 @@ struct rgb_plan {
   int64_t scratch_off = 0, ws_floats = 0, n_params = 0;
   std::vector<BufDesc> bufs;
   std::vector<WDesc> wts;
-  std::vector<int32_t> prog[4];  // fwd, bwd, fwd_seq, bwd_seq
+  std::vector<int32_t> prog[kSections];  // fwd, bwd, fwd_seq, bwd_seq, bwd_bucketed
   float* ws = nullptr;
   int64_t cursor = 0;
   int64_t last_t1 = -1;  // t1 of the last backward window (window buffer views)
@@ -231,7 +236,7 @@ struct rgb_plan {
 
   // device copies for the persistent SCC kernel: program sections, tables,
   // grid-barrier state; plus the per-loop eligibility decisions
-  int32_t* prog_dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int32_t* prog_dev[kSections] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   SccBuf* bufs_dev = nullptr;
   SccW* wts_dev = nullptr;
   unsigned* bar_dev = nullptr;
@@ -241,7 +246,15 @@ struct rgb_plan {
   // wavefront: extra streams (one per stage after the first) and events
   std::vector<cudaStream_t> wf_streams;
   std::vector<cudaEvent_t> wf_events;
-  int wf_ok[4] = {-1, -1, -1, -1};  // per section: structure eligible (cached after the first look)
+  int wf_ok[kSections] = {-1, -1, -1, -1, -1};  // per section: structure eligible (cached after the first look)
+  // bucketed gradient exchange (rgb_backward_window_allreduce): the
+  // communicator of the running call, its stream and fork/join events
+  rgb_comm* comm = nullptr;
+  float* comm_g = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> comm_events;
+  int comm_next = 0;
+  bool comm_forked = false;
   unsigned char* tcache_pool = nullptr;
   int tcache_next = 0;
   struct SccPlan {
@@ -336,11 +349,13 @@ struct rgb_plan {
     if (bar_dev) cudaFree(bar_dev);
     if (tcache_pool) cudaFree(tcache_pool);
     for (auto e : wf_events) cudaEventDestroy(e);
+    for (auto e : comm_events) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto q : wf_streams) cudaStreamDestroy(q);
   }
 
   int upload_scc_tables() {
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kSections; ++k) {
       if (prog[k].empty() || prog_dev[k]) continue;
       if (cudaMalloc(&prog_dev[k], prog[k].size() * 4) != cudaSuccess ||
           cudaMemcpy(prog_dev[k], prog[k].data(), prog[k].size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -903,6 +918,17 @@ struct rgb_plan {
     return rc;
   }
 
+  cudaEvent_t ev_tmp = nullptr;
+  int next_comm_event(cudaEvent_t* out) {
+    if (comm_next >= (int)comm_events.size()) {  // (event creation is legal inside a graph capture)
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(RGB_ERR_CUDA, "comm event");
+      comm_events.push_back(e);
+    }
+    *out = comm_events[comm_next++];
+    return RGB_OK;
+  }
+
   int run(const int32_t* p, int64_t n, const Ctx& c, cudaStream_t st) {
     Reader rd{p, n};
     while (rd.i < n) {
@@ -1175,6 +1201,30 @@ struct rgb_plan {
           for (int q = 0; q < nl; ++q) note_launch();
         }
         prof_stop(slot, st, PROF_DW, flops, bytes);
+      } else if (kind == STEP_AR) {
+        // all-reduce marker of the bucketed backward: the dW of this bucket is
+        // enqueued on `st`; sum its gradient ranges over the GPUs on the
+        // communication stream (forked from `st` here, joined at the end of
+        // rgb_backward_window_allreduce) while the backward continues
+        const int nr = rd.next();
+        std::vector<std::pair<int64_t, int64_t>> ranges;
+        for (int i = 0; i < nr; ++i) {
+          const int32_t a0 = rd.next(), a1 = rd.next(), b0 = rd.next(), b1 = rd.next();
+          ranges.push_back({join64(a0, a1), join64(b0, b1)});
+        }
+        if (comm && comm_g) {
+          if ((rc = next_comm_event(&ev_tmp))) return rc;
+          if ((rc = cuda_rc(cudaEventRecord(ev_tmp, st), "bucket record"))) return rc;
+          if ((rc = cuda_rc(cudaStreamWaitEvent(comm_stream, ev_tmp, 0), "bucket wait"))) return rc;
+          comm_forked = true;
+          if ((rc = comm_group(true))) return rc;
+          for (const auto& r : ranges)
+            if ((rc = comm_allreduce_f32(comm, comm_g + r.first, (size_t)(r.second - r.first), comm_stream))) {
+              comm_group(false);
+              return rc;
+            }
+          if ((rc = comm_group(false))) return rc;
+        }
       } else {
         return fail(RGB_ERR_KERNEL, "unknown step %d", kind);
       }
@@ -1203,6 +1253,14 @@ int cuda_rc(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return RGB_OK;
   return fail(RGB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
+
+}  // namespace
+
+namespace rgb {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace rgb
+
+namespace {
 
 // report (and clear) the sticky input-error flags the kernels raise
 int check_err_flag(rgb_plan* p, int flag, cudaStream_t st) {
@@ -1386,7 +1444,7 @@ int rgb_plan_create(const int32_t* prog, int64_t n, rgb_plan** out) {
   p->scratch_off = join64(prog[14], prog[15]);
   p->ws_floats = join64(prog[16], prog[17]);
   p->n_params = join64(prog[18], prog[19]);
-  int64_t lens[4] = {prog[20], prog[21], prog[22], prog[23]};
+  int64_t lens[kSections] = {prog[20], prog[21], prog[22], prog[23], prog[24]};
   int64_t pos = kHeader;
   if (pos + 4LL * nb + 4LL * nw > n) {
     delete p;
@@ -1394,7 +1452,7 @@ int rgb_plan_create(const int32_t* prog, int64_t n, rgb_plan** out) {
   }
   for (int i = 0; i < nb; ++i, pos += 4) p->bufs.push_back({prog[pos], prog[pos + 1], join64(prog[pos + 2], prog[pos + 3])});
   for (int i = 0; i < nw; ++i, pos += 4) p->wts.push_back({prog[pos], prog[pos + 1], join64(prog[pos + 2], prog[pos + 3])});
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < kSections; ++k) {
     if (pos + lens[k] > n) {
       delete p;
       return fail(RGB_ERR_KERNEL, "truncated program section %d", k);
@@ -1613,6 +1671,46 @@ int rgb_backward_window(rgb_plan* p, const float* wt, float* g, int h, int h_pri
   int rc = p->run_wavefront(prog.data(), (int64_t)prog.size(), c, as_stream(stream), &wf);
   if (rc || wf) return rc;
   return p->run(prog.data(), (int64_t)prog.size(), c, as_stream(stream));
+}
+
+int rgb_backward_window_allreduce(rgb_plan* p, const float* wt, float* g, int h, int h_prime, rgb_comm* comm,
+                                  void* stream) {
+  if (!p || !p->ws || !wt || !g) return fail(RGB_ERR_KERNEL, "null argument or unbound plan");
+  if (p->prog[4].empty()) return fail(RGB_ERR_KERNEL, "program has no bucketed backward section");
+  if (!(1 <= h_prime && h_prime <= h)) return fail(RGB_ERR_ENGINE, "need 1 <= h'=%d <= h=%d", h_prime, h);
+  if (h > p->hmax) return fail(RGB_ERR_ENGINE, "window h=%d exceeds state h=%d", h, p->hmax);
+  if (p->cursor < h_prime) return fail(RGB_ERR_ENGINE, "t1=%lld leaves no room for %d injected frames",
+                                       (long long)p->cursor, h_prime);
+  cudaStream_t st = as_stream(stream);
+  if (comm && !p->comm_stream &&
+      cudaStreamCreateWithFlags(&p->comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(RGB_ERR_CUDA, "communication stream");
+  Ctx c;
+  c.t1 = p->cursor;
+  c.t_a = c.t1 - h + 1;
+  c.frames = h;
+  c.t0 = c.t1 - h_prime;
+  c.chunk_base = c.t0 + 1;
+  c.wt = wt;
+  c.g = g;
+  c.section = 4;
+  const auto& prog = p->prog[4];
+  c.sec_base = prog.data();
+  p->last_t1 = c.t1;
+  p->comm = comm;
+  p->comm_g = g;
+  p->comm_next = 0;
+  p->comm_forked = false;
+  int rc = p->run(prog.data(), (int64_t)prog.size(), c, st);
+  if (!rc && p->comm_forked) {  // join: SGD on `st` needs every bucket summed
+    cudaEvent_t e;
+    rc = p->next_comm_event(&e);
+    if (!rc) rc = cuda_rc(cudaEventRecord(e, p->comm_stream), "join record");
+    if (!rc) rc = cuda_rc(cudaStreamWaitEvent(st, e, 0), "join wait");
+  }
+  p->comm = nullptr;
+  p->comm_g = nullptr;
+  return rc;
 }
 
 int rgb_sgd_update(rgb_plan* p, float* w, float* wt, const float* g, float lr, void* stream) {

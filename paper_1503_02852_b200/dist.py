@@ -17,7 +17,7 @@ import os
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_streams", "GradientExchange", "init_from_env"]
+__all__ = ["shard_streams", "GradientExchange", "NcclExchange", "init_from_env"]
 
 
 def shard_streams(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -48,6 +48,67 @@ class GradientExchange:
         t = torch.tensor([value], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
+
+
+class NcclExchange:
+    """The GPU exchange through the C ABI (include/rnngraph_b200.h): one NCCL
+    communicator per process (rgb_comm_init; rank 0's unique id travels
+    through the torch.distributed store -- torch is plumbing here), and the
+    bucketed backward (rgb_backward_window_allreduce) that sums each
+    supernode's weight gradients over the GPUs while the backward of the
+    supernodes below it runs.  Trainer.step(..., exchange=NcclExchange())
+    uses it instead of backward + a separate all-reduce."""
+
+    native = True
+
+    def __init__(self, group=None):
+        import ctypes
+
+        from . import _lib
+        self._lib = _lib.lib()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(self._lib.rgb_comm_unique_id(ctypes.cast(uid, ctypes.c_void_p)), "comm_unique_id")
+        if self.world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            ctypes.memmove(uid, box[0], 128)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.rgb_comm_init(ctypes.cast(uid, ctypes.c_void_p), self.world, self.rank, ctypes.byref(h)),
+                   "comm_init")
+        self.handle = h
+
+    def allreduce_(self, flat: torch.Tensor) -> torch.Tensor:
+        import ctypes
+
+        from . import _lib
+        _lib.check(self._lib.rgb_allreduce_grads(self.handle, ctypes.c_void_p(flat.data_ptr()), flat.numel(),
+                                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return flat
+
+    def max_(self, value: float, device=None) -> float:
+        import ctypes
+
+        from . import _lib
+        if self.world == 1:
+            return value
+        t = torch.tensor([value], dtype=torch.float64, device=device or "cuda")
+        _lib.check(self._lib.rgb_allreduce_f64(self.handle, ctypes.c_void_p(t.data_ptr()), 1, 1,
+                                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return float(t.item())
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.rgb_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 def init_from_env(backend: str) -> tuple[int, int, int]:

@@ -726,10 +726,16 @@ class Trainer:
                                              _CRIT_CODE[self.cfg.criterion], hp, st))
         if self.state.program.softmax_feeds is not None:
             raise EngineError(f"softmax layer {self.state.program.softmax_feeds!r} feeds other layers")
-        _lib.check(L.rgb_backward_window(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat), self.cfg.h, hp,
-                                         self._seq, st))
-        if exchange is not None:
-            exchange.allreduce_(self.grads.flat)
+        if exchange is not None and getattr(exchange, "native", False) and not self._seq:
+            # bucketed backward: each supernode's dW summed over the GPUs while
+            # the backward below it runs (C ABI + NCCL, dist.NcclExchange)
+            _lib.check(L.rgb_backward_window_allreduce(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat),
+                                                       self.cfg.h, hp, exchange.handle, st))
+        else:
+            _lib.check(L.rgb_backward_window(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat), self.cfg.h, hp,
+                                             self._seq, st))
+            if exchange is not None:
+                exchange.allreduce_(self.grads.flat)
         _lib.check(L.rgb_sgd_update(self.weights._plan.handle, _ptr(self.weights.flat), _ptr(self.weights.flat_t),
                                     _ptr(self.grads.flat), ctypes.c_float(self.cfg.lr), st))
 

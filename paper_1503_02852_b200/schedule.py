@@ -52,7 +52,7 @@ __all__ = ["Program", "build_program", "EngineError"]
 MAGIC = 0x52474231
 HEADER = 32
 RING, WIN, CHUNK = 0, 1, 2
-STEP_EW, STEP_GEMM, STEP_SOFTMAX, STEP_LOOP, STEP_DW = 1, 2, 3, 4, 5
+STEP_EW, STEP_GEMM, STEP_SOFTMAX, STEP_LOOP, STEP_DW, STEP_AR = 1, 2, 3, 4, 5, 6
 EW_FWD_ADD, EW_FWD_MUL, EW_CONST1, EW_BWD = 0, 1, 2, 3
 ACT = {Activation.IDENTITY: 0, Activation.SIGMOID: 1, Activation.TANH: 2, Activation.SOFTMAX: 3}
 MAX_TERMS, MAX_RANK1, MAX_FAC, MAX_CHAIN, MAX_SEGS, MAX_JOBS, MAX_CHAINS, MAX_DW = 4, 3, 4, 6, 4, 8, 8, 48
@@ -155,6 +155,11 @@ class Dw:
     jobs: list      # (eps_buf, eps_shift, y_buf, y_shift, cid)
 
 
+@dataclass
+class AllReduce:
+    ranges: list    # (first, last) float offsets into the flat gradient, [first, last)
+
+
 # ---------------------------------------------------------------------------
 # packing items into launches
 
@@ -219,7 +224,7 @@ def pack(items, single_frame: bool):
         cur = None
 
     for it in items:
-        if isinstance(it, (Softmax, Loop, Dw)):
+        if isinstance(it, (Softmax, Loop, Dw, AllReduce)):
             flush()
             steps.append(it)
             continue
@@ -332,6 +337,10 @@ def encode(steps) -> list[int]:
                 out += [STEP_DW, len(part)]
                 for j in part:
                     out += list(j)
+        elif isinstance(st, AllReduce):
+            out += [STEP_AR, len(st.ranges)]
+            for a, b in st.ranges:
+                out += [*_split64(a), *_split64(b)]
         else:  # pragma: no cover
             raise TypeError(st)
     return out
@@ -552,6 +561,69 @@ class _Emitter:
             items.append(Loop(False, pack(body, True)))
         return pack(items, False)
 
+    def _dw_jobs(self, conns):
+        jobs = []
+        for c in conns:
+            e, s = self.eps_ref(c.id, 0)
+            jobs.append((e, s, self.y[c.src], -c.delay, c.id))
+        return jobs
+
+    def _ar_ranges(self, conns):
+        """Flat-gradient ranges of ``conns``, adjacent ones merged."""
+        w_off, _ = weight_offsets(self.net)
+        spans = sorted((w_off[c.id], w_off[c.id] + self.net.layer(c.dst).size * self.net.layer(c.src).size)
+                       for c in conns)
+        out = []
+        for a, b in spans:
+            if out and a <= _align4(out[-1][1]):
+                out[-1] = (out[-1][0], max(out[-1][1], b))
+            else:
+                out.append((a, b))
+        return out
+
+    def backward_bucketed(self):
+        """The hoisted backward with the weight gradients in buckets for the
+        multi-GPU exchange.  Supernodes are visited in reverse
+        topological order as in backward(); the dW of an edge can run once the
+        supernode holding its destination is done (its eps are final there,
+        engine.py:519-566).  Finished edges collect into a bucket that is
+        flushed -- one grouped dW step, then an all-reduce marker over those
+        edges' gradient ranges -- right before the next recurrent SCC loop, so
+        the executor sums the bucket over the GPUs while that latency-bound
+        frame loop runs; the last bucket follows the last supernode.  Every
+        dense edge lands in exactly one bucket (cfg4: 4 buckets, top layer
+        first)."""
+        self._phase, self._partial, self._folded = "b", {}, {}
+        self.softmax_feeds = None
+        topo = [self.cg.nodes[i] for i in reversed(self.cg.topo_order)]
+        items, pending, done = [], [], set()
+
+        def flush():
+            nonlocal pending
+            if pending:
+                items.append(Dw(self._dw_jobs(pending)))
+                items.append(AllReduce(self._ar_ranges(pending)))
+            pending = []
+
+        for node in topo:
+            if not node.recurrent:
+                items += self._bwd_layer(node.internal_order[0], "all")
+            else:
+                for lid in reversed(node.internal_order):
+                    items += self._bwd_layer(lid, "ext")
+                body = []
+                for lid in reversed(node.internal_order):
+                    body += self._bwd_layer(lid, "int")
+                flush()
+                items.append(Loop(True, pack(body, True)))
+            members = set(node.internal_order)
+            conns = [c for c in self.net.iter_dense() if c.dst in members and c.id not in done]
+            done.update(c.id for c in conns)
+            pending += conns
+        pending += [c for c in self.net.iter_dense() if c.id not in done]
+        flush()
+        return pack(items, False)
+
     def backward(self, sequential: bool):
         self._phase, self._partial, self._folded = "b", {}, {}
         self.softmax_feeds = None
@@ -627,6 +699,7 @@ def build_program(net: NetworkDef, cg: CondensedGraph, S: int, h: int, chunk: in
     em = _Emitter(net, cg, S, h, cap)
     fwd = em.forward(False)
     fwd_seq = em.forward(True)
+    bwd_bkt = em.backward_bucketed()
     bwd = em.backward(False)
     softmax_feeds = em.softmax_feeds
     bwd_seq = em.backward(True)
@@ -635,12 +708,12 @@ def build_program(net: NetworkDef, cg: CondensedGraph, S: int, h: int, chunk: in
     L.scratch_off = L.ws_floats
     tgt = _align(h * S * max(net.layer(em.lout.id).size, 2))
     L.ws_floats = L.scratch_off + tgt + _align(2 * h * S) + ALIGN
-    sections = [encode(fwd), encode(bwd), encode(fwd_seq), encode(bwd_seq)]
+    sections = [encode(fwd), encode(bwd), encode(fwd_seq), encode(bwd_seq), encode(bwd_bkt)]
     hdr = [0] * HEADER
     hdr[0:14] = [MAGIC, 1, S, h, cap, net.max_delay, len(L.bufs), len(net.connections), em.y[em.lin.id],
                  em.stage, em.y[em.lout.id], em.inj, em.lin.size, em.lout.size]
     hdr[14:20] = [*_split64(L.scratch_off), *_split64(L.ws_floats), *_split64(L.n_params)]
-    hdr[20:24] = [len(s) for s in sections]
+    hdr[20:25] = [len(s) for s in sections]
     words = list(hdr)
     for kind, width, o, _ in L.bufs:
         words += [kind, width, *_split64(o)]
@@ -652,10 +725,15 @@ def build_program(net: NetworkDef, cg: CondensedGraph, S: int, h: int, chunk: in
     for s in sections:
         words += s
     stats = {"forward": _count(fwd), "backward": _count(bwd), "forward_seq": _count(fwd_seq),
-             "backward_seq": _count(bwd_seq)}
+             "backward_seq": _count(bwd_seq), "backward_bucketed": _count(bwd_bkt),
+             "buckets": [st.ranges for st in bwd_bkt if isinstance(st, AllReduce)]}
     return Program(words=np.asarray(words, dtype=np.int32), layout=L, y_buf=dict(em.y), in_buf=em.y[em.lin.id],
                    out_buf=em.y[em.lout.id], stage_buf=em.stage, inj_buf=em.inj, softmax_feeds=softmax_feeds,
                    stats=stats)
+
+
+def _align4(v: int) -> int:
+    return (v + 3) // 4 * 4
 
 
 def _split64(v: int):

@@ -41,7 +41,7 @@ class Sim:
         self.in_buf, self.stage_buf, self.out_buf, self.inj_buf, self.n_in, self.n_out = w[8:14]
         self.ws_floats = _j64(w[16], w[17])
         self.n_params = _j64(w[18], w[19])
-        lens = w[20:24]
+        lens = w[20:25]
         pos = SC.HEADER
         self.bufs = []
         for _ in range(nb):
@@ -206,6 +206,12 @@ class Sim:
                     Y = self.view(ctx, yb, ys, F)
                     rows, cols, off = self.wts[cid]
                     ctx["g"][off:off + rows * cols] = (-(E.T @ Y)).ravel()
+                    ctx.setdefault("dw_written", []).append((off, off + rows * cols))
+            elif kind == SC.STEP_AR:
+                # the executor sums these ranges over the GPUs at this point:
+                # record them with the dW ranges written so far
+                ranges = [(_j64(next(rd), next(rd)), _j64(next(rd), next(rd))) for _ in range(next(rd))]
+                ctx.setdefault("ar", []).append((ranges, list(ctx.get("dw_written", []))))
             else:
                 raise AssertionError(kind)
 
@@ -224,10 +230,11 @@ class Sim:
         _, _, off = self.bufs[self.inj_buf]
         self.ws[off:off + d.size] = d.ravel()
 
-    def backward(self, wt, g, h, hp, sequential=False):
+    def backward(self, wt, g, h, hp, sequential=False, bucketed=False):
         t1 = self.cursor
         ctx = dict(t_a=t1 - h + 1, frames=h, chunk_base=t1 - hp + 1, t1=t1, t0=t1 - hp, w=None, wt=wt, g=g)
-        self.run(self.prog[3 if sequential else 1], ctx)
+        self.run(self.prog[4 if bucketed else (3 if sequential else 1)], ctx)
+        return ctx
 
 
 def flat_weights(prog, W: dict):

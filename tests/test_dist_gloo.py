@@ -116,3 +116,21 @@ def test_two_rank_gradient_exchange_equals_single_process():
             assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
         assert np.abs(w - ref_w).max() <= 1e-12
     assert np.array_equal(results[0][1], results[1][1])  # replicas stay bit-identical
+
+
+def test_bench_spawns_its_own_ranks_without_a_launcher():
+    """`python bench.py --gpus 2` (no torchrun, no WORLD_SIZE) re-launches
+    itself under torch.distributed.run; --dry-setup stops after the rank
+    setup (gloo on CPU) so the launcher logic is tested without GPUs."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--dry-setup"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=repo)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(s) for s in out.stdout.splitlines() if s.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 for d in lines)
+    assert sorted(tuple(d["streams"]) for d in lines) == [(0, 256), (256, 512)]

@@ -15,7 +15,27 @@ from paper_1503_02852_b200.schedule import EngineError, build_program
 from program_sim import Sim, flat_weights, unflat
 
 
-def _run_both(net, S, h, hp, iters, lr, seed, sequential=False, chunk=None, crit=O.CE, hw=None):
+def _check_buckets(net, prog, ctx):
+    """Bucketed backward: every dense edge's gradient range is all-reduced
+    exactly once, after the dW step that wrote it, and never written again."""
+    L = prog.layout
+    covered = np.zeros(L.n_params, dtype=int)
+    for ranges, written in ctx["ar"]:
+        for a, b in ranges:
+            covered[a:b] += 1
+            for c in net.iter_dense():
+                o = L.w_off[c.id]
+                n = net.layer(c.dst).size * net.layer(c.src).size
+                if a <= o < b:
+                    assert (o, o + n) in written, c.id
+    for c in net.iter_dense():
+        o = L.w_off[c.id]
+        n = net.layer(c.dst).size * net.layer(c.src).size
+        assert (covered[o:o + n] == 1).all(), c.id
+    assert len(ctx["dw_written"]) == len(set(ctx["dw_written"]))
+
+
+def _run_both(net, S, h, hp, iters, lr, seed, sequential=False, chunk=None, crit=O.CE, hw=None, bucketed=False):
     cg = condense(net)
     prog = build_program(net, cg, S, h, chunk)
     sim = Sim(prog.words)
@@ -40,7 +60,9 @@ def _run_both(net, S, h, hp, iters, lr, seed, sequential=False, chunk=None, crit
         g = O.backward_window(net, cg, W, st, st.cursor, hw, hp, d)
         sim.set_injection(O.inject_output_error(t, out_s))
         gflat = np.zeros(prog.layout.n_params)
-        sim.backward(wt, gflat, hw, hp, sequential=sequential)
+        ctx = sim.backward(wt, gflat, hw, hp, sequential=sequential, bucketed=bucketed)
+        if bucketed:
+            _check_buckets(net, prog, ctx)
         gs = unflat(prog, net, gflat)
         for cid in g:
             worst = max(worst, normwise(gs[cid], g[cid]))
@@ -60,6 +82,38 @@ def test_program_matches_oracle_on_golden_cases(name, sequential):
                       sequential=sequential, chunk=spec["hp"],
                       crit=spec.get("criterion", O.CE))
     assert worst < 1e-10
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_bucketed_backward_matches_oracle(name):
+    """The multi-GPU backward (per-supernode dW buckets + all-reduce markers,
+    SURVEY §8(e)) computes the same gradients, and every bucket is complete
+    when its all-reduce is issued."""
+    spec = CASES[name]
+    if spec.get("frame_parallel") is False:
+        pytest.skip("bucketed only for the hoisted schedule")
+    net = case_net(name)
+    worst = _run_both(net, spec["S"], spec["h"], spec["hp"], spec["iters"], spec["lr"], spec["seed"],
+                      chunk=spec["hp"], crit=spec.get("criterion", O.CE), bucketed=True)
+    assert worst < 1e-10
+
+
+def test_cfg4_buckets_follow_reverse_topological_order():
+    net = build_stacked_lstm(1024, [1024] * 3, 1024)
+    prog = build_program(net, condense(net), 4, 4, 2)
+    buckets = prog.stats["buckets"]
+    assert len(buckets) == 4  # one before each SCC loop (top layer first), one at the end
+    off = prog.layout.w_off
+
+    def bucket_of(src, dst):
+        o = off[net.find_connection(src, dst).id]
+        return [i for i, bk in enumerate(buckets) if any(a <= o < b for a, b in bk)]
+
+    assert bucket_of("out_prod_2", "out") == [0]       # the output layer's edges first
+    assert bucket_of("cell_2", "in_gate_2") == [1]     # layer 2's SCC before layer 1's loop
+    assert bucket_of("in", "in_gate_0") == [3]         # the bottom layer last
+    total = sum(b - a for bk in buckets for a, b in bk)
+    assert total >= sum(net.layer(c.dst).size * net.layer(c.src).size for c in net.iter_dense())
 
 
 @pytest.mark.parametrize("S,h,hp", [(1, 5, 2), (3, 7, 3), (2, 4, 4), (2, 9, 1)])
