@@ -65,6 +65,7 @@ _SIGS = {
     "rgb_set_tc_precision": ([_I], _I),
     "rgb_set_scc_mode": ([_I], _I),
     "rgb_set_wavefront": ([_I], _I),
+    "rgb_set_frame_loop": ([_I], _I),
     "rgb_gemm_nt": ([_P, _P, _P, _I, _I, _I, _I, _P], _I),
     "rgb_gemm_dw": ([_P, _P, _P, _I, _I, _I, ctypes.c_float, _I, _P], _I),
     "rgb_gemm_nt_tma": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),

@@ -109,6 +109,16 @@ int cuda_rc(cudaError_t e, const char* what);
 bool g_wavefront_active = false;
 bool use_tc(double flops) { return g_gemm_mode == 2 || (g_gemm_mode == 0 && flops >= kTcMinFlops); }
 
+// persistent tensor-core frame loops for large S (try_frame_loop); 1 = on.
+// Off by default: at cfg4 it measured 644k vs 686k frames/s for the per-frame
+// launches with programmatic dependent launch (the per-frame
+// cost is the L2-bound main loop and the latency-bound chain epilogue, not
+// the launches).
+int g_frame_loop = [] {
+  const char* e = getenv("RGB_FRAME_LOOP");
+  return e ? atoi(e) : 0;
+}();
+
 // cross-layer wavefront of the forward section; 1 = on
 int g_wavefront = [] {
   const char* e = getenv("RGB_WAVEFRONT");
@@ -247,6 +257,25 @@ struct rgb_plan {
   std::vector<cudaStream_t> wf_streams;
   std::vector<cudaEvent_t> wf_events;
   int wf_ok[kSections] = {-1, -1, -1, -1, -1};  // per section: structure eligible (cached after the first look)
+  // persistent tensor-core frame loops (launch_tc_frame_loop): per (loop,
+  // ring phase, operands) the per-frame GemmGroup / EwLaunch blocks on the
+  // device (uploaded once from pinned host copies; a CUDA graph replays the
+  // launch with the same blocks) and the loops' grid-barrier words
+  struct FrameLoopBlocks {
+    int ok = 1;  // 0: the loop's shape does not suit the kernel (per-frame launches)
+    GemmGroup* d_groups = nullptr;
+    EwLaunch* d_ew = nullptr;
+    void* h_pinned = nullptr;
+    int n_ew = 0, fuse_ew = 0;
+    double flops = 0;
+  };
+  std::map<std::vector<int64_t>, FrameLoopBlocks> frame_loops;
+  unsigned* fl_bar = nullptr;
+  // blocks are carved from one device + one pinned arena, allocated at the
+  // first (eager) frame loop: a CUDA graph capture may not allocate
+  char* fl_dev = nullptr;
+  char* fl_host = nullptr;
+  size_t fl_cap = 0, fl_used = 0;
   // bucketed gradient exchange (rgb_backward_window_allreduce): the
   // communicator of the running call, its stream and fork/join events
   rgb_comm* comm = nullptr;
@@ -350,6 +379,9 @@ struct rgb_plan {
     if (tcache_pool) cudaFree(tcache_pool);
     for (auto e : wf_events) cudaEventDestroy(e);
     for (auto e : comm_events) cudaEventDestroy(e);
+    if (fl_dev) cudaFree(fl_dev);
+    if (fl_host) cudaFreeHost(fl_host);
+    if (fl_bar) cudaFree(fl_bar);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto q : wf_streams) cudaStreamDestroy(q);
   }
@@ -734,6 +766,68 @@ struct rgb_plan {
     return RGB_OK;
   }
 
+  // one GEMM step (the words after its kind) -> GemmGroup for context c
+  int parse_gemm(Reader& rd, const Ctx& c, GemmGroup& G, int (*seg_cid)[kMaxSegs]) {
+    int rc = RGB_OK;
+    std::memset(&G, 0, sizeof G);
+    G.njobs = rd.next();
+    if (G.njobs < 1 || G.njobs > kMaxJobs) return fail(RGB_ERR_KERNEL, "bad job count");
+    G.rows = c.frames * S;
+    G.ring = ring_for(c);
+    G.tile_start[0] = 0;
+    if ((rc = ensure_weight_maps(c.w, c.wt))) return rc;
+    bool all_tma = !maps.empty();
+    for (int j = 0; j < G.njobs; ++j) {
+      GemmJob& jb = G.job[j];
+      jb.nseg = rd.next();
+      if (jb.nseg < 1 || jb.nseg > kMaxSegs) return fail(RGB_ERR_KERNEL, "bad segment count");
+      for (int s = 0; s < jb.nseg; ++s) {
+        const int ab = rd.next(), ash = rd.next(), cid = rd.next(), trans = rd.next();
+        seg_cid[j][s] = cid;
+        float* a;
+        if ((rc = resolve(c, ab, ash, c.frames, &a))) return rc;
+        if (cid < 0 || cid >= (int)wts.size() || wts[cid].rows == 0)
+          return fail(RGB_ERR_KERNEL, "bad weight %d", cid);
+        const WDesc& wd = wts[cid];
+        jb.seg[s].a = a;
+        jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
+        jb.seg[s].k = trans ? wd.rows : wd.cols;
+        if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
+        const int mi = (int)wmap0() + 8 * cid + (trans ? 4 : 0);
+        if (all_tma && map_ok[ab] && w_maps_ok(cid, trans)) {
+          jb.seg[s].ta = maps_dev + ab;
+          jb.seg[s].tb = maps_dev + mi;
+          jb.seg[s].tblo = nullptr;
+          jb.seg[s].arow = (int)((a - (ws + bufs[ab].off)) / bufs[ab].width);
+        } else {
+          all_tma = false;
+        }
+      }
+      if ((rc = parse_chain(rd, c, true, jb.epi))) return rc;
+      jb.n = jb.epi.width;
+      const int tm = (G.rows + 63) / 64, tn = (jb.n + 63) / 64;
+      G.tiles_n[j] = tn;
+      G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
+    }
+    G.tma = all_tma ? 1 : 0;
+
+    return rd.ok ? RGB_OK : fail(RGB_ERR_KERNEL, "truncated program");
+  }
+
+  // one elementwise step (the words after its kind) -> EwLaunch for context c
+  int parse_ew(Reader& rd, const Ctx& c, EwLaunch& L) {
+    std::memset(&L, 0, sizeof L);
+    L.nchains = rd.next();
+    if (L.nchains < 1 || L.nchains > kMaxChains) return fail(RGB_ERR_KERNEL, "bad chain count");
+    L.rows = c.frames * S;
+    L.ring = ring_for(c);
+    for (int i = 0; i < L.nchains; ++i) {
+      int rc = parse_chain(rd, c, false, L.chain[i]);
+      if (rc) return rc;
+    }
+    return RGB_OK;
+  }
+
   const int* cur_seg_cid = nullptr;  // [kMaxJobs][kMaxSegs] connection ids of the GEMM being parsed
 
   // Id mode: segments whose A operand is the input ring become W^T row
@@ -918,6 +1012,127 @@ struct rgb_plan {
     return rc;
   }
 
+  // A recurrent loop whose body is one GEMM step followed by elementwise
+  // steps runs as ONE persistent tensor-core launch over all its frames
+  // (tma_frame_loop_kernel) when the per-frame GEMM is tensor-core sized.
+  // *handled = false: not eligible, the caller launches frame by frame.
+  int try_frame_loop(const int32_t* body, int64_t len, const Ctx& c, bool reverse, cudaStream_t st, bool* handled) {
+    *handled = false;
+    std::vector<int64_t> starts;
+    for (int64_t i = 0; i < len;) {
+      const int64_t w = step_words(body, i, len);
+      if (w <= 0) return RGB_OK;
+      starts.push_back(i);
+      i += w;
+    }
+    const int nsteps = (int)starts.size();
+    if (nsteps < 1 || nsteps > 3 || body[0] != STEP_GEMM) return RGB_OK;
+    for (int k = 1; k < nsteps; ++k)
+      if (body[starts[k]] != STEP_EW) return RGB_OK;
+    const int n_ew = nsteps - 1;
+    std::vector<int64_t> key = {c.section, (int64_t)(body - c.sec_base), pmod(c.t_a, cap), c.frames,
+                                c.t1 - c.t_a, c.t0 - c.t_a, c.chunk_base - c.t_a, (int64_t)reverse,
+                                (int64_t)(uintptr_t)c.w, (int64_t)(uintptr_t)c.wt, (int64_t)(uintptr_t)c.g,
+                                (int64_t)get_tc_terms()};
+    auto it = frame_loops.find(key);
+    if (it != frame_loops.end() && !it->second.ok) return RGB_OK;
+    if (it == frame_loops.end()) {
+      // build the per-frame blocks (host), check eligibility, upload
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      FrameLoopBlocks fb;
+      fb.n_ew = n_ew;
+      const size_t gbytes = sizeof(GemmGroup) * c.frames, ebytes = sizeof(EwLaunch) * c.frames * n_ew;
+      std::vector<GemmGroup> groups(c.frames);
+      std::vector<EwLaunch> ews((size_t)c.frames * n_ew);
+      int seg_cid[kMaxJobs][kMaxSegs];
+      for (int f = 0; f < c.frames && fb.ok; ++f) {
+        Ctx ci = c;
+        ci.t_a = reverse ? c.t_a + c.frames - 1 - f : c.t_a + f;
+        ci.frames = 1;
+        ci.in_loop = true;
+        Reader rg{body + starts[0] + 1, (nsteps > 1 ? starts[1] : len) - starts[0] - 1};
+        int rc = parse_gemm(rg, ci, groups[f], seg_cid);
+        if (rc) return rc;
+        if (!groups[f].tma) fb.ok = 0;
+        for (int e = 0; e < n_ew; ++e) {
+          Reader re{body + starts[1 + e] + 1, (2 + e < nsteps ? starts[2 + e] : len) - starts[1 + e] - 1};
+          if ((rc = parse_ew(re, ci, ews[(size_t)f * n_ew + e]))) return rc;
+        }
+      }
+      double flops = 0;
+      for (int j = 0; j < groups[0].njobs; ++j) {
+        int64_t ksum = 0;
+        for (int q = 0; q < groups[0].job[j].nseg; ++q) ksum += groups[0].job[j].seg[q].k;
+        flops += 2.0 * groups[0].rows * groups[0].job[j].n * (double)ksum;
+      }
+      fb.flops = flops * c.frames;
+      if (!use_tc(flops) || S < 64) fb.ok = 0;
+      // the elementwise steps run in the epilogue when each is one chain over
+      // the jobs' common width (element-local to a tile spanning every job)
+      fb.fuse_ew = n_ew > 0 && n_ew + groups[0].njobs <= 4;
+      for (int e = 0; e < n_ew && fb.fuse_ew; ++e)
+        fb.fuse_ew = ews[e].nchains == 1 && ews[e].chain[0].width == groups[0].job[0].n;
+      const size_t need = (gbytes + ebytes + 255) & ~size_t(255);
+      if (fb.ok && !fl_dev) {
+        if (cs != cudaStreamCaptureStatusNone) {
+          fb.ok = 0;  // first seen inside a capture: no allocation possible; per-frame launches
+        } else {
+          fl_cap = (size_t)64 << 20;
+          if (cudaMalloc(&fl_dev, fl_cap) != cudaSuccess || cudaMallocHost(&fl_host, fl_cap) != cudaSuccess ||
+              cudaMalloc(&fl_bar, 2 * sizeof(unsigned)) != cudaSuccess ||
+              cudaMemset(fl_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+            return fail(RGB_ERR_CUDA, "frame-loop arena allocation");
+        }
+      }
+      if (fb.ok && fl_used + need > fl_cap) fb.ok = 0;  // arena full: per-frame launches
+      if (fb.ok) {
+        fb.d_groups = reinterpret_cast<GemmGroup*>(fl_dev + fl_used);
+        fb.d_ew = ebytes ? reinterpret_cast<EwLaunch*>(fl_dev + fl_used + gbytes) : nullptr;
+        fb.h_pinned = fl_host + fl_used;
+        fl_used += need;
+        std::memcpy(fb.h_pinned, groups.data(), gbytes);
+        if (ebytes) std::memcpy(static_cast<char*>(fb.h_pinned) + gbytes, ews.data(), ebytes);
+        // enqueued (and, inside a capture, recorded) on the stream; the pinned
+        // source stays alive and unchanged with the cache entry
+        if (cudaMemcpyAsync(fb.d_groups, fb.h_pinned, gbytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            (ebytes && cudaMemcpyAsync(fb.d_ew, static_cast<char*>(fb.h_pinned) + gbytes, ebytes,
+                                       cudaMemcpyHostToDevice, st) != cudaSuccess))
+          return fail(RGB_ERR_CUDA, "frame-loop block upload");
+        fb.ok = 2;  // uploaded; the launch below decides the shape
+        (void)cs;
+      }
+      it = frame_loops.emplace(key, fb).first;
+      if (!fb.ok) return RGB_OK;
+      // first use: the group of frame 0 (host copy) decides the launch shape
+      it->second.ok = 1;
+      GemmGroup g0 = groups[0];
+      const int slot = prof_start(st);
+      const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, n_ew, fb.fuse_ew, c.frames, fl_bar, st);
+      if (lrc < 0) {
+        it->second.ok = 0;
+        return RGB_OK;
+      }
+      note_launch();
+      prof_stop(slot, st, PROF_GEMM_FRAME, fb.flops, 0.0);
+      if (lrc) return fail(RGB_ERR_CUDA, "frame-loop launch: %s", cudaGetErrorString((cudaError_t)lrc));
+      *handled = true;
+      return RGB_OK;
+    }
+    // known loop and phase: launch with the device blocks (frame 0 read back
+    // from the pinned host copy for the launch shape)
+    const FrameLoopBlocks& fb = it->second;
+    const GemmGroup& g0 = *static_cast<const GemmGroup*>(fb.h_pinned);
+    const int slot = prof_start(st);
+    const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, fb.n_ew, fb.fuse_ew, c.frames, fl_bar, st);
+    if (lrc < 0) return RGB_OK;
+    note_launch();
+    prof_stop(slot, st, PROF_GEMM_FRAME, fb.flops, 0.0);
+    if (lrc) return fail(RGB_ERR_CUDA, "frame-loop launch: %s", cudaGetErrorString((cudaError_t)lrc));
+    *handled = true;
+    return RGB_OK;
+  }
+
   cudaEvent_t ev_tmp = nullptr;
   int next_comm_event(cudaEvent_t* out) {
     if (comm_next >= (int)comm_events.size()) {  // (event creation is legal inside a graph capture)
@@ -970,47 +1185,7 @@ struct rgb_plan {
         int seg_cid[kMaxJobs][kMaxSegs];
         cur_seg_cid = &seg_cid[0][0];
         GemmGroup G;
-        std::memset(&G, 0, sizeof G);
-        G.njobs = rd.next();
-        if (G.njobs < 1 || G.njobs > kMaxJobs) return fail(RGB_ERR_KERNEL, "bad job count");
-        G.rows = c.frames * S;
-        G.ring = ring_for(c);
-        G.tile_start[0] = 0;
-        if ((rc = ensure_weight_maps(c.w, c.wt))) return rc;
-        bool all_tma = !maps.empty();
-        for (int j = 0; j < G.njobs; ++j) {
-          GemmJob& jb = G.job[j];
-          jb.nseg = rd.next();
-          if (jb.nseg < 1 || jb.nseg > kMaxSegs) return fail(RGB_ERR_KERNEL, "bad segment count");
-          for (int s = 0; s < jb.nseg; ++s) {
-            const int ab = rd.next(), ash = rd.next(), cid = rd.next(), trans = rd.next();
-            seg_cid[j][s] = cid;
-            float* a;
-            if ((rc = resolve(c, ab, ash, c.frames, &a))) return rc;
-            if (cid < 0 || cid >= (int)wts.size() || wts[cid].rows == 0)
-              return fail(RGB_ERR_KERNEL, "bad weight %d", cid);
-            const WDesc& wd = wts[cid];
-            jb.seg[s].a = a;
-            jb.seg[s].b = (trans ? c.wt : c.w) + wd.off;
-            jb.seg[s].k = trans ? wd.rows : wd.cols;
-            if (bufs[ab].width != jb.seg[s].k) return fail(RGB_ERR_KERNEL, "segment K mismatch (cid %d)", cid);
-            const int mi = (int)wmap0() + 8 * cid + (trans ? 4 : 0);
-            if (all_tma && map_ok[ab] && w_maps_ok(cid, trans)) {
-              jb.seg[s].ta = maps_dev + ab;
-              jb.seg[s].tb = maps_dev + mi;
-              jb.seg[s].tblo = nullptr;
-              jb.seg[s].arow = (int)((a - (ws + bufs[ab].off)) / bufs[ab].width);
-            } else {
-              all_tma = false;
-            }
-          }
-          if ((rc = parse_chain(rd, c, true, jb.epi))) return rc;
-          jb.n = jb.epi.width;
-          const int tm = (G.rows + 63) / 64, tn = (jb.n + 63) / 64;
-          G.tiles_n[j] = tn;
-          G.tile_start[j + 1] = G.tile_start[j] + tm * tn;
-        }
-        G.tma = all_tma ? 1 : 0;
+        if ((rc = parse_gemm(rd, c, G, seg_cid))) return rc;
         if (id_mode && (rc = gather_input_segments(G, c, st))) return rc;
         if (G.njobs == 0) continue;
         double flops = 0, bytes = 0;
@@ -1096,6 +1271,14 @@ struct rgb_plan {
             note_launch();
             prof_stop(slot, st, PROF_SCC, sp.flops_per_frame * c.frames, 0.0);
             if (e != cudaSuccess) return fail(RGB_ERR_CUDA, "persistent SCC launch: %s", cudaGetErrorString(e));
+            rd.i += len;
+            continue;
+          }
+        }
+        if (g_frame_loop && !id_mode && !g_wavefront_active && g_gemm_mode != 1 && c.section >= 0 && c.frames >= 2) {
+          bool handled = false;
+          if ((rc = try_frame_loop(body, len, c, reverse != 0, st, &handled))) return rc;
+          if (handled) {
             rd.i += len;
             continue;
           }
@@ -1281,6 +1464,11 @@ int rgb_abi_version(void) { return RGB_ABI_VERSION; }
 
 int rgb_set_scc_mode(int on) {
   g_scc_mode = on ? 1 : 0;
+  return RGB_OK;
+}
+
+int rgb_set_frame_loop(int on) {
+  g_frame_loop = on ? 1 : 0;
   return RGB_OK;
 }
 

@@ -1679,6 +1679,751 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_const
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent frame loop of a recurrent SCC at large S.  The reference walks
+// the frames of a recurrent supernode one at a time (engine.py:405-413
+// forward, :568-576 backward); the per-frame work here is one grouped NT GEMM
+// (the intra-SCC dense edges, e.g. cell(t-1) -> {in, forget} gates of an
+// LSTM, [S x 1024] x [1024 x 2048] at cfg4) with the fused chain epilogue,
+// optionally followed by elementwise steps (the LSTM cell update).  Launched
+// once per frame that costs a launch, the TMEM / barrier prologue, a cold
+// pipeline and the teardown per frame (~33 us per frame-step at cfg4 with a
+// ~6 us tensor floor).  This kernel runs the whole loop:
+//   * one cooperative launch (all CTAs co-resident; cluster split-K as in the
+//     per-frame kernel), every CTA owns the same output tile (and K split) in
+//     every frame; TMEM, barriers and the pipeline live across frames;
+//   * the weight operand (B) does not depend on the frame: its TMA loads for
+//     frame f+1 stream into free pipeline slots while frame f's epilogue and
+//     the frame barrier run; only the state operand (A) waits for the barrier;
+//   * frame f+1 starts after a grid barrier on frame f's outputs (release:
+//     __threadfence + atomic; acquire + fence.proxy.async before the TMA
+//     loads of A, which read what other SMs stored);
+//   * split-K partial tiles are reduced through DSMEM with mbarrier handshakes
+//     among the epilogue warps (part_ready / read_done), so the producer and
+//     MMA warps never join a per-frame cluster barrier;
+//   * the trailing elementwise steps of a frame run on all CTAs between two
+//     grid barriers.
+// Per-frame operands (segment rows, epilogue / elementwise pointers, ring
+// mirror split) come from a device array of per-frame GemmGroup / EwLaunch
+// blocks built once per (loop, ring phase) by the executor.
+struct FrameLoop {
+  const GemmGroup* frames;  // [nframes], loop order
+  const EwLaunch* ew;       // [nframes * n_ew] or null
+  int nframes, n_ew;
+  int fuse_ew;              // 1: the elementwise steps run in the epilogue (element-local to the tile)
+  int bu;                   // units per job in a tile (the tile's BN = njobs * bu)
+  int prefetch;             // 1: warp 11 prefetches the chains' operands into L2 (off by default)
+  int forward;              // 1: fused chain evaluation with register forwarding (frame_chains_fused)
+  unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
+};
+
+template <int BN>
+struct FCfg {
+  static constexpr int BK = 32;
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // [A raw][B][B_lo] (A hi/lo go to TMEM)
+  static constexpr int EPI_LD = BN + 4;
+  static constexpr int TILE_BYTES = BM * EPI_LD * 4;         // dedicated epilogue staging tile
+  static constexpr int CHAINS = 4;                           // chain slots (jobs, fused elementwise chains)
+  static constexpr int BUDGET = 232448 - 1024 - 512 - CHAINS * kChainBytes - TILE_BYTES;
+  static constexpr int RAW = BUDGET / STAGE_BYTES;
+  static constexpr int TCAP = (512 - BN) / 64;               // A stages of 64 TMEM columns
+  static constexpr int STAGES = RAW < TCAP ? (RAW > 8 ? 8 : RAW) : (TCAP > 8 ? 8 : TCAP);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TILE_BYTES + 1024 + 512 + CHAINS * kChainBytes;
+  static_assert(STAGES >= 2, "frame loop pipeline");
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid barrier over the co-resident CTAs: arrive (one thread per CTA, after
+// the CTA's stores) and wait for generation `target`
+__device__ __forceinline__ void grid_arrive(unsigned* bar, unsigned nblocks) {
+  __threadfence();
+  if (atomicAdd(&bar[0], 1u) == nblocks - 1) {
+    atomicExch(&bar[0], 0u);
+    __threadfence();
+    atomicAdd(&bar[1], 1u);
+  }
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Poll with relaxed loads and a short sleep (an acquire load per poll
+// invalidates the SM's L1 -- measured to slow the epilogue warps' operand
+// loads ~2x while the TMA / prefetch warps wait), acquire once at the end.
+__device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
+  long long t0 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while ((int)(ld_relaxed_u32(bar + 1) - target) < 0) {
+    __nanosleep(100);
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000LL) __trap();  // 4 s: a lost CTA -- fail loudly instead of hanging the GPU
+  }
+  (void)ld_acquire_u32(bar + 1);
+}
+
+#ifdef RGB_FL_TRACE
+__device__ long long g_fl_trace[64][16];  // CTA 0: per frame, globaltimer at the phase boundaries
+__device__ int g_fl_frame;
+__device__ __forceinline__ void fl_mark(int f, int e) {  // SM cycles (globaltimer ticks ~1 us)
+  if (blockIdx.x == 0 && f < 64) g_fl_trace[f][e] = clock64();
+}
+#define FL_MARK(f, e) fl_mark(f, e)
+#else
+#define FL_MARK(f, e)
+#endif
+
+// ---- fused chain evaluation with register forwarding (frame loops) ----
+// The ops of a frame's chains (every job's chain, then the fused elementwise
+// steps) run back to back per element group in one thread.  An op's operand
+// that an earlier op of the same group produced (same pointer: same buffer,
+// frame and shift) is served from a 4-slot register cache instead of a
+// store -> load round trip through global memory (~1 us each, measured with
+// tools/trace_frame_loop.py); every other operand of every op is prefetched
+// into L1 before the first op, so the group pays one memory latency instead
+// of one per op.  Arithmetic per element is exactly ew_apply's.
+template <int R>
+struct FlCache {
+  const float* p[4];
+  float4 v[4][R];
+};
+
+template <int R>
+__device__ __forceinline__ void fl_push(FlCache<R>& c, const float* p, const float4 (&v)[R]) {
+#pragma unroll
+  for (int sl = 3; sl > 0; --sl) {
+    c.p[sl] = c.p[sl - 1];
+#pragma unroll
+    for (int u = 0; u < R; ++u) c.v[sl][u] = c.v[sl - 1][u];
+  }
+  c.p[0] = p;
+#pragma unroll
+  for (int u = 0; u < R; ++u) c.v[0][u] = v[u];
+}
+
+template <int R>
+__device__ __forceinline__ void fl_get(const FlCache<R>& c, const float* p, const int64_t (&e)[R],
+                                       const bool (&ok)[R], float4 dflt, float4 (&out)[R]) {
+  bool hit = false;
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    if (!hit && c.p[sl] == p) {
+      hit = true;
+#pragma unroll
+      for (int u = 0; u < R; ++u) out[u] = c.v[sl][u];
+    }
+  }
+  if (!hit) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) out[u] = ok[u] ? ld4(p, e[u]) : dflt;
+  }
+}
+
+__device__ __forceinline__ void fl_prefetch(const float* p, int64_t e) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p + e));
+}
+
+template <int R>
+__device__ __forceinline__ void fl_prefetch_op(const EwOp& op, const int64_t (&e)[R], const bool (&ok)[R]) {
+  for (int i = 0; i < op.nterm; ++i)
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) fl_prefetch(op.term[i], e[u]);
+  for (int i = 0; i < op.nfac; ++i)
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) fl_prefetch(op.fac[i], e[u]);
+  if (op.y)
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) fl_prefetch(op.y, e[u]);
+  if (op.base)
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) fl_prefetch(op.base, e[u]);
+}
+
+template <int R>
+__device__ __forceinline__ void fl_op(const EwOp& op, int width, const int64_t (&r)[R], const int64_t (&e)[R],
+                                      int j, const bool (&ok)[R], const RingWrite& ring, bool has_acc,
+                                      const float4 (&acc)[R], FlCache<R>& cache) {
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f), one = make_float4(1.f, 1.f, 1.f, 1.f);
+  float4 v[R], t[R];
+  const int kind = op.kind;
+  if (kind == EW_CONST1) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      v[u] = one;
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, one);
+    }
+    fl_push(cache, op.out, v);
+    return;
+  }
+  if (kind == EW_FWD_MUL) {
+    fl_get(cache, op.fac[0], e, ok, zero, v);
+    for (int i = 1; i < op.nfac; ++i) {
+      fl_get(cache, op.fac[i], e, ok, zero, t);
+#pragma unroll
+      for (int u = 0; u < R; ++u) v[u] = mul4(v[u], t[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
+    fl_push(cache, op.out, v);
+    return;
+  }
+  if (has_acc) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = acc[u];
+  } else if (op.base) {
+    fl_get(cache, op.base, e, ok, zero, v);
+  } else {
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = zero;
+  }
+  for (int i = 0; i < op.nterm; ++i) {  // ascending sum, as ew_apply
+    fl_get(cache, op.term[i], e, ok, zero, t);
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[u] = add4(v[u], t[u]);
+  }
+  if (kind == EW_FWD_ADD) {
+    for (int i = 0; i < op.nrank1; ++i) {
+      const float4 w = ld4(op.r1w[i], j);
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const float sv = ok[u] ? op.r1src[i][r[u]] : 0.0f;
+        v[u] = add4(v[u], make_float4(w.x * sv, w.y * sv, w.z * sv, w.w * sv));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      v[u] = make_float4(act_apply(op.act, v[u].x), act_apply(op.act, v[u].y), act_apply(op.act, v[u].z),
+                         act_apply(op.act, v[u].w));
+      if (ok[u]) ring_store4(op.out, e[u], r[u], width, op.out_is_ring, ring, v[u]);
+    }
+    fl_push(cache, op.out, v);
+    return;
+  }
+  // EW_BWD
+  if (op.act == ACT_SIGMOID || op.act == ACT_TANH) {
+    fl_get(cache, op.y, e, ok, zero, t);
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+      v[u] = mul4(v[u], make_float4(act_deriv(op.act, t[u].x), act_deriv(op.act, t[u].y),
+                                    act_deriv(op.act, t[u].z), act_deriv(op.act, t[u].w)));
+  }
+  if (op.inj) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      t[u] = (ok[u] && r[u] >= op.inj_row0) ? ld4(op.inj, (r[u] - op.inj_row0) * width + j) : zero;
+      v[u] = add4(v[u], t[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u)
+    if (ok[u]) st4(op.out, e[u], v[u]);
+  fl_push(cache, op.out, v);
+  if (op.nfac == 0) return;
+  float4 f[kMaxFac][R];
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+    if (i < op.nfac) {
+      fl_get(cache, op.fac[i], e, ok, one, f[i]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < R; ++u) f[i][u] = one;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxFac; ++i) {
+    if (i >= op.nfac || !op.eps[i]) continue;
+    float4 pv[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      pv[u] = v[u];
+#pragma unroll
+      for (int k = 0; k < kMaxFac; ++k)
+        if (k != i) pv[u] = mul4(pv[u], f[k][u]);
+      if (ok[u]) st4(op.eps[i], e[u], pv[u]);
+    }
+    fl_push(cache, op.eps[i], pv);
+  }
+}
+
+// The job chains (op 0 of job j takes tile_s columns [j*bu, (j+1)*bu)) and the
+// fused elementwise chains over rows [r_lo, r_hi) x units [u0, u0 + bu), one
+// element group (R rows x 4 units) per thread at a time.
+template <int R>
+__device__ __forceinline__ void frame_chains_fused(const EwChain* chains, int J, int nch, const RingWrite* rings,
+                                                   const float* tile_s, int ld, int m0, int u0, int bu, int N,
+                                                   int r_lo, int r_hi, int tid) {
+  const int ncols = min(bu, N - u0);
+  if (ncols <= 0 || r_hi <= r_lo || ncols % 4) return;
+  const int g4 = ncols / 4, lanes = 256 / g4 * g4;
+  if (tid >= lanes) return;
+  const int g = tid % g4, layer = tid / g4, layers = lanes / g4;
+  const int j = u0 + 4 * g;
+#pragma unroll 1
+  for (int rb = r_lo + layer; rb < r_hi; rb += layers * R) {
+    int64_t rr[R], e[R];
+    bool ok[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int rl = rb + u * layers;
+      ok[u] = rl < r_hi;
+      rr[u] = m0 + (ok[u] ? rl : r_lo);
+      e[u] = rr[u] * N + j;
+    }
+    for (int c = 0; c < nch; ++c)
+      for (int k = 0; k < chains[c].nops; ++k) fl_prefetch_op<R>(chains[c].op[k], e, ok);
+    FlCache<R> cache;
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) cache.p[sl] = nullptr;
+    for (int c = 0; c < nch; ++c) {
+      float4 a[R];
+      const bool has_acc = c < J;
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int rl = rb + u * layers;
+        a[u] = has_acc ? *reinterpret_cast<const float4*>(tile_s + (ok[u] ? rl : r_lo) * ld + c * bu + 4 * g)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int k = 0; k < chains[c].nops; ++k)
+        fl_op<R>(chains[c].op[k], N, rr, e, j, ok, rings[c], has_acc && k == 0, a, cache);
+    }
+  }
+}
+
+// every chain of the set can take the fused 16-byte path
+__device__ __forceinline__ bool chains_vec_ok(const EwChain* chains, int nch, int N) {
+  for (int c = 0; c < nch; ++c)
+    if (!chain_vec_ok(chains[c], N)) return false;
+  return true;
+}
+
+// A chain over rows [r_lo, r_hi) x units [u0, u0 + bu) of the tile; with
+// `acc`, op 0 takes the staged accumulator columns [c0, c0 + bu) of tile_s.
+// 16-byte groups, R rows per thread and pass (one operand latency per op
+// covers R rows); scalar fallback for unaligned chains.
+template <int R>
+__device__ __forceinline__ void frame_chain(const EwChain& ch, const float* tile_s, int ld, int c0, bool acc,
+                                            int m0, int u0, int bu, int N, int r_lo, int r_hi,
+                                            const RingWrite& ring, int tid) {
+  const int ncols = min(bu, N - u0);
+  if (ncols <= 0 || r_hi <= r_lo) return;
+  if (chain_vec_ok(ch, N) && ncols % 4 == 0) {
+    const int g4 = ncols / 4, lanes_per_layer = 256 / g4 * g4;
+    if (tid >= lanes_per_layer) return;
+    const int g = tid % g4, layer = tid / g4, layers = lanes_per_layer / g4;
+#pragma unroll 1
+    for (int rb = r_lo + layer; rb < r_hi; rb += layers * R) {
+      int64_t rr[R];
+      bool ok[R];
+      float4 a[R];
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int rl = rb + u * layers;
+        ok[u] = rl < r_hi;
+        rr[u] = m0 + (ok[u] ? rl : r_lo);
+        a[u] = acc ? *reinterpret_cast<const float4*>(tile_s + (ok[u] ? rl : r_lo) * ld + c0 + 4 * g)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#ifdef RGB_FL_TRACE
+      for (int k = 0; k < ch.nops; ++k) {
+        ew_apply_vec_variant<R>(ch.op[k], N, rr, u0 + 4 * g, ok, ring, acc && k == 0, a);
+        if (tid == 0 && k < 6) fl_mark(g_fl_frame, 8 + k);
+      }
+#ifdef RGB_FL_TRACE2
+      // the same ops again (idempotent): warm-cache / warm-TLB latency per op
+      for (int k = 0; k < ch.nops; ++k) {
+        ew_apply_vec_variant<R>(ch.op[k], N, rr, u0 + 4 * g, ok, ring, acc && k == 0, a);
+        if (tid == 0 && k < 2) fl_mark(g_fl_frame, 14 + k);
+      }
+#endif
+#else
+      ew_chain_vec<R>(ch, N, rr, u0 + 4 * g, ok, ring, acc, a);
+#endif
+    }
+    return;
+  }
+  for (int e = tid; e < (r_hi - r_lo) * ncols; e += 256) {
+    const int rl = r_lo + e / ncols, cl = e % ncols;
+    const float a = acc ? tile_s[rl * ld + c0 + cl] : 0.0f;
+    for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], N, m0 + rl, u0 + cl, ring, acc && k == 0, a);
+  }
+}
+
+
+// Tiles: 128 stream rows x `bu` units of EVERY job of the GEMM step (the jobs
+// share the A operand, e.g. cell(t-1) feeding the input and forget gates), so
+// one MMA of N = njobs * bu covers them all and the step's elementwise ops
+// (the cell update reading both gates' products) are element-local to the
+// tile: they run in the epilogue instead of behind another grid barrier.
+constexpr int kFrameThreads = 384;  // warps 0-7 convert + epilogue, 8 / 10 TMA, 9 MMA, 11 L2 prefetch
+
+template <int BN>
+__global__ void __launch_bounds__(kFrameThreads, 1)
+    tma_frame_loop_kernel(const __grid_constant__ FrameLoop fl, const __grid_constant__ GemmGroup p) {
+  using C = FCfg<BN>;
+  constexpr int BK = C::BK;
+  constexpr int NST = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* tile_s = reinterpret_cast<float*>(smem + NST * C::STAGE_BYTES);
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE_BYTES + C::TILE_BYTES);
+  uint64_t* conv_full = tma_full + 8;
+  uint64_t* empty = conv_full + 8;
+  uint64_t* done = empty + 8;            // MMA of a frame complete
+  uint64_t* acc_empty = done + 1;        // epilogue has read the accumulator
+  uint64_t* part_ready = acc_empty + 1;  // split-K: partial tiles of the cluster staged
+  uint64_t* read_done = part_ready + 1;  // split-K: peers finished reading this CTA's tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(read_done + 1);
+  EwChain* chains = reinterpret_cast<EwChain*>(smem + NST * C::STAGE_BYTES + C::TILE_BYTES + 512);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int split = blockIdx.x % splits, tile_lin = blockIdx.x / splits;
+  const int csplit = p.csplit ? splits : 1;
+  const int J = p.njobs, bu = fl.bu;
+  const int ublocks = (p.job[0].n + bu - 1) / bu;
+  const int m0 = (tile_lin / ublocks) * BM, u0 = (tile_lin % ublocks) * bu;
+  const int M = p.rows, N = p.job[0].n;
+  const int box = bu == 32 ? 0 : (bu == 64 ? 1 : (bu == 128 ? 2 : 3));
+  int nstages = 0;
+  for (int sg = 0; sg < p.job[0].nseg; ++sg) nstages += (p.job[0].seg[sg].k + BK - 1) / BK;
+  const int s_begin = (int)((long long)split * nstages / splits);
+  nstages = (int)((long long)(split + 1) * nstages / splits) - s_begin;
+  const unsigned nbar = 1u + (fl.fuse_ew ? 0u : (unsigned)fl.n_ew);  // grid barriers per frame
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&tma_full[s], 2);
+      mbar_init(&conv_full[s], kProducers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(acc_empty, 1);
+    mbar_init(part_ready, csplit);
+    mbar_init(read_done, csplit);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // the barrier generation at launch; every CTA reads it before its first
+  // arrival, and no barrier completes before every CTA arrived
+  const unsigned gen0 = *reinterpret_cast<volatile unsigned*>(fl.bar + 1);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (csplit > 1) cluster_sync();
+  else __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 11) {
+    if (!fl.prefetch) goto tail;
+    // ---- L2 prefetch of frame f's epilogue operands (the chains' inputs that
+    // do not come from the accumulator: hoisted partials, gate activations,
+    // delayed state, co-factors, ...) while the main loop runs: the chains
+    // are latency-bound on these loads (~1-2 us per op from HBM)
+    for (int f = 0; f < fl.nframes; ++f) {
+      if (f > 0) grid_wait(fl.bar, gen0 + (unsigned)f * nbar);
+      const GemmGroup& pf = fl.frames[f];
+      const int rlo = csplit > 1 ? split * BM / csplit : 0, rhi = min(csplit > 1 ? (split + 1) * BM / csplit : BM, M - m0);
+      const int bytes = min(bu, N - u0) * 4;
+      if (bytes <= 0 || (bytes & 15)) continue;
+      const int nch = J + (fl.fuse_ew ? fl.n_ew : 0);
+      int slot = 0;
+      for (int c = 0; c < nch; ++c) {
+        const EwChain& ch = c < J ? pf.job[c].epi : fl.ew[(size_t)f * fl.n_ew + (c - J)].chain[0];
+        for (int k = 0; k < ch.nops; ++k) {
+          const EwOp& o = ch.op[k];
+          const float* ptrs[kMaxTerms + kMaxFac + 2];
+          int np = 0;
+          for (int i = 0; i < o.nterm; ++i) ptrs[np++] = o.term[i];
+          for (int i = 0; i < o.nfac; ++i) ptrs[np++] = o.fac[i];
+          if (o.y) ptrs[np++] = o.y;
+          if (o.base) ptrs[np++] = o.base;
+          for (int i = 0; i < np; ++i) {
+            for (int rr = rlo; rr < rhi; ++rr, ++slot) {
+              if ((slot & 31) != lane) continue;
+              const float* a = ptrs[i] + ((int64_t)(m0 + rr) * N + u0);
+              if (reinterpret_cast<uintptr_t>(a) & 15) continue;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 8 || warp == 10) {
+    if (lane == 0) {
+      // ---- TMA: warp 8 loads the state operand A (after the frame barrier),
+      // warp 10 the weights B of every job (frame independent: runs ahead)
+      const bool load_a = warp == 8;
+      int g = 0;
+      for (int f = 0; f < fl.nframes; ++f) {
+        const GemmGroup& pf = fl.frames[f];
+        if (load_a && f > 0) {
+          grid_wait(fl.bar, gen0 + (unsigned)f * nbar);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        if (load_a) FL_MARK(f, 0);
+        int seg = 0, k0 = 0;
+        for (int skip = s_begin; skip > 0;) {
+          const int ns = (pf.job[0].seg[seg].k + BK - 1) / BK;
+          if (skip >= ns) {
+            skip -= ns;
+            ++seg;
+          } else {
+            k0 = skip * BK;
+            skip = 0;
+          }
+        }
+        for (int it = 0; it < nstages; ++it, ++g) {
+          const int s = g % NST;
+          mbar_wait(&empty[s], ((g / NST) & 1) ^ 1);
+          uint8_t* base = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
+          if (load_a) {
+            tma_load_2d(base, pf.job[0].seg[seg].ta, k0, pf.job[0].seg[seg].arow + m0, &tma_full[s]);
+          } else {
+            for (int j = 0; j < J; ++j)  // job j's bu weight rows land at rows [j*bu, (j+1)*bu) of B
+              tma_load_2d(base + C::A_BYTES + j * bu * 128, map_at(pf.job[j].seg[seg].tb, box), k0, u0,
+                          &tma_full[s]);
+          }
+          k0 += BK;
+          if (k0 >= pf.job[0].seg[seg].k) {
+            k0 = 0;
+            ++seg;
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ---- MMA issuer: A hi / lo from TMEM, B from shared memory ----
+      const uint32_t idesc = idesc_tf32(BM, BN, 0, 0);
+      const bool split3 = p.terms != 1;
+      int g = 0;
+      for (int f = 0; f < fl.nframes; ++f) {
+        if (f > 0) mbar_wait(acc_empty, (f - 1) & 1);
+        for (int it = 0; it < nstages; ++it, ++g) {
+          const int s = g % NST;
+          mbar_wait(&conv_full[s], (g / NST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t b_hi = smem_u32(smem + s * C::STAGE_BYTES) + C::A_BYTES, b_lo = b_hi + C::B_BYTES;
+          const uint32_t ta_hi = tmem + BN + 64 * s, ta_lo = ta_hi + 32;
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint64_t dbh = smem_desc(b_hi + j * 32, 16, 1024, 2), dbl = smem_desc(b_lo + j * 32, 16, 1024, 2);
+            const uint32_t acc0 = (it > 0 || j > 0) ? 1u : 0u;
+            if (split3) {
+              mma_tf32_ta(tmem, ta_lo + 8 * j, dbh, idesc, acc0);
+              mma_tf32_ta(tmem, ta_hi + 8 * j, dbl, idesc, 1u);
+            }
+            mma_tf32_ta(tmem, ta_hi + 8 * j, dbh, idesc, split3 ? 1u : acc0);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(done);
+      }
+    }
+  } else {
+    // ---- warps 0-7: converters, then per frame the epilogue and the
+    // elementwise steps ----
+    const int tid = threadIdx.x;
+    const int quarter = warp & 3, kh = warp >> 2, r = quarter * 32 + lane;
+    int g = 0;
+    for (int f = 0; f < fl.nframes; ++f) {
+      const GemmGroup& pf = fl.frames[f];
+      for (int it = 0; it < nstages; ++it, ++g) {
+        const int s = g % NST;
+        mbar_wait(&tma_full[s], (g / NST) & 1);
+        uint8_t* base = smem + s * C::STAGE_BYTES;
+        {
+          const uint8_t* arow = base + r * 128;
+          float hi[16], lo[16];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = kh * 4 + cc;
+            const float4 x = *reinterpret_cast<const float4*>(arow + ((c ^ (r & 7)) * 16));
+            hi[4 * cc] = x.x, hi[4 * cc + 1] = x.y, hi[4 * cc + 2] = x.z, hi[4 * cc + 3] = x.w;
+          }
+          if (p.terms != 1) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) lo[q] = tf32_residual(hi[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) hi[q] = tf32_rna(hi[q]);
+          }
+          const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + BN + 64 * s + 16 * kh;
+          tmem_st16(ta, hi);
+          if (p.terms != 1) tmem_st16(ta + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        }
+        if (p.terms != 1) {
+          const float4* b_hi = reinterpret_cast<const float4*>(base + C::A_BYTES);
+          float4* b_lo = reinterpret_cast<float4*>(base + C::A_BYTES + C::B_BYTES);
+          for (int q = tid; q < C::B_BYTES / 16; q += kProducers) {
+            const float4 x = b_hi[q];
+            b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+          }
+        } else {
+          round_tf32_inplace(base + C::A_BYTES, C::B_BYTES, tid, kProducers);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv_full[s]);
+      }
+      // ---- epilogue of frame f ----
+      for (int j = 0; j < J; ++j) stage_chain(&chains[j], pf.job[j].epi, tid, 256);
+      if (fl.fuse_ew)
+        for (int e = 0; e < fl.n_ew; ++e) stage_chain(&chains[J + e], fl.ew[(size_t)f * fl.n_ew + e].chain[0], tid, 256);
+      if (csplit > 1 && f > 0) mbar_wait_cluster(read_done, (f - 1) & 1);  // peers done with tile_s
+      mbar_wait(done, f & 1);
+      if (tid == 0) FL_MARK(f, 1);
+      // acquire the frame barrier the A loads waited on: the chains read
+      // operands other SMs stored in earlier frames (no stale L1 lines)
+      if (f > 0) (void)ld_acquire_u32(fl.bar + 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      {  // accumulator -> tile_s (warp w: TMEM lane quarter w%4, column half w/4)
+        const int half = warp >> 2, r_loc = quarter * 32 + lane;
+        for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
+          float v[16];
+          tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc, v);
+          float4* dst = reinterpret_cast<float4*>(tile_s + r_loc * C::EPI_LD + cc);
+          dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+          dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+          dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+          dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tid == 0) mbar_arrive(acc_empty);
+      if (tid == 0) FL_MARK(f, 2);
+      int r_lo = 0, r_hi = BM;
+      if (csplit > 1) {
+        // this CTA sums rows [r_lo, r_hi) of the cluster's partial tiles in split order
+        if (tid < csplit) mbar_arrive_cluster(part_ready, (uint32_t)tid);
+        mbar_wait_cluster(part_ready, f & 1);
+        r_lo = split * BM / csplit;
+        r_hi = (split + 1) * BM / csplit;
+        // every remote load of a batch is issued before the first is used
+        // (a DSMEM round trip is ~200 cycles; serial loads made this 3.5 us)
+        constexpr int G4 = BN / 4;
+        const int nq = (r_hi - r_lo) * G4;
+        for (int q0 = tid; q0 < nq; q0 += 256 * 8) {
+          float4 a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = q0 + 256 * i;
+            const int off = (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4;
+            a[i] = q < nq ? ld_dsmem4(tile_s + off, 0u) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int k = 1; k < csplit; ++k) {
+            float4 b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int q = q0 + 256 * i;
+              const int off = (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4;
+              b[i] = q < nq ? ld_dsmem4(tile_s + off, (uint32_t)k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = add4(a[i], b[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = q0 + 256 * i;
+            if (q < nq) *reinterpret_cast<float4*>(tile_s + (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4) = a[i];
+          }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (tid < csplit) mbar_arrive_cluster(read_done, (uint32_t)tid);
+      }
+      if (tid == 0) FL_MARK(f, 3);
+#ifdef RGB_FL_TRACE
+      if (tid == 0 && blockIdx.x == 0) g_fl_frame = f;
+#endif
+      const int rows_hi = min(r_hi, M - m0);
+      const int nch = J + (fl.fuse_ew ? fl.n_ew : 0);
+      if (fl.forward && chains_vec_ok(chains, nch, N) && min(bu, N - u0) % 4 == 0) {
+        RingWrite rings[4];
+        for (int c = 0; c < nch; ++c) rings[c] = c < J ? pf.ring : fl.ew[(size_t)f * fl.n_ew + (c - J)].ring;
+        frame_chains_fused<2>(chains, J, nch, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid);
+      } else {
+        for (int j = 0; j < J; ++j)
+          frame_chain<4>(chains[j], tile_s, C::EPI_LD, j * bu, true, m0, u0, bu, N, r_lo, rows_hi, pf.ring, tid);
+        if (fl.fuse_ew) {
+          // the step's elementwise ops read the job chains' outputs at the same
+          // (row, unit): visible to the CTA after the barrier
+          for (int e = 0; e < fl.n_ew; ++e) {
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            frame_chain<4>(chains[J + e], tile_s, C::EPI_LD, 0, false, m0, u0, bu, N, r_lo, rows_hi,
+                           fl.ew[(size_t)f * fl.n_ew + e].ring, tid);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tid == 0) FL_MARK(f, 4);
+      if (tid == 0) grid_arrive(fl.bar, gridDim.x);
+      // ---- unfused elementwise steps of frame f (all CTAs, between grid barriers) ----
+      for (int e = 0; e < (fl.fuse_ew ? 0 : fl.n_ew); ++e) {
+        const EwLaunch& L = fl.ew[(size_t)f * fl.n_ew + e];
+        if (tid == 0) grid_wait(fl.bar, gen0 + (unsigned)f * nbar + 1u + (unsigned)e);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        (void)ld_acquire_u32(fl.bar + 1);  // every thread: acquire before reading other SMs' stores
+        if (tid == 0) FL_MARK(f, 5);
+        for (int c = 0; c < L.nchains; ++c) {
+          stage_chain(&chains[0], L.chain[c], tid, 256);
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const EwChain& ch = chains[0];
+          if (chain_vec_ok(ch, ch.width)) {
+            const uint32_t w4 = (uint32_t)(ch.width / 4);
+            const uint32_t nq = (uint32_t)L.rows * w4;
+            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint32_t q = blockIdx.x * 256u + tid; q < nq; q += gridDim.x * 256u) {
+              const uint32_t r32 = q / w4;
+              const int64_t rr[1] = {(int64_t)r32};
+              const bool ok[1] = {true};
+              const float4 acc[1] = {zero};
+              ew_chain_vec<1>(ch, ch.width, rr, (int)(q - r32 * w4) * 4, ok, L.ring, false, acc);
+            }
+          } else {
+            const int64_t total = (int64_t)L.rows * ch.width;
+            for (int64_t q = (int64_t)blockIdx.x * 256 + tid; q < total; q += (int64_t)gridDim.x * 256) {
+              const int64_t rr = q / ch.width;
+              const int j = (int)(q - rr * ch.width);
+              for (int k = 0; k < ch.nops; ++k) ew_apply(ch.op[k], ch.width, rr, j, L.ring, false, 0.0f);
+            }
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+        if (tid == 0) FL_MARK(f, 6);
+        if (tid == 0) grid_arrive(fl.bar, gridDim.x);
+      }
+    }
+  }
+tail:
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (csplit > 1) cluster_sync();  // peers' last DSMEM reads of this CTA's tile are done
+  else __syncthreads();
+  if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // Widest N tile that still gives most of the 148 SMs a tile.
 template <class F>
 int pick_bn(F tiles_for) {
@@ -1930,6 +2675,103 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   return 2;
 }
 
+
+// Persistent frame loop (tma_frame_loop_kernel): -1 when the loop's GEMM step
+// does not suit it (the caller then launches per frame), else a CUDA status.
+// The jobs must share their A segments and width (tiles span every job);
+// the tile width per job (bu) and the K split are chosen so that 96..148 CTAs
+// run, preferring no split (no DSMEM reduction).  fuse_ew: the elementwise
+// steps are element-local over the jobs' width and run in the epilogue.
+int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const EwLaunch* d_ew, int n_ew,
+                         int fuse_ew, int nframes, unsigned* bar, cudaStream_t s) {
+  GemmGroup p = g0;
+  p.terms = g_tc_terms;
+  if (!p.tma || p.njobs < 1 || p.njobs > 4) return -1;
+  const int W = p.job[0].n, J = p.njobs;
+  for (int j = 1; j < J; ++j) {
+    if (p.job[j].n != W || p.job[j].nseg != p.job[0].nseg) return -1;
+    for (int q = 0; q < p.job[0].nseg; ++q)
+      if (p.job[j].seg[q].a != p.job[0].seg[q].a || p.job[j].seg[q].k != p.job[0].seg[q].k) return -1;
+  }
+  const int mt = (p.rows + tc::BM - 1) / tc::BM;
+  static int forced_bu = -1, forced_split = -1;  // RGB_FL_BU / RGB_FL_SPLIT: experiments
+  if (forced_bu < 0) {
+    const char* e = getenv("RGB_FL_BU");
+    forced_bu = e ? atoi(e) : 0;
+    e = getenv("RGB_FL_SPLIT");
+    forced_split = e ? atoi(e) : 0;
+  }
+  // Tile width first: the main loop is bound by L2 -> SM operand traffic
+  // (A is re-read once per unit block, B once per 128-row block), so the
+  // widest tile (J * bu = 128) wins, then the smallest K split that still
+  // occupies >= 96 SMs (tools/trace_frame_loop.py, cfg4: forward J=2 bu=64
+  // split 2, backward J=1 bu=128 split 4; bu=32 without a split was 1.7x
+  // slower in the main loop).
+  int bu = 0, sp = 1;
+  for (int cand : {128, 64, 32}) {
+    if (forced_bu && cand != forced_bu) continue;
+    if (J * cand > 128 || J * cand < 32) continue;
+    for (int split : {1, 2, 4}) {
+      if (forced_split && split != forced_split) continue;
+      const int ctas = mt * ((W + cand - 1) / cand) * split;
+      if (ctas >= (forced_bu || forced_split ? 1 : 96) && ctas <= 148) {
+        bu = cand;
+        sp = split;
+        break;
+      }
+    }
+    if (bu) break;
+  }
+  if (!bu || (sp > 1 && !csplit_enabled())) return -1;
+  const int BN = J * bu;
+  p.splits = sp;
+  p.csplit = sp > 1 ? 1 : 0;
+  p.pair = 0;
+  const int blocks = mt * ((W + bu - 1) / bu) * sp;
+  static int prefetch = -1;  // RGB_FL_PREFETCH=0: no L2 prefetch of the chains' operands (experiments)
+  if (prefetch < 0) {
+    const char* e = getenv("RGB_FL_PREFETCH");
+    prefetch = e ? atoi(e) != 0 : 0;  // off: 1 measured 554k -> 418k frames/s (the bulk prefetches delay the TMA loads)
+  }
+  static int fwd = -1;  // RGB_FL_FORWARD=0: chains through global memory (experiments)
+  if (fwd < 0) {
+    const char* e = getenv("RGB_FL_FORWARD");
+    fwd = e ? atoi(e) != 0 : 0;  // off: the register-forwarding evaluator spills (168-register cap) and measured slower
+  }
+  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, bar};
+  auto launch = [&](auto kernel, int smem) -> int {
+    static bool bad = false;  // cooperative cluster launches unsupported: stay per-frame
+    if (bad) return -1;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(tc::kFrameThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = sp;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = sp > 1 ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, fl, p);
+    if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported || e == cudaErrorCooperativeLaunchTooLarge) {
+      cudaGetLastError();
+      bad = e != cudaErrorCooperativeLaunchTooLarge;
+      return -1;
+    }
+    return (int)e;
+  };
+  if (BN == 128) return launch(tc::tma_frame_loop_kernel<128>, tc::FCfg<128>::SMEM);
+  if (BN == 64) return launch(tc::tma_frame_loop_kernel<64>, tc::FCfg<64>::SMEM);
+  if (BN == 32) return launch(tc::tma_frame_loop_kernel<32>, tc::FCfg<32>::SMEM);
+  if (BN == 96) return launch(tc::tma_frame_loop_kernel<96>, tc::FCfg<96>::SMEM);
+  return -1;
+}
+
 void launch_tc_gemm_dw(DwGroup p, cudaStream_t s) {
   p.terms = g_tc_terms;
   const bool pair = p.tma && wide_pair_enabled() && !getenv("RGB_TC_BN");
@@ -1990,6 +2832,11 @@ void set_tc_config(int pair, int persist, int csplit) {
 }
 }  // namespace rgb
 
+#ifdef RGB_FL_TRACE
+extern "C" int rgb_exp_fl_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, rgb::tc::g_fl_trace, sizeof(rgb::tc::g_fl_trace)) == cudaSuccess ? 0 : 3;  // [64][16]
+}
+#endif
 #ifdef RGB_EXP_TRACE
 extern "C" int rgb_exp_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, rgb::tc::g_trace, sizeof(rgb::tc::g_trace)) == cudaSuccess ? 0 : 3;  // [6][1024]

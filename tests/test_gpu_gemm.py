@@ -423,3 +423,44 @@ def test_cfg4_shape_tf32_mode(_tf32):
     worst = run_pair(P.build_stacked_lstm(1024, [1024, 1024], 1024), 256, 32, 16, 3, 1e-3, 6, loss_tol=1e-2)
     print(f"cfg4-shape TF32 step error {worst:.2e}")
     assert worst < TF32_STEP_BOUND
+
+
+@pytest.mark.parametrize("S", [128, 256])
+def test_persistent_frame_loop_matches_oracle(S):
+    """The persistent tensor-core frame loop (rgb_set_frame_loop(1): one
+    cooperative launch per recurrent loop, grid barrier per frame, split-K
+    through DSMEM, the LSTM cell update fused into the epilogue) against the
+    oracle, with every delta / eps / dW compared, and through CUDA-graph replay
+    bit for bit equal to its eager steps."""
+    from test_gpu_engine import run_pair
+    L = _lib.lib()
+    _lib.check(L.rgb_set_frame_loop(1))
+    _lib.check(L.rgb_set_wavefront(0))  # (the wavefront runs frame loops per block, per-frame launches)
+    n0 = ctypes.c_int64()
+    _lib.check(L.rgb_launch_count(ctypes.byref(n0)))
+    try:
+        assert run_pair(P.build_stacked_lstm(256, [512, 512], 256), S, 16, 8, 3, 1e-3, 7) < 1e-4
+        n1 = ctypes.c_int64()
+        _lib.check(L.rgb_launch_count(ctypes.byref(n1)))
+        # 3 iterations x (2 forward + 2 backward loops): the per-frame schedule would
+        # launch >= 8 + 16 kernels per loop pair; the frame loops keep it well below
+        assert n1.value - n0.value < 3 * 60
+        net = P.build_stacked_lstm(128, [512, 512], 128)
+        cfg = P.TrainConfig(h=16, h_prime=8, lr=0.01, iterations=1)
+        wa, wb = P.Weights.init(net, 2), P.Weights.init(net, 2)
+        ta, tb = P.Trainer(net, wa, S, cfg), P.Trainer(net, wb, S, cfg)
+        tb.enable_graphs()
+        gx, gt = tb.graph_inputs()
+        rng = np.random.default_rng(3)
+        for _ in range(5):
+            x = torch.tensor(rng.uniform(-1, 1, size=(8 * S, 128)), dtype=torch.float32, device="cuda")
+            t = torch.tensor(rng.integers(0, 128, size=8 * S), device="cuda")
+            ta.step(x, t)
+            gx.copy_(x)
+            gt.copy_(t)
+            tb.step_graphed()
+            assert ta.loss() == tb.loss()
+        assert torch.equal(wa.flat, wb.flat)
+    finally:
+        _lib.check(L.rgb_set_frame_loop(0))
+        _lib.check(L.rgb_set_wavefront(1))

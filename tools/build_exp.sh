@@ -6,4 +6,4 @@ cd "$(dirname "$0")/../paper_1503_02852_b200"
 name=$1; shift
 mkdir -p ../tools/_exp
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared "$@" \
-  -o ../tools/_exp/$name.so csrc/rgb_kernels.cu csrc/rgb_tc_gemm.cu csrc/rgb_scc.cu csrc/rgb_plan.cu csrc/rgb_prof.cu
+  -o ../tools/_exp/$name.so csrc/rgb_kernels.cu csrc/rgb_tc_gemm.cu csrc/rgb_scc.cu csrc/rgb_plan.cu csrc/rgb_prof.cu csrc/rgb_comm.cu -ldl
