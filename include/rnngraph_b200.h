@@ -158,7 +158,8 @@ int rgb_reset_stream(rgb_plan* plan, int stream_index, void* stream);
 
 /* Read-only view of one schedule buffer over frames [t_lo, t_hi] (frame-major
  * rows of `width` floats, contiguous): activation rings (layer y, edge z) at
- * the current cursor, or the error buffers of the LAST backward window -- the
+ * the current cursor, or the error buffers of the backward window that ended
+ * at the current cursor (the last rgb_backward_window or its replay) -- the
  * per-layer deltas and the per-edge eps of multiplicative destinations that
  * the reference computes as locals of backward_window (engine.py:512-566).
  * Buffer ids come from the program's buffer table (schedule.Layout). */

@@ -1997,13 +1997,17 @@ int rgb_window_view(const rgb_plan* p, int buffer, int64_t t_lo, int64_t t_hi, c
   if (buffer < 0 || buffer >= (int)p->bufs.size() || t_hi < t_lo) return fail(RGB_ERR_KERNEL, "bad buffer or frame range");
   const BufDesc& b = p->bufs[buffer];
   if (b.kind == BUF_WIN && p->last_t1 < 0) return fail(RGB_ERR_ENGINE, "no backward window has run on this plan");
-  if (b.kind == BUF_WIN && t_lo <= p->last_t1 - p->hmax)
+  if (b.kind == BUF_WIN && (t_lo <= p->cursor - p->hmax || t_hi > p->cursor))
     return fail(RGB_ERR_ENGINE, "frames [%lld, %lld] outside the last window (%lld, %lld]", (long long)t_lo,
-                (long long)t_hi, (long long)(p->last_t1 - p->hmax), (long long)p->last_t1);
+                (long long)t_hi, (long long)(p->cursor - p->hmax), (long long)p->cursor);
   if (b.kind == BUF_CHUNK) return fail(RGB_ERR_KERNEL, "chunk buffers have no frame view");
+  // the window buffers hold the backward window that ended at the cursor
+  // (the last rgb_backward_window call, or its CUDA-graph replay: a replay
+  // does not pass through this host code, but always ends at the cursor the
+  // caller then sets)
   Ctx c;
   c.t_a = t_lo;
-  c.t1 = p->last_t1;
+  c.t1 = p->cursor;
   c.frames = (int)(t_hi - t_lo + 1);
   float* q;
   int rc = p->resolve(c, buffer, 0, c.frames, &q);

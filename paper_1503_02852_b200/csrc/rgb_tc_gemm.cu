@@ -1535,18 +1535,27 @@ constexpr int kMaxStagesPerAcc = 16;
 
 // stages per accumulation chunk for a launch whose tiles are at most
 // `max_stages` deep: 0 (unchunked) when the whole K fits the bound, else
-// 8 (3xTF32) / 24 (TF32) -- <= 96 truncating accumulations per chunk.
+// 8 / 16 (3xTF32 dW / NT) or 24 / 48 (TF32) -- <= 96 / 192 truncating
+// accumulations per chunk.
 // RGB_TC_KC overrides (experiments).
-int chunk_stages(int terms, int max_stages) {
-  static int forced = -1;
+int chunk_stages(int terms, int max_stages, bool dw) {
+  static int forced = -1, forced_nt = -1;
   if (forced < 0) {
     const char* e = getenv("RGB_TC_KC");
     forced = e ? atoi(e) : 0;
+    e = getenv("RGB_TC_KC_NT");
+    forced_nt = e ? atoi(e) : 0;
   }
   const int per_acc = terms == 1 ? (max_stages + 2) / 3 : max_stages;
   if (per_acc <= kMaxStagesPerAcc) return 0;
+  if (!dw && forced_nt > 0) return forced_nt;
   if (forced > 0) return forced;
-  return terms == 1 ? 24 : 8;
+  // dW (K = h*S, 16384 at cfg4) 8 stages per chunk; the NT GEMMs (K <= 4096)
+  // 16: cfg4 after 4 training steps 5.5e-5 worst normwise vs 4.3e-5 with 8
+  // everywhere and 8.6e-5 with 32 for NT (tools/diag_parity.py), at 702k vs
+  // 683k / 720k frames/s
+  if (terms == 1) return dw ? 24 : 48;
+  return dw ? 8 : 16;
 }
 
 template <int BN, bool IS_DW, bool PAIR, class P>
@@ -1578,7 +1587,7 @@ void launch_persistent(const P& p, int ntiles, int max_stages, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, p, ntiles, chunk_stages(p.terms, max_stages));
+  cudaLaunchKernelEx(&cfg, k, p, ntiles, chunk_stages(p.terms, max_stages, IS_DW));
 }
 
 template <int BN, bool IS_DW, bool PAIR, class P>
