@@ -321,7 +321,49 @@ def measure_tf32(P, L, cfg, S, value_fp32, steps=10):
     v = hp * S / (ms / 1000.0)
     return {"gemm_precision": "tf32 (1 tcgen05 product per k-step)", "frames_per_s": v, "ms_per_step": ms,
             "speedup_vs_3xtf32": v / value_fp32, "steps": steps,
-            "bound": "normwise 2e-2 vs the float64 oracle per training step (tests/test_gpu_gemm.py)"}
+            "bound": "normwise 2e-3 vs the float64 oracle per training step, operands rounded to nearest tf32 "
+                     "(tests/test_gpu_gemm.py, BASELINE.md §5)"}
+
+
+def measure_tf32_peak(seconds=2.0):
+    """Dense TF32 tensor throughput of this GPU, measured like MEASURED_PEAKS.json's
+    bf16 figure: cuBLAS fp32 matmul with TF32 allowed, 8192^3 (2*N^3 FLOP),
+    best of 10 (burst) and back to back for ~`seconds` (sustained).  The fp32
+    (3xTF32) ceiling of the tensor-core GEMMs is a third of it."""
+    import torch
+    n = 8192
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        c = torch.empty(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        reps = max(1, int(seconds * 1000.0 / best))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        sus = e0.elapsed_time(e1) / reps
+        del a, b, c
+        torch.cuda.empty_cache()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    flop = 2.0 * n ** 3
+    return {"burst_tflops": flop / best / 1e9, "sustained_tflops": flop / sus / 1e9,
+            "how": "cuBLAS fp32 matmul, TF32 allowed, 8192^3: best of 10 / back to back ~2 s (CUDA events)"}
 
 
 def recurrent_summary(prof, steps, net, hp, h):
@@ -472,19 +514,21 @@ def run_ours(args, cfg):
         achieved = p["bytes"] / p["launches"] / per_launch_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm}
     traffic = None
-    tpath = os.path.join(HERE, "profiles", "r01_traffic.json")
+    tpath = os.path.join(HERE, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):  # committed ncu --set full capture (dram read + write per launch)
         with open(tpath) as f:
             traffic = json.load(f).get(top, {}).get("dram_bytes_per_launch")
     roof.update({"traffic": traffic, "kernel": top, "peak_source": peak_src + " (MEASURED_PEAKS.json)",
                  "share_of_step": p["ms"] / sum(v["ms"] for v in prof.values())})
     if roof["bound"] == "tensor":
-        # fp32 work on tensor cores is 3xTF32: three tf32 MMAs (half the bf16
-        # rate) per fp32 product, so the ceiling for this dtype is peak / 6
+        # fp32 work on tensor cores is 3xTF32: three kind::tf32 MMAs per fp32
+        # product, so this dtype's ceiling is the MEASURED dense TF32 rate / 3
         terms = 1 if args.tc_precision == "tf32" else 3
+        tf32 = measure_tf32_peak()
         roof["fp32_emulation"] = "3xTF32" if terms == 3 else "TF32"
-        roof["fp32_ceiling"] = tflops / (2.0 * terms)
-        roof["frac_of_fp32_ceiling"] = achieved / (tflops / (2.0 * terms))
+        roof["tf32_peak_measured"] = tf32
+        roof["fp32_ceiling"] = tf32["sustained_tflops"] / terms
+        roof["frac_of_fp32_ceiling"] = achieved / roof["fp32_ceiling"]
     F_iter = algorithmic_flops(net, S_total, h, hp)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
