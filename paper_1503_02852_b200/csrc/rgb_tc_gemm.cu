@@ -1067,15 +1067,17 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // blocks = CTAs (2 per pair tile when PAIR)
 // ---------------------------------------------------------------------------
 // Persistent form of the TMA kernel for launches of several waves: each CTA
-// (pair) walks output tiles blockIdx, blockIdx + grid, ...; the accumulator is
-// double-buffered in TMEM so that 4 dedicated epilogue warps drain tile i
-// while the producers, converters and MMA issuer already run tile i+1 (in the
-// one-tile kernel the epilogue was ~25% of every multi-wave launch).
-//   warps 0-7 converters, 8 TMA A, 9 MMA, 10 TMA B, 11-14 epilogue.
-// Barriers: per stage tma_full / conv_full / empty (as above), per running
-// sum r_full (MMA commit -> epilogue) / r_empty (epilogue -> MMA), per chunk
-// accumulator x_full / x_empty.  The epilogue stages 16-column chunks of the
-// tile in a private smem slice (TMEM -> smem -> coalesced 16-byte row walk).
+// (pair) walks output tiles blockIdx, blockIdx + grid, ...; two chunk
+// accumulators in TMEM let 8 dedicated epilogue warps fold / drain one while
+// the producers, converters and MMA issuer fill the other (in the one-tile
+// kernel the epilogue was ~25% of every multi-wave launch).
+//   warps 0-3 converters, 4-11 epilogue (two groups), 12 TMA A, 13 MMA, 14 TMA B;
+//   setmaxnreg moves registers from the converter / producer warp groups to
+//   the epilogue, whose threads hold the tile's running sum (BN/2 floats).
+// Barriers: per stage tma_full / conv_full / empty (as above), per chunk
+// accumulator x_full (MMA commit -> epilogue) / x_empty (epilogue -> MMA).
+// The epilogue stages 16-column chunks of the tile in a private smem slice
+// (registers -> smem -> coalesced 16-byte row walk).
 //
 // K-chunked accumulation.  tcgen05 adds each k-step's products into the fp32
 // TMEM accumulator with truncation (round toward zero) in the alignment, so
@@ -1084,14 +1086,15 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // 3.1e-4 coherent data vs 6e-6 for SIMT fp32; the cfg4 dW depth h*S is
 // 16384).  So for deep K the MMA issuer restarts a fresh chunk accumulator X
 // every `kc` stages; the epilogue warps fold each finished chunk into the
-// tile's running sum R with round-to-nearest fp32 adds (tcgen05.ld X, R ->
-// FADD -> tcgen05.st R; R = X for chunk 0) and then release X.  R is private
-// to the epilogue threads, so the output pass of tile i overlaps the MMAs of
-// tile i+1's first chunk.  Truncation then acts on <= 3*kc*(BK/8)
-// accumulations per chunk.  Shallow launches (kc == 0) accumulate straight
-// into two alternating running sums as before.
-constexpr int kPersThreads = 480;
-constexpr int kPersConv = 128;  // converter threads (warps 0-3)
+// tile's running sum R -- held in the epilogue threads' registers -- with
+// round-to-nearest fp32 adds (tcgen05.ld X -> FADD; R = X for chunk 0) and
+// release X while the MMAs fill the other X; the output pass of tile i
+// overlaps the MMAs of tile i+1.  Truncation then acts on <= 3*kc*(BK/8)
+// accumulations per chunk.  (Round 2 first kept R in TMEM beside a single
+// chunk accumulator at 256-column tiles, so the MMA waited for every fold:
+// ~6% of the cfg4 step; R in registers with two X removes the wait.)
+constexpr int kPersThreads = 512;  // 4 warp groups: converters | epilogue 0 | epilogue 1 | TMA A, MMA, TMA B
+constexpr int kPersConv = 128;    // converter threads (warps 0-3)
 constexpr int kEpiCols = 16;    // columns per epilogue chunk
 constexpr int kEpiLd = 20;      // padded chunk row (floats)
 
@@ -1106,13 +1109,11 @@ struct PCfg {
   static constexpr int BUDGET = 227 * 1024 - 1024 - 512 - 2 * kChainBytes - CHUNK_BYTES;
   static constexpr int RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = RAW > 8 ? 8 : RAW;
-  // TMEM: K-chunked mode: one running sum R then NX chunk accumulators X;
-  // unchunked mode: two running sums (see tma_gemm_persistent)
-  static constexpr int NX = 512 / BN - 1;  // chunk accumulators beside one running sum
-  static constexpr int TMEM_COLS = 512;
+  // TMEM: two chunk accumulators X (the running sum lives in the epilogue's registers)
+  static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512 + 2 * kChainBytes + CHUNK_BYTES;
   static_assert(STAGES >= 2, "persistent pipeline needs two stages");
-  static_assert(TMEM_COLS == 512 && 2 * BN <= 512, "running sums and chunk accumulators fill TMEM");
+  static_assert(TMEM_COLS <= 512, "two chunk accumulators fit TMEM");
 };
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -1162,6 +1163,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   using C = PCfg<BN, BNL>;
   constexpr int BK = C::BK;
   constexpr int kBoxIdx = box_idx<BNL>();
+  constexpr int HALF = BN / 2;  // running-sum columns per epilogue thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // Plain TF32 (p.terms == 1, single CTAs) needs no residual halves: each
@@ -1171,21 +1173,14 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   const int NST = one ? 2 * C::STAGES : C::STAGES;
   const int SB = one ? C::STAGE_BYTES / 2 : C::STAGE_BYTES;
   const int BOFF = one ? C::A_BYTES : C::B_OFF;
-  // kc == 0: unchunked (every tile accumulates in one of two running sums R,
-  // the epilogue of tile i overlaps the MMAs of tile i+1); kc > 0: K-chunked,
-  // one running sum R (TMEM columns [0, BN)) and NX chunk accumulators X
-  const bool chunked = kc > 0;
-  const int NR = chunked ? 1 : 2, NX = C::NX;
-  if (!chunked) kc = 1 << 30;
-  static_assert(6 * C::STAGES * 8 + 10 * 8 + 8 <= 512 && C::NX <= 3, "barrier region");
+  if (kc <= 0) kc = 1 << 30;  // one chunk per tile
+  static_assert(6 * C::STAGES * 8 + 4 * 8 + 8 <= 512, "barrier region");
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* conv_full = tma_full + 2 * C::STAGES;
   uint64_t* empty = conv_full + 2 * C::STAGES;
-  uint64_t* r_full = empty + 2 * C::STAGES;  // [NR]
-  uint64_t* r_empty = r_full + 2;            // [NR]
-  uint64_t* x_full = r_empty + 2;            // [NX <= 3]
-  uint64_t* x_empty = x_full + 3;            // [NX <= 3]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 3);
+  uint64_t* x_full = empty + 2 * C::STAGES;  // [2] chunk accumulators
+  uint64_t* x_empty = x_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 2);
   EwChain* chain_s = reinterpret_cast<EwChain*>(smem + C::STAGES * C::STAGE_BYTES + 512);
   float* chunk_s = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512 + 2 * kChainBytes);
 
@@ -1200,16 +1195,12 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&r_full[b], 1);
-      mbar_init(&r_empty[b], 2 * NCTA);  // both epilogue groups of every CTA
-    }
-    for (int b = 0; b < 3; ++b) {
       mbar_init(&x_full[b], 1);
-      mbar_init(&x_empty[b], 2 * NCTA);
+      mbar_init(&x_empty[b], 2 * NCTA);  // both epilogue groups of every CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) {
+  if (warp == 13) {
     if constexpr (PAIR) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                    "r"(C::TMEM_COLS));
@@ -1226,63 +1217,59 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8 || warp == 10) {
-    if (lane == 0) {
-      // ---------------- TMA producers (A: warp 8, B: warp 10) ----------------
-      const bool load_a = warp == 8;
-      int g = 0;  // global stage counter
-      for (int t = first; t < ntiles; t += stride) {
-        const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
-        const auto& job = p.job[T.jid];
-        int seg = 0, k0 = 0;
-        for (int it = 0; it < T.nstages; ++it, ++g) {
-          const int s = g % NST;
-          mbar_wait(&empty[s], ((g / NST) & 1) ^ 1);
-          uint8_t* base = smem + s * SB;
-          mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
-          if constexpr (IS_DW) {
-            if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, T.m0 / 32, &tma_full[s]);
-            else tma_load_3d(base + BOFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, T.nb0 / 32, &tma_full[s]);
-            k0 += BK;
-          } else {
-            const Seg& sg = job.seg[seg];
-            if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + T.m0, &tma_full[s]);
-            else tma_load_2d(base + BOFF, map_at(sg.tb, kBoxIdx), k0, T.nb0, &tma_full[s]);
-            k0 += BK;
-            if (k0 >= sg.k) {
-              k0 = 0;
-              ++seg;
+  if (warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    if (warp == 12 || warp == 14) {
+      if (lane == 0) {
+        // ---------------- TMA producers (A: warp 12, B: warp 14) ----------------
+        const bool load_a = warp == 12;
+        int g = 0;  // global stage counter
+        for (int t = first; t < ntiles; t += stride) {
+          const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+          const auto& job = p.job[T.jid];
+          int seg = 0, k0 = 0;
+          for (int it = 0; it < T.nstages; ++it, ++g) {
+            const int s = g % NST;
+            mbar_wait(&empty[s], ((g / NST) & 1) ^ 1);
+            uint8_t* base = smem + s * SB;
+            mbar_expect_tx(&tma_full[s], load_a ? C::A_BYTES : C::B_BYTES);
+            if constexpr (IS_DW) {
+              if (load_a) tma_load_3d(base, map_at(job.te, 2), 0, job.erow + k0, T.m0 / 32, &tma_full[s]);
+              else tma_load_3d(base + BOFF, map_at(job.ty, kBoxIdx), 0, job.yrow + k0, T.nb0 / 32, &tma_full[s]);
+              k0 += BK;
+            } else {
+              const Seg& sg = job.seg[seg];
+              if (load_a) tma_load_2d(base, sg.ta, k0, sg.arow + T.m0, &tma_full[s]);
+              else tma_load_2d(base + BOFF, map_at(sg.tb, kBoxIdx), k0, T.nb0, &tma_full[s]);
+              k0 += BK;
+              if (k0 >= sg.k) {
+                k0 = 0;
+                ++seg;
+              }
             }
           }
         }
       }
-    }
-  } else if (warp == 9) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer ----------------
+    } else if (warp == 13 && lane == 0 && rank == 0) {
+      // ---------------- MMA issuer: every chunk into a fresh X ----------------
       const uint32_t idesc = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       const bool split = p.terms != 1;
-      int g = 0, ti = 0, xc = 0;
-      for (int t = first; t < ntiles; t += stride, ++ti) {
+      int g = 0, xc = 0;
+      for (int t = first; t < ntiles; t += stride) {
         const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
-        const int rb = ti % NR;
-        uint32_t acc = tmem + rb * BN;
-        if (!chunked) {
-          if constexpr (PAIR) mbar_wait_cluster(&r_empty[rb], ((ti / NR) & 1) ^ 1);
-          else mbar_wait(&r_empty[rb], ((ti / NR) & 1) ^ 1);
-        }
         int xb = -1, chunk_end = 0;
+        uint32_t acc = tmem;
         for (int it = 0; it < T.nstages; ++it, ++g) {
-          if (chunked && it == chunk_end) {  // next chunk: a fresh accumulator X
+          if (it == chunk_end) {  // next chunk: the other accumulator, once the epilogue folded it
             if (xb >= 0) {
               if constexpr (PAIR) mma_commit_pair(&x_full[xb]);
               else mma_commit(&x_full[xb]);
               ++xc;
             }
-            xb = xc % NX;
-            if constexpr (PAIR) mbar_wait_cluster(&x_empty[xb], ((xc / NX) & 1) ^ 1);
-            else mbar_wait(&x_empty[xb], ((xc / NX) & 1) ^ 1);
-            acc = tmem + (1 + xb) * BN;
+            xb = xc & 1;
+            if constexpr (PAIR) mbar_wait_cluster(&x_empty[xb], ((xc >> 1) & 1) ^ 1);
+            else mbar_wait(&x_empty[xb], ((xc >> 1) & 1) ^ 1);
+            acc = tmem + xb * BN;
             chunk_end += kc;
           }
           const int s = g % NST;
@@ -1308,7 +1295,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
               dbh = smem_desc(b_hi + off, 16, 1024, 2);
               dbl = smem_desc(b_lo + off, 16, 1024, 2);
             }
-            const uint32_t acc0 = (it > (chunked ? chunk_end - kc : 0) || j > 0) ? 1u : 0u;
+            const uint32_t acc0 = (it > chunk_end - kc || j > 0) ? 1u : 0u;
             if constexpr (PAIR) {
               if (split) {
                 mma_tf32_pair(acc, dal, dbh, idesc, acc0);
@@ -1326,17 +1313,13 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           if constexpr (PAIR) mma_commit_pair(&empty[s]);
           else mma_commit(&empty[s]);
         }
-        if (chunked) {  // the tile's last chunk accumulator
-          if constexpr (PAIR) mma_commit_pair(&x_full[xb]);
-          else mma_commit(&x_full[xb]);
-          ++xc;
-        } else {
-          if constexpr (PAIR) mma_commit_pair(&r_full[rb]);
-          else mma_commit(&r_full[rb]);
-        }
+        if constexpr (PAIR) mma_commit_pair(&x_full[xb]);  // the tile's last chunk
+        else mma_commit(&x_full[xb]);
+        ++xc;
       }
     }
   } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     // ---------------- converters (warps 0-3) ----------------
     int g = 0;
     for (int t = first; t < ntiles; t += stride) {
@@ -1346,22 +1329,22 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         mbar_wait(&tma_full[s], (g / NST) & 1);
         uint8_t* base = smem + s * SB;
         if (p.terms != 1) {
-        const float4* a_hi = reinterpret_cast<const float4*>(base);
-        float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
+          const float4* a_hi = reinterpret_cast<const float4*>(base);
+          float4* a_lo = reinterpret_cast<float4*>(base + C::A_BYTES);
 #pragma unroll
-        for (int i = 0; i < C::A_BYTES / 16 / kPersConv; ++i) {
-          const int q = threadIdx.x + i * kPersConv;
-          const float4 x = a_hi[q];
-          a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
-        }
-        const float4* b_hi = reinterpret_cast<const float4*>(base + BOFF);
-        float4* b_lo = reinterpret_cast<float4*>(base + BOFF + C::B_BYTES);
+          for (int i = 0; i < C::A_BYTES / 16 / kPersConv; ++i) {
+            const int q = threadIdx.x + i * kPersConv;
+            const float4 x = a_hi[q];
+            a_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+          }
+          const float4* b_hi = reinterpret_cast<const float4*>(base + BOFF);
+          float4* b_lo = reinterpret_cast<float4*>(base + BOFF + C::B_BYTES);
 #pragma unroll
-        for (int i = 0; i < C::B_BYTES / 16 / kPersConv; ++i) {
-          const int q = threadIdx.x + i * kPersConv;
-          const float4 x = b_hi[q];
-          b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
-        }
+          for (int i = 0; i < C::B_BYTES / 16 / kPersConv; ++i) {
+            const int q = threadIdx.x + i * kPersConv;
+            const float4 x = b_hi[q];
+            b_lo[q] = make_float4(tf32_residual(x.x), tf32_residual(x.y), tf32_residual(x.z), tf32_residual(x.w));
+          }
         } else {  // plain TF32: round both operands to nearest in place (the MMA would truncate)
           round_tf32_inplace(base, C::A_BYTES, threadIdx.x, kPersConv);
           round_tf32_inplace(base + BOFF, C::B_BYTES, threadIdx.x, kPersConv);
@@ -1378,72 +1361,55 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         }
       }
     }
-  } else if ((warp >= 4 && warp < 8) || warp >= 11) {
-    // ---------------- epilogue: two groups of 4 warps (4-7, 11-14) ----------------
-    // group g drains 16-column chunks g, g+2, ... of the tile through its own
-    // SMEM staging chunk and chain copy; named barrier 3+g
-    const int grp = warp >= 11 ? 1 : 0;
-    const int et = threadIdx.x - (grp ? 11 : 4) * 32;  // 0..127
-    const int quarter = warp & 3;                      // TMEM lane quarter this warp may read
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    // ---------------- epilogue: two warp groups (4-7, 8-11) ----------------
+    // Thread (lane quarter q, lane l) of group g owns accumulator row 32q+l,
+    // columns {16-column chunks g, g+2, ...}: the tile's running sum R lives in
+    // its registers.  Each finished chunk accumulator X is read (tcgen05.ld)
+    // and added to R with round-to-nearest fp32 adds, then released to the MMA
+    // -- which meanwhile fills the other X -- so the K-chunking costs no MMA
+    // stall.  After the last chunk R goes through the group's SMEM staging
+    // chunk to the coalesced output walk (chain epilogue or dW store).
+    const int grp = warp >= 8 ? 1 : 0;
+    const int et = threadIdx.x - (grp ? 8 : 4) * 32;  // 0..127
+    const int quarter = warp & 3;                     // TMEM lane quarter this warp may read
     const int r_loc = quarter * 32 + lane;
     EwChain* my_chain = reinterpret_cast<EwChain*>(reinterpret_cast<uint8_t*>(chain_s) + grp * kChainBytes);
     float* my_chunk = chunk_s + grp * (BM * kEpiLd);
     const int bar = 3 + grp;
     auto gsync = [&] { asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory"); };
-    auto release_bar = [&](uint64_t* bar) {  // this group's last TMEM access of a buffer is done
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      gsync();
-      if (et == 0) {
-        if (rank == 0) mbar_arrive(bar);
-        else mbar_arrive_cluster(bar, 0);
-      }
-    };
-    int ti = 0, staged_job = -1, xc = 0;
-    for (int t = first; t < ntiles; t += stride, ++ti) {
+    float R[HALF];
+    int staged_job = -1, xc = 0;
+    for (int t = first; t < ntiles; t += stride) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
-      const int rb = ti % NR;
-      auto release = [&](int) {
-        if (!chunked) release_bar(&r_empty[rb]);
-      };
-      const uint32_t racc = tmem + rb * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-      // K-chunked: fold every chunk of the tile into R (R = X, then R += X;
-      // round-to-nearest fp32 adds) over this group's 16-column slices -- the
-      // same slices the output pass reads, so R never crosses threads
-      const int nch = chunked ? (T.nstages + kc - 1) / kc : 0;
+      const int nch = (T.nstages + kc - 1) / kc;
       for (int c = 0; c < nch; ++c, ++xc) {
-        const int xb = xc % NX;
-        mbar_wait(&x_full[xb], (xc / NX) & 1);
+        const int xb = xc & 1;
+        mbar_wait(&x_full[xb], (xc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t xacc = tmem + (1 + xb) * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-        for (int c0 = grp * kEpiCols; c0 < BN; c0 += 2 * kEpiCols) {
-          float vx[16], vr[16];
-          tmem_ld16(xacc + c0, vx);
-          if (c > 0) {
-            tmem_ld16(racc + c0, vr);
+        const uint32_t xacc = tmem + xb * BN + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) vr[q] += vx[q];
-            tmem_st16(racc + c0, vr);
-          } else {
-            tmem_st16(racc + c0, vx);
-          }
+        for (int q = 0; q < HALF / 16; ++q) {
+          float v[16];
+          tmem_ld16(xacc + grp * kEpiCols + q * 2 * kEpiCols, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) R[q * 16 + i] = c > 0 ? R[q * 16 + i] + v[i] : v[i];
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        release_bar(&x_empty[xb]);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        gsync();
+        if (et == 0) {
+          if (rank == 0) mbar_arrive(&x_empty[xb]);
+          else mbar_arrive_cluster(&x_empty[xb], 0);
+        }
       }
       if constexpr (!IS_DW) {
         if (T.jid != staged_job) {  // the chain of this tile's job
-          gsync();
           stage_chain(my_chain, p.job[T.jid].epi, et, 128);
           gsync();
           staged_job = T.jid;
         }
       }
-      const int b = rb;
-      if (!chunked) {
-        mbar_wait(&r_full[rb], (ti / NR) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      }
-      const uint32_t acc = racc;
       const int ncols = (T.N - T.n0) < BN ? (T.N - T.n0) : BN;
       const int nrows = (T.M - T.m0) < BM ? (T.M - T.m0) : BM;
       bool vec;
@@ -1454,15 +1420,23 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
       } else {
         vec = chain_vec_ok(*my_chain, T.N);
       }
-      const int first_c = grp * kEpiCols;
-      if (first_c >= ncols) release(b);  // no chunk for this group
-      for (int c0 = first_c; c0 < ncols; c0 += 2 * kEpiCols) {
+#pragma unroll 1
+      for (int q = 0; q < HALF / 16; ++q) {
+        const int c0 = grp * kEpiCols + q * 2 * kEpiCols;
+        if (c0 >= ncols) break;
+        // this thread's 16 values of chunk q (selected without dynamic register indexing)
         float v[16];
-        tmem_ld16(acc + c0, v);
-        if (c0 + 2 * kEpiCols >= ncols) release(b);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = R[i];
+#pragma unroll
+        for (int qq = 1; qq < HALF / 16; ++qq)
+          if (qq == q) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = R[qq * 16 + i];
+          }
         float4* dst = reinterpret_cast<float4*>(my_chunk + r_loc * kEpiLd);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         gsync();
         const int cw = (ncols - c0) < kEpiCols ? (ncols - c0) : kEpiCols;
         if (vec) {
@@ -1515,7 +1489,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if constexpr (PAIR) cluster_sync();
   else __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     if constexpr (PAIR) {
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
     } else {
@@ -1534,8 +1508,8 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
 constexpr int kMaxStagesPerAcc = 16;
 
 // stages per accumulation chunk for a launch whose tiles are at most
-// `max_stages` deep: 0 (unchunked) when the whole K fits the bound, else
-// 8 / 16 (3xTF32 dW / NT) or 24 / 48 (TF32) -- <= 96 / 192 truncating
+// `max_stages` deep: 0 (one chunk per tile) when the whole K fits the bound,
+// else 4 / 16 (3xTF32 dW / NT) or 12 / 48 (TF32) -- <= 48 / 192 truncating
 // accumulations per chunk.
 // RGB_TC_KC overrides (experiments).
 int chunk_stages(int terms, int max_stages, bool dw) {
@@ -1550,12 +1524,13 @@ int chunk_stages(int terms, int max_stages, bool dw) {
   if (per_acc <= kMaxStagesPerAcc) return 0;
   if (!dw && forced_nt > 0) return forced_nt;
   if (forced > 0) return forced;
-  // dW (K = h*S, 16384 at cfg4) 8 stages per chunk; the NT GEMMs (K <= 4096)
-  // 16: cfg4 after 4 training steps 5.5e-5 worst normwise vs 4.3e-5 with 8
-  // everywhere and 8.6e-5 with 32 for NT (tools/diag_parity.py), at 702k vs
-  // 683k / 720k frames/s
-  if (terms == 1) return dw ? 24 : 48;
-  return dw ? 8 : 16;
+  // dW (K = h*S, 16384 at cfg4): 4 stages per chunk (the folds cost the dW
+  // epilogue nothing it cannot hide); the NT GEMMs (K <= 4096, chain-heavy
+  // epilogues that are the kernel's bound): 16.  cfg4 after 5 training steps
+  // (tools/diag_parity.py, profiles/r02_chunk_size_sweep.log): worst 4.9e-5;
+  // NT 8 -> 4.3e-5 at -3% throughput, NT unchunked -> 8.8e-5 (too close to 1e-4)
+  if (terms == 1) return dw ? 12 : 48;
+  return dw ? 4 : 16;
 }
 
 template <int BN, bool IS_DW, bool PAIR, class P>
@@ -2374,8 +2349,12 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
         for (int c = 0; c < nch; ++c) rings[c] = c < J ? pf.ring : fl.ew[(size_t)f * fl.n_ew + (c - J)].ring;
         frame_chains_fused<2>(chains, J, nch, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid);
       } else {
+#ifndef RGB_FL_R
+#define RGB_FL_R 4
+#endif
         for (int j = 0; j < J; ++j)
-          frame_chain<4>(chains[j], tile_s, C::EPI_LD, j * bu, true, m0, u0, bu, N, r_lo, rows_hi, pf.ring, tid);
+          frame_chain<RGB_FL_R>(chains[j], tile_s, C::EPI_LD, j * bu, true, m0, u0, bu, N, r_lo, rows_hi, pf.ring,
+                                tid);
         if (fl.fuse_ew) {
           // the step's elementwise ops read the job chains' outputs at the same
           // (row, unit): visible to the CTA after the barrier
