@@ -394,7 +394,7 @@ def run_ours(args, cfg):
     ex = GradientExchange()  # timing max over ranks (torch.distributed plumbing)
     # the gradient exchange itself: NCCL through the C ABI, bucketed and
     # overlapped with the backward (rgb_backward_window_allreduce)
-    nex = NcclExchange() if world > 1 else None
+    nex = NcclExchange(bucketed=args.bucketed) if world > 1 else None
     S_total = cfg["S"] * (world if args.scaling == "weak" else 1)
     lo, hi = shard_streams(S_total, world, rank)
     S = hi - lo
@@ -537,8 +537,9 @@ def run_ours(args, cfg):
                                                      "Weights.init seed 0)",
         "config": {"workload": cfg["name"] + ": " + cfg["desc"], "streams_total": S_total, "streams_per_gpu": S,
                    "h": h, "h_prime": hp, "global_batch_frames": hp * S_total,
-                   "parallelism": f"dp{world} (streams sharded; dW summed by NCCL through the C ABI in "
-                                  f"per-supernode buckets overlapped with the backward)" if world > 1 else "dp1",
+                   "parallelism": (f"dp{world} (streams sharded; dW summed by NCCL through the C ABI, "
+                                   + ("per-SCC buckets overlapped with the backward)" if args.bucketed
+                                      else "one all-reduce after the backward)")) if world > 1 else "dp1",
                    "l2": "no flush: per-step working set (history + W + W^T + dW) exceeds the 126 MB L2",
                    "schedule": "hoisted (paper §3.1)",
                    "launch": "CUDA-graph replay per ring phase" if graphs else "eager",
@@ -630,6 +631,8 @@ def main(argv=None):
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dry-setup", action="store_true", help="rank setup only (launcher test, CPU)")
+    ap.add_argument("--bucketed", action="store_true",
+                    help="N>1: bucketed backward with the all-reduce overlapped (DESIGN.md §8; off: one all-reduce)")
     raw = sys.argv[1:] if argv is None else list(argv)
     args = ap.parse_args(raw)
     if args.warmup < 3:

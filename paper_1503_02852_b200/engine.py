@@ -726,7 +726,7 @@ class Trainer:
                                              _CRIT_CODE[self.cfg.criterion], hp, st))
         if self.state.program.softmax_feeds is not None:
             raise EngineError(f"softmax layer {self.state.program.softmax_feeds!r} feeds other layers")
-        if exchange is not None and getattr(exchange, "native", False) and not self._seq:
+        if exchange is not None and getattr(exchange, "bucketed", False) and not self._seq:
             # bucketed backward: each supernode's dW summed over the GPUs while
             # the backward below it runs (C ABI + NCCL, dist.NcclExchange)
             _lib.check(L.rgb_backward_window_allreduce(plan, _ptr(self.weights.flat_t), _ptr(self.grads.flat),

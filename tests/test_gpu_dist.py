@@ -26,10 +26,31 @@ def exchange():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     torch.cuda.set_device(0)
-    ex = NcclExchange()
+    ex = NcclExchange(bucketed=True)
     yield ex
     torch.cuda.synchronize()
     ex.close()
+
+
+def test_single_allreduce_exchange_equals_plain_step(exchange):
+    """The default exchange: plain backward, then one NCCL all-reduce of the
+    flat gradient through the C ABI (rgb_allreduce_grads)."""
+    ex = NcclExchange.__new__(NcclExchange)
+    ex.__dict__.update(exchange.__dict__)
+    ex.bucketed = False
+    net = P.build_lstm(64, 128, 64)
+    cfg = P.TrainConfig(h=8, h_prime=4, lr=0.01, iterations=1)
+    wa, wb = P.Weights.init(net, 1), P.Weights.init(net, 1)
+    ta, tb = P.Trainer(net, wa, 16, cfg), P.Trainer(net, wb, 16, cfg)
+    rng = np.random.default_rng(1)
+    for _ in range(4):
+        x = torch.tensor(rng.uniform(-1, 1, size=(64, 64)), dtype=torch.float32, device="cuda")
+        t = torch.tensor(rng.integers(0, 64, size=64), device="cuda")
+        ta.step(x, t)
+        tb.step(x, t, ex)
+        assert ta.loss() == tb.loss()
+    assert torch.equal(wa.flat, wb.flat)
+    ex.handle = None  # owned by the fixture
 
 
 def test_comm_size_and_flat_allreduce(exchange):
