@@ -1019,14 +1019,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_gemm_kernel(const __grid_c
       const int r_lo = split * BM / csplit, r_hi = (split + 1) * BM / csplit;
       float* tile_s = reinterpret_cast<float*>(smem);
       if (warp < 8) {
+        // every remote load of a batch is in flight before the first is used
+        // (a DSMEM round trip is ~200 cycles; the serial form cost ~1 us more
+        // per frame, tools/trace_frame_loop.py)
         constexpr int G4 = BN / 4;
         using CE = Cfg<BN>;
-        for (int q = threadIdx.x; q < (r_hi - r_lo) * G4; q += 256) {
-          const int off = (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4;
-          float4 a = ld_dsmem4(tile_s + off, PAIR ? rank : 0u);
-          for (int k = 1; k < csplit; ++k)
-            a = add4(a, ld_dsmem4(tile_s + off, PAIR ? (uint32_t)(2 * k) + rank : (uint32_t)k));
-          *reinterpret_cast<float4*>(tile_s + off) = a;
+        const int nq = (r_hi - r_lo) * G4;
+        for (int q0 = threadIdx.x; q0 < nq; q0 += 256 * 4) {
+          float4 a[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = q0 + 256 * i;
+            a[i] = q < nq ? ld_dsmem4(tile_s + (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4, PAIR ? rank : 0u)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int k = 1; k < csplit; ++k) {
+            float4 b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int q = q0 + 256 * i;
+              b[i] = q < nq ? ld_dsmem4(tile_s + (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4,
+                                        PAIR ? (uint32_t)(2 * k) + rank : (uint32_t)k)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = add4(a[i], b[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = q0 + 256 * i;
+            if (q < nq) *reinterpret_cast<float4*>(tile_s + (r_lo + q / G4) * CE::EPI_LD + (q % G4) * 4) = a[i];
+          }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
         CTA_MARK(3)
