@@ -1,5 +1,7 @@
 """GPU parity at the exact shapes of the benchmarked configs (BASELINE.json
-configs[1] and [3]), run the way bench.py runs them, against the float64 oracle.
+configs[1], [2] and [3]; configs[0] and [4] are covered by the golden cfg1 case
+and test_gpu_engine.test_configs_small_scale), run the way bench.py runs them,
+against the float64 oracle.
 
 * cfg4 (the headline): build_stacked_lstm(1024, [1024]*3, 1024), S = 512,
   h = 32, h' = 16, the default kernel variants (CTA pairs, persistent GEMMs,
@@ -92,4 +94,14 @@ def test_cfg2_intra_stream_config_matches_oracle():
     report = []
     worst = run_graphed_vs_oracle(net, S=1, h=512, hp=256, iters=3, lr=1e-3, seed=1, report=report)
     print("cfg2 per-iteration normwise errors:", report)
+    assert worst < TOL, report
+
+
+def test_cfg3_multistream_config_matches_oracle():
+    """cfg3 (BASELINE.json configs[2]): 2 x LSTM512, 64 streams, h = 32, h' = 16 --
+    persistent SCC loops over 64 stream rows, cross-layer wavefront."""
+    net = P.build_stacked_lstm(512, [512, 512], 512)
+    report = []
+    worst = run_graphed_vs_oracle(net, S=64, h=32, hp=16, iters=4, lr=1e-3, seed=2, report=report)
+    print("cfg3 per-iteration normwise errors:", report)
     assert worst < TOL, report
