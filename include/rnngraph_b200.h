@@ -178,12 +178,12 @@ int rgb_set_gemm_mode(int mode);
  * with W_rec resident in shared memory and a grid barrier per dense
  * dependency; 0 launches the loop body once per frame. */
 int rgb_set_scc_mode(int on);
-/* Persistent tensor-core frame loops: 1 runs every recurrent loop
+/* Persistent tensor-core frame loops: 1 (default) runs every recurrent loop
  * whose body is one tensor-core sized GEMM step plus elementwise steps (the
  * large-S LSTM / stacked-LSTM SCCs, engine.py:405-413, 568-576) as one
  * cooperative launch over all its frames with a grid barrier per dependent
- * step; 0 (default; measured faster at cfg4,
- * DESIGN.md §9) launches the body once per frame. */
+ * step; 0 launches the body once per frame
+ * (with programmatic dependent launch; DESIGN.md §9 compares the two). */
 int rgb_set_frame_loop(int on);
 /* Cross-layer wavefront: the stages between persistent SCC
  * loops of a forward / backward section run on their own streams over frame

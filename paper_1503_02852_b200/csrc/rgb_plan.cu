@@ -110,13 +110,13 @@ bool g_wavefront_active = false;
 bool use_tc(double flops) { return g_gemm_mode == 2 || (g_gemm_mode == 0 && flops >= kTcMinFlops); }
 
 // persistent tensor-core frame loops for large S (try_frame_loop); 1 = on.
-// Off by default: at cfg4 it measured 644k vs 686k frames/s for the per-frame
-// launches with programmatic dependent launch (the per-frame
-// cost is the L2-bound main loop and the latency-bound chain epilogue, not
-// the launches).
+// With the LSTM cell chains evaluated in registers and the next frame's
+// inputs stored first (tc::lstm_chains) it measured 727k vs 699k frames/s for
+// the per-frame launches at cfg4; without them (generic chains through
+// global memory) 668k.
 int g_frame_loop = [] {
   const char* e = getenv("RGB_FRAME_LOOP");
-  return e ? atoi(e) : 0;
+  return e ? atoi(e) : 1;
 }();
 
 // cross-layer wavefront of the forward section; 1 = on
@@ -266,9 +266,62 @@ struct rgb_plan {
     GemmGroup* d_groups = nullptr;
     EwLaunch* d_ew = nullptr;
     void* h_pinned = nullptr;
-    int n_ew = 0, fuse_ew = 0;
+    int n_ew = 0, fuse_ew = 0, pattern = 0;
     double flops = 0;
   };
+
+  // The LSTM cell chain sets the frame loop evaluates in registers with the
+  // next frame's inputs stored first (tc::lstm_chains): 1 forward (two gate
+  // jobs, fused cell update), 2 backward (one delta job, 5-op chain), 0 other.
+  // g1 = the next frame's group: its GEMM must read only the critical outputs.
+  static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+  static int lstm_pattern(const GemmGroup& g, const GemmGroup& g1, const EwLaunch* ew, int n_ew, bool fuse) {
+    auto plain = [](const EwOp& o) { return !o.inj && !o.base && o.nrank1 == 0 && a16(o.out); };
+    auto reads_only = [&](const GemmGroup& n, const float* a, const float* b) {
+      for (int j = 0; j < n.njobs; ++j)
+        for (int s = 0; s < n.job[j].nseg; ++s)
+          if (n.job[j].seg[s].a != a && n.job[j].seg[s].a != b) return false;
+      return true;
+    };
+    if (g.job[0].n % 4) return 0;
+    if (g.njobs == 1 && n_ew == 0 && g.job[0].epi.nops == 5) {
+      const EwOp* o = g.job[0].epi.op;
+      for (int k = 0; k < 5; ++k)
+        if (o[k].kind != EW_BWD || !plain(o[k])) return 0;
+      if (o[0].act != ACT_IDENTITY || o[0].nterm != 2 || o[0].nfac || !a16(o[0].term[0]) || !a16(o[0].term[1]))
+        return 0;
+      for (int k = 1; k <= 2; ++k)
+        if (o[k].act != ACT_IDENTITY || o[k].nterm != 1 || o[k].term[0] != o[0].out || o[k].nfac != 2 ||
+            !o[k].eps[0] || !o[k].eps[1] || !a16(o[k].fac[0]) || !a16(o[k].fac[1]) || !a16(o[k].eps[0]) ||
+            !a16(o[k].eps[1]))
+          return 0;
+      for (int k = 3; k <= 4; ++k) {
+        const float* t = o[k].term[0];
+        if ((o[k].act != ACT_SIGMOID && o[k].act != ACT_TANH) || !o[k].y || !a16(o[k].y) || o[k].nterm != 1 ||
+            o[k].nfac || (t != o[1].eps[0] && t != o[1].eps[1] && t != o[2].eps[0] && t != o[2].eps[1]))
+          return 0;
+      }
+      return reads_only(g1, o[3].out, o[4].out) ? 2 : 0;
+    }
+    if (g.njobs == 2 && n_ew == 1 && fuse && ew[0].nchains == 1 && ew[0].chain[0].nops == 1) {
+      for (int j = 0; j < 2; ++j) {
+        const EwChain& ch = g.job[j].epi;
+        if (ch.nops != 2) return 0;
+        const EwOp &o0 = ch.op[0], &o1 = ch.op[1];
+        if (o0.kind != EW_FWD_ADD || !plain(o0) || o0.nterm != 1 || !a16(o0.term[0])) return 0;
+        if (o1.kind != EW_FWD_MUL || !plain(o1) || o1.nfac != 2 || (o1.fac[0] != o0.out && o1.fac[1] != o0.out) ||
+            !a16(o1.fac[0]) || !a16(o1.fac[1]))
+          return 0;
+      }
+      const EwOp& e = ew[0].chain[0].op[0];
+      const float *pa = g.job[0].epi.op[1].out, *pb = g.job[1].epi.op[1].out;
+      if (e.kind != EW_FWD_ADD || !plain(e) || e.nterm != 2 ||
+          !((e.term[0] == pa && e.term[1] == pb) || (e.term[0] == pb && e.term[1] == pa)))
+        return 0;
+      return reads_only(g1, e.out, e.out) ? 1 : 0;
+    }
+    return 0;
+  }
   std::map<std::vector<int64_t>, FrameLoopBlocks> frame_loops;
   unsigned* fl_bar = nullptr;
   // blocks are carved from one device + one pinned arena, allocated at the
@@ -1073,6 +1126,7 @@ struct rgb_plan {
       fb.fuse_ew = n_ew > 0 && n_ew + groups[0].njobs <= 4;
       for (int e = 0; e < n_ew && fb.fuse_ew; ++e)
         fb.fuse_ew = ews[e].nchains == 1 && ews[e].chain[0].width == groups[0].job[0].n;
+      if (c.frames >= 2) fb.pattern = lstm_pattern(groups[0], groups[1], ews.data(), n_ew, fb.fuse_ew != 0);
       const size_t need = (gbytes + ebytes + 255) & ~size_t(255);
       if (fb.ok && !fl_dev) {
         if (cs != cudaStreamCaptureStatusNone) {
@@ -1108,7 +1162,7 @@ struct rgb_plan {
       it->second.ok = 1;
       GemmGroup g0 = groups[0];
       const int slot = prof_start(st);
-      const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, n_ew, fb.fuse_ew, c.frames, fl_bar, st);
+      const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, n_ew, fb.fuse_ew, fb.pattern, c.frames, fl_bar, st);
       if (lrc < 0) {
         it->second.ok = 0;
         return RGB_OK;
@@ -1124,7 +1178,8 @@ struct rgb_plan {
     const FrameLoopBlocks& fb = it->second;
     const GemmGroup& g0 = *static_cast<const GemmGroup*>(fb.h_pinned);
     const int slot = prof_start(st);
-    const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, fb.n_ew, fb.fuse_ew, c.frames, fl_bar, st);
+    const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, fb.n_ew, fb.fuse_ew, fb.pattern, c.frames, fl_bar,
+                                         st);
     if (lrc < 0) return RGB_OK;
     note_launch();
     prof_stop(slot, st, PROF_GEMM_FRAME, fb.flops, 0.0);

@@ -1116,6 +1116,9 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // accumulations per chunk.  (Round 2 first kept R in TMEM beside a single
 // chunk accumulator at 256-column tiles, so the MMA waited for every fold:
 // ~6% of the cfg4 step; R in registers with two X removes the wait.)
+#ifndef RGB_PERS_RE
+#define RGB_PERS_RE 2  // rows per thread per pass of the persistent epilogue's row walk
+#endif
 constexpr int kPersThreads = 512;  // 4 warp groups: converters | epilogue 0 | epilogue 1 | TMA A, MMA, TMA B
 constexpr int kPersConv = 128;    // converter threads (warps 0-3)
 constexpr int kEpiCols = 16;    // columns per epilogue chunk
@@ -1464,7 +1467,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         const int cw = (ncols - c0) < kEpiCols ? (ncols - c0) : kEpiCols;
         if (vec) {
           // 4 lanes per row (16-byte groups), 32 rows per pass, RE rows per thread
-          constexpr int RE = 2;
+          constexpr int RE = RGB_PERS_RE;
           const int sub = et >> 2, lc = et & 3, cl = lc * 4;
           if (cl < cw) {
 #pragma unroll 1
@@ -1722,6 +1725,7 @@ struct FrameLoop {
   int bu;                   // units per job in a tile (the tile's BN = njobs * bu)
   int prefetch;             // 1: warp 11 prefetches the chains' operands into L2 (off by default)
   int forward;              // 1: fused chain evaluation with register forwarding (frame_chains_fused)
+  int pattern;              // 1 / 2: the LSTM cell forward / backward chains (lstm_chains), 0: generic
   unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
 };
 
@@ -2019,6 +2023,158 @@ __device__ __forceinline__ bool chains_vec_ok(const EwChain* chains, int nch, in
   return true;
 }
 
+// ---- LSTM cell chains: critical outputs first ------------------------------
+// The host recognises the two chain sets of a peephole-LSTM SCC loop
+// (FrameLoop::pattern; the builders' cell wiring, engine.py:405-413 / 568-576):
+//   1 forward (tiles span both gate jobs, the cell update fused):
+//     g_j = act(acc_j + pf_j), p_j = x_j * g_j (j = input / forget gate),
+//     cell = act(p_a + p_b)
+//   2 backward: d = acc + e(t+1) + pb;  (d1, e10, e11) = (d, d*f11, d*f10);
+//     (d2, e20, e21) likewise; dg3 = e[k3] * f'(y3); dg4 = e[k4] * f'(y4).
+// Every value of an element group stays in registers (no store -> load round
+// trip); pass 0 stores only what the next frame's GEMM reads (cell(t), or the
+// two gate deltas) before the frame barrier, pass 1 -- run by four dedicated
+// store warps while the next frame's main loop runs -- recomputes the group
+// and stores the rest.  Arithmetic and order are exactly ew_apply's.
+__device__ __forceinline__ float4 act4(int act, float4 v) {
+  return make_float4(act_apply(act, v.x), act_apply(act, v.y), act_apply(act, v.z), act_apply(act, v.w));
+}
+__device__ __forceinline__ float4 dact4(int act, float4 y) {
+  return make_float4(act_deriv(act, y.x), act_deriv(act, y.y), act_deriv(act, y.z), act_deriv(act, y.w));
+}
+
+template <int R>
+__device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain* chains, const RingWrite* rings,
+                                            const float* tile_s, int ld, int m0, int u0, int bu, int N, int r_lo,
+                                            int r_hi, int tid, int nthr) {
+  const int ncols = min(bu, N - u0);
+  if (ncols <= 0 || r_hi <= r_lo) return;
+  const int g4 = ncols / 4, lanes = nthr / g4 * g4;
+  if (tid >= lanes) return;
+  const int g = tid % g4, layer = tid / g4, layers = lanes / g4;
+  const int j = u0 + 4 * g;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int rb = r_lo + layer; rb < r_hi; rb += layers * R) {
+    int64_t rr[R], e[R];
+    bool ok[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int rl = rb + u * layers;
+      ok[u] = rl < r_hi;
+      rr[u] = m0 + (ok[u] ? rl : r_lo);
+      e[u] = rr[u] * N + j;
+    }
+    auto acc_of = [&](int c, float4 (&a)[R]) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int rl = rb + u * layers;
+        a[u] = *reinterpret_cast<const float4*>(tile_s + (ok[u] ? rl : r_lo) * ld + c * bu + 4 * g);
+      }
+    };
+    auto load = [&](const float* p, float4 (&v)[R]) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) v[u] = ok[u] ? ld4(p, e[u]) : zero;
+    };
+    auto store = [&](const EwOp& op, const RingWrite& ring, const float4 (&v)[R]) {
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        if (ok[u]) ring_store4(op.out, e[u], rr[u], N, op.out_is_ring, ring, v[u]);
+    };
+    auto store_to = [&](float* p, const float4 (&v)[R]) {
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        if (ok[u]) st4(p, e[u], v[u]);
+    };
+    if (pattern == 1) {
+      const EwOp& ew = chains[2].op[0];
+      float4 pa[R], pb[R];
+#pragma unroll
+      for (int jb = 0; jb < 2; ++jb) {
+        const EwOp& o0 = chains[jb].op[0];
+        const EwOp& o1 = chains[jb].op[1];
+        float4 a[R], t[R], x[R], gt[R], pr[R];
+        acc_of(jb, a);
+        load(o0.term[0], t);
+        const int gi = o1.fac[0] == o0.out ? 0 : 1;
+        load(o1.fac[1 - gi], x);
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          gt[u] = act4(o0.act, add4(a[u], t[u]));
+          pr[u] = gi == 0 ? mul4(gt[u], x[u]) : mul4(x[u], gt[u]);
+        }
+        if (pass == 1) {
+          store(o0, rings[jb], gt);
+          store(o1, rings[jb], pr);
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          if (jb == 0) pa[u] = pr[u];
+          else pb[u] = pr[u];
+        }
+      }
+      if (pass == 0) {
+        const bool a_first = ew.term[0] == chains[0].op[1].out;
+        float4 c[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const float4 t0 = a_first ? pa[u] : pb[u], t1 = a_first ? pb[u] : pa[u];
+          c[u] = act4(ew.act, add4(add4(zero, t0), t1));
+        }
+        store(ew, rings[2], c);
+      }
+    } else {
+      const EwOp* o = chains[0].op;
+      float4 a[R], t0[R], t1[R];
+      acc_of(0, a);
+      load(o[0].term[0], t0);
+      load(o[0].term[1], t1);
+      float4 d0[R];
+#pragma unroll
+      for (int u = 0; u < R; ++u) d0[u] = add4(add4(a[u], t0[u]), t1[u]);
+      float4 f10[R], f11[R], f20[R], f21[R];
+      load(o[1].fac[0], f10);
+      load(o[1].fac[1], f11);
+      load(o[2].fac[0], f20);
+      load(o[2].fac[1], f21);
+      float4 d1[R], e10[R], e11[R], d2[R], e20[R], e21[R];
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        d1[u] = add4(zero, d0[u]);
+        e10[u] = mul4(d1[u], f11[u]);
+        e11[u] = mul4(d1[u], f10[u]);
+        d2[u] = add4(zero, d0[u]);
+        e20[u] = mul4(d2[u], f21[u]);
+        e21[u] = mul4(d2[u], f20[u]);
+      }
+      if (pass == 0) {
+        // the two gate deltas: eps k of ops 1 / 2 through f' of their y
+#pragma unroll
+        for (int q = 3; q <= 4; ++q) {
+          const float* src = o[q].term[0];
+          float4 y[R], v[R];
+          load(o[q].y, y);
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            const float4 s = src == o[1].eps[0] ? e10[u] : src == o[1].eps[1] ? e11[u]
+                           : src == o[2].eps[0] ? e20[u] : e21[u];
+            v[u] = mul4(add4(zero, s), dact4(o[q].act, y[u]));
+          }
+          store_to(o[q].out, v);
+        }
+      } else {
+        store_to(o[0].out, d0);
+        store_to(o[1].out, d1);
+        store_to(o[1].eps[0], e10);
+        store_to(o[1].eps[1], e11);
+        store_to(o[2].out, d2);
+        store_to(o[2].eps[0], e20);
+        store_to(o[2].eps[1], e21);
+      }
+    }
+  }
+}
+
 // A chain over rows [r_lo, r_hi) x units [u0, u0 + bu) of the tile; with
 // `acc`, op 0 takes the staged accumulator columns [c0, c0 + bu) of tile_s.
 // 16-byte groups, R rows per thread and pass (one operand latency per op
@@ -2077,7 +2233,7 @@ __device__ __forceinline__ void frame_chain(const EwChain& ch, const float* tile
 // one MMA of N = njobs * bu covers them all and the step's elementwise ops
 // (the cell update reading both gates' products) are element-local to the
 // tile: they run in the epilogue instead of behind another grid barrier.
-constexpr int kFrameThreads = 384;  // warps 0-7 convert + epilogue, 8 / 10 TMA, 9 MMA, 11 L2 prefetch
+constexpr int kFrameThreads = 512;  // warps 0-7 convert + epilogue, 8 / 10 TMA, 9 MMA, 11 L2 prefetch, 12-15 stores
 
 template <int BN>
 __global__ void __launch_bounds__(kFrameThreads, 1)
@@ -2095,7 +2251,9 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
   uint64_t* acc_empty = done + 1;        // epilogue has read the accumulator
   uint64_t* part_ready = acc_empty + 1;  // split-K: partial tiles of the cluster staged
   uint64_t* read_done = part_ready + 1;  // split-K: peers finished reading this CTA's tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(read_done + 1);
+  uint64_t* st_go = read_done + 1;       // LSTM patterns: pass 1 of a frame may start
+  uint64_t* st_done = st_go + 1;         // LSTM patterns: pass 1 of a frame is done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_done + 1);
   EwChain* chains = reinterpret_cast<EwChain*>(smem + NST * C::STAGE_BYTES + C::TILE_BYTES + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -2123,6 +2281,8 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
     mbar_init(acc_empty, 1);
     mbar_init(part_ready, csplit);
     mbar_init(read_done, csplit);
+    mbar_init(st_go, 1);
+    mbar_init(st_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 9) {
@@ -2139,8 +2299,28 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // registers: the converter / epilogue warp groups get 168, the producer
+  // group 48, the store group keeps 128 (2 x 128 x 168 + 128 x 48 + 128 x 128 = 64K)
+  if (warp >= 12) {
+    // ---- LSTM patterns: pass 1 (the non-critical outputs) of each frame,
+    // overlapping the next frame's main loop ----
+    if (fl.pattern) {
+    const int stid = threadIdx.x - 384;
+    const int rlo = csplit > 1 ? split * BM / csplit : 0;
+    const int rhi = min(csplit > 1 ? (split + 1) * BM / csplit : BM, M - m0);
+    for (int f = 0; f < fl.nframes; ++f) {
+      mbar_wait(st_go, f & 1);
+      const GemmGroup& pf = fl.frames[f];
+      RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)f * fl.n_ew].ring : pf.ring};
+      lstm_chains<2>(fl.pattern, 1, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, rlo, rhi, stid, 128);
+      asm volatile("bar.sync 5, 128;" ::: "memory");
+      if (stid == 0) mbar_arrive(st_done);
+    }
+    }
+  } else if (warp < 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
   if (warp == 11) {
-    if (!fl.prefetch) goto tail;
+    if (fl.prefetch) {
     // ---- L2 prefetch of frame f's epilogue operands (the chains' inputs that
     // do not come from the accumulator: hoisted partials, gate activations,
     // delayed state, co-factors, ...) while the main loop runs: the chains
@@ -2173,6 +2353,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
           }
         }
       }
+    }
     }
   } else if (warp == 8 || warp == 10) {
     if (lane == 0) {
@@ -2247,7 +2428,10 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
         mma_commit(done);
       }
     }
-  } else {
+  }
+  }
+  if (warp < 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
     // ---- warps 0-7: converters, then per frame the epilogue and the
     // elementwise steps ----
     const int tid = threadIdx.x;
@@ -2295,6 +2479,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
         mbar_arrive(&conv_full[s]);
       }
       // ---- epilogue of frame f ----
+      if (fl.pattern && f > 0) mbar_wait(st_done, (f - 1) & 1);  // pass 1 of f-1 done with tile_s / chains
       for (int j = 0; j < J; ++j) stage_chain(&chains[j], pf.job[j].epi, tid, 256);
       if (fl.fuse_ew)
         for (int e = 0; e < fl.n_ew; ++e) stage_chain(&chains[J + e], fl.ew[(size_t)f * fl.n_ew + e].chain[0], tid, 256);
@@ -2367,7 +2552,10 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
 #endif
       const int rows_hi = min(r_hi, M - m0);
       const int nch = J + (fl.fuse_ew ? fl.n_ew : 0);
-      if (fl.forward && chains_vec_ok(chains, nch, N) && min(bu, N - u0) % 4 == 0) {
+      if (fl.pattern) {
+        RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)f * fl.n_ew].ring : pf.ring};
+        lstm_chains<2>(fl.pattern, 0, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid, 256);
+      } else if (fl.forward && chains_vec_ok(chains, nch, N) && min(bu, N - u0) % 4 == 0) {
         RingWrite rings[4];
         for (int c = 0; c < nch; ++c) rings[c] = c < J ? pf.ring : fl.ew[(size_t)f * fl.n_ew + (c - J)].ring;
         frame_chains_fused<2>(chains, J, nch, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid);
@@ -2391,6 +2579,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid == 0) FL_MARK(f, 4);
       if (tid == 0) grid_arrive(fl.bar, gridDim.x);
+      if (fl.pattern && tid == 0) mbar_arrive(st_go);  // the store warps take the rest of the frame
       // ---- unfused elementwise steps of frame f (all CTAs, between grid barriers) ----
       for (int e = 0; e < (fl.fuse_ew ? 0 : fl.n_ew); ++e) {
         const EwLaunch& L = fl.ew[(size_t)f * fl.n_ew + e];
@@ -2428,7 +2617,6 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       }
     }
   }
-tail:
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (csplit > 1) cluster_sync();  // peers' last DSMEM reads of this CTA's tile are done
   else __syncthreads();
@@ -2694,7 +2882,7 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
 // run, preferring no split (no DSMEM reduction).  fuse_ew: the elementwise
 // steps are element-local over the jobs' width and run in the epilogue.
 int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const EwLaunch* d_ew, int n_ew,
-                         int fuse_ew, int nframes, unsigned* bar, cudaStream_t s) {
+                         int fuse_ew, int pattern, int nframes, unsigned* bar, cudaStream_t s) {
   GemmGroup p = g0;
   p.terms = g_tc_terms;
   if (!p.tma || p.njobs < 1 || p.njobs > 4) return -1;
@@ -2749,7 +2937,13 @@ int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const E
     const char* e = getenv("RGB_FL_FORWARD");
     fwd = e ? atoi(e) != 0 : 0;  // off: the register-forwarding evaluator spills (168-register cap) and measured slower
   }
-  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, bar};
+  static int pat_env = -1;  // RGB_FL_PATTERN=0: the generic chain evaluator (experiments)
+  if (pat_env < 0) {
+    const char* e = getenv("RGB_FL_PATTERN");
+    pat_env = e ? atoi(e) != 0 : 1;
+  }
+  if (!pat_env || (pattern == 1 && !(J == 2 && bu % 4 == 0)) || (pattern == 2 && J != 1)) pattern = 0;
+  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, bar};
   auto launch = [&](auto kernel, int smem) -> int {
     static bool bad = false;  // cooperative cluster launches unsupported: stay per-frame
     if (bad) return -1;

@@ -462,5 +462,5 @@ def test_persistent_frame_loop_matches_oracle(S):
             assert ta.loss() == tb.loss()
         assert torch.equal(wa.flat, wb.flat)
     finally:
-        _lib.check(L.rgb_set_frame_loop(0))
+        _lib.check(L.rgb_set_frame_loop(1))
         _lib.check(L.rgb_set_wavefront(1))
