@@ -425,8 +425,8 @@ def test_cfg4_shape_tf32_mode(_tf32):
     assert worst < TF32_STEP_BOUND
 
 
-@pytest.mark.parametrize("S", [256])
-def test_persistent_frame_loop_matches_oracle(S):
+@pytest.mark.parametrize("S,frame_loop", [(256, 1), (256, 0)])
+def test_persistent_frame_loop_matches_oracle(S, frame_loop):
     """The persistent tensor-core frame loop (rgb_set_frame_loop(1): one
     cooperative launch per recurrent loop, grid barrier per frame, split-K
     through DSMEM, the LSTM cell update fused into the epilogue) against the
@@ -434,7 +434,7 @@ def test_persistent_frame_loop_matches_oracle(S):
     bit for bit equal to its eager steps."""
     from test_gpu_engine import run_pair
     L = _lib.lib()
-    _lib.check(L.rgb_set_frame_loop(1))
+    _lib.check(L.rgb_set_frame_loop(frame_loop))  # 0: the per-frame PDL launches of the same loops
     _lib.check(L.rgb_set_wavefront(0))  # (the wavefront runs frame loops per block, per-frame launches)
     n0 = ctypes.c_int64()
     _lib.check(L.rgb_launch_count(ctypes.byref(n0)))
@@ -442,9 +442,9 @@ def test_persistent_frame_loop_matches_oracle(S):
         assert run_pair(P.build_stacked_lstm(256, [512, 512], 256), S, 16, 8, 3, 1e-3, 7) < 1e-4
         n1 = ctypes.c_int64()
         _lib.check(L.rgb_launch_count(ctypes.byref(n1)))
-        # 3 iterations x (2 forward + 2 backward loops): the per-frame schedule would
-        # launch >= 8 + 16 kernels per loop pair; the frame loops keep it well below
-        assert n1.value - n0.value < 3 * 60
+        # 3 iterations x (2 forward + 2 backward loops): the per-frame schedule
+        # launches >= 8 + 16 kernels per loop pair; the frame loops keep it well below
+        assert (n1.value - n0.value < 3 * 60) == bool(frame_loop)
         net = P.build_stacked_lstm(128, [512, 512], 128)
         cfg = P.TrainConfig(h=16, h_prime=8, lr=1e-4, iterations=1)  # raw gradient sums over S streams
         wa, wb = P.Weights.init(net, 2), P.Weights.init(net, 2)
