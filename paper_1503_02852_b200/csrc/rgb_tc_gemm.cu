@@ -1726,6 +1726,7 @@ struct FrameLoop {
   int prefetch;             // 1: warp 11 prefetches the chains' operands into L2 (off by default)
   int forward;              // 1: fused chain evaluation with register forwarding (frame_chains_fused)
   int pattern;              // 1 / 2: the LSTM cell forward / backward chains (lstm_chains), 0: generic
+  int preload;              // 1: the pattern's operands are loaded before the split-K reduction (lstm_pre)
   unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
 };
 
@@ -2175,6 +2176,167 @@ __device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain
   }
 }
 
+// Pass 0 of lstm_chains split in two around the split-K reduction: every
+// operand that does not come from the accumulator (hoisted pre-activations,
+// gate outputs, cell(t-1) stored one frame earlier, the eps the store warps
+// wrote behind the previous barrier) is copied into shared memory by bulk
+// copies (one per operand row) first, so the loads overlap the DSMEM
+// reduction; the second half reads the reduced accumulator, evaluates two row
+// groups at a time and stores.  Operand k's slab (rows [r_lo, r_hi) x the
+// tile's units) is the pipeline's A region (even k) or B_lo region (odd k) of
+// stage k / 2: idle from the frame's last MMA until the next frame's A loads
+// (which wait for this CTA's barrier arrival) and conversions (done by these
+// same threads).  Same operands and arithmetic order as lstm_chains pass 0.
+__device__ __forceinline__ int lstm_nops(int pattern) { return pattern == 1 ? 4 : 6; }
+
+template <int SLAB>
+__device__ __forceinline__ bool lstm_pre_ok(int bu, int N, int u0, int r_lo, int r_hi) {
+  const int ncols = min(bu, N - u0);
+  if (ncols <= 0 || r_hi <= r_lo) return true;  // nothing to do
+  return ncols % 4 == 0 && N % 4 == 0 && u0 % 4 == 0 && (r_hi - r_lo) * ncols * 4 <= SLAB;
+}
+
+__device__ __forceinline__ const float* lstm_bwd_fac(const EwOp* o, int q) {
+  const float* src = o[q].term[0];
+  return src == o[1].eps[0] ? o[1].fac[1] : src == o[1].eps[1] ? o[1].fac[0]
+       : src == o[2].eps[0] ? o[2].fac[1] : o[2].fac[0];
+}
+
+__device__ __forceinline__ const float* lstm_operand(int pattern, const GemmGroup& pg, int k) {
+  if (pattern == 1) {
+    const EwOp &o0 = pg.job[k >> 1].epi.op[0], &o1 = pg.job[k >> 1].epi.op[1];
+    return (k & 1) ? o1.fac[o1.fac[0] == o0.out ? 1 : 0] : o0.term[0];
+  }
+  const EwOp* o = pg.job[0].epi.op;
+  switch (k) {
+    case 0: return o[0].term[0];
+    case 1: return o[0].term[1];
+    case 2: return lstm_bwd_fac(o, 3);
+    case 3: return lstm_bwd_fac(o, 4);
+    case 4: return o[3].y;
+    default: return o[4].y;
+  }
+}
+
+template <int STAGE_BYTES, int A_BYTES, int B_BYTES>
+__device__ __forceinline__ uint32_t lstm_slab(uint32_t pipe, int k) {
+  return pipe + (k >> 1) * STAGE_BYTES + ((k & 1) ? A_BYTES + B_BYTES : 0);
+}
+
+// the store warps: 16-byte cp.async of every operand element group, arriving
+// on `full` (count nthr) when this thread's copies have landed
+template <int STAGE_BYTES, int A_BYTES, int B_BYTES>
+__device__ __forceinline__ void lstm_pre(int pattern, const GemmGroup& pg, int m0, int u0, int bu, int N, int r_lo,
+                                         int r_hi, int tid, int nthr, uint32_t pipe, uint64_t* full) {
+  const int ncols = max(0, min(bu, N - u0)), rows = max(0, r_hi - r_lo), np = lstm_nops(pattern);
+  const int g4 = ncols / 4, per_k = rows * g4;
+  const uint32_t row_bytes = (uint32_t)ncols * 4u;
+  const float* ptr[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) ptr[k] = k < np ? lstm_operand(pattern, pg, k) : nullptr;
+  for (int it = tid; it < np * per_k; it += nthr) {
+    const int k = it / per_k, rem = it - k * per_k, r = rem / g4, c4 = rem - r * g4;
+    const float* src = ptr[k] + ((int64_t)(m0 + r_lo + r) * N + u0 + 4 * c4);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(lstm_slab<STAGE_BYTES, A_BYTES, B_BYTES>(pipe, k) +
+                                                                    (uint32_t)r * row_bytes + 16u * c4),
+                 "l"(__cvta_generic_to_global(src))
+                 : "memory");
+  }
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(full)) : "memory");
+}
+
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+template <int STAGE_BYTES, int A_BYTES, int B_BYTES>
+__device__ __forceinline__ void lstm_post(int pattern, const EwChain* chains, const RingWrite* rings,
+                                          const float* tile_s, int ld, int m0, int u0, int bu, int N, int r_lo,
+                                          int r_hi, int tid, int nthr, uint32_t pipe) {
+  const int ncols = min(bu, N - u0);
+  if (ncols <= 0 || r_hi <= r_lo) return;
+  const int g4 = ncols / 4, lanes = nthr / g4 * g4;
+  if (tid >= lanes) return;
+  const int g = tid % g4, layer = tid / g4, layers = lanes / g4;
+  const int j = u0 + 4 * g;
+  const uint32_t row_bytes = (uint32_t)ncols * 4u;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const EwOp* o = chains[0].op;
+  auto v = [&](int rl, int k) {
+    return lds4(lstm_slab<STAGE_BYTES, A_BYTES, B_BYTES>(pipe, k) + (uint32_t)(rl - r_lo) * row_bytes + 16u * g);
+  };
+  constexpr int U = 2;  // row groups in flight per thread
+#pragma unroll 1
+  for (int rb = r_lo + layer; rb < r_hi; rb += U * layers) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int rq = rb + u * layers;
+      const bool ok = rq < r_hi;
+      const int rl = ok ? rq : rb;
+      const int64_t rr = m0 + rl, e = rr * N + j;
+      if (pattern == 1) {
+        const EwOp& ew = chains[2].op[0];
+        float4 pr[2];
+#pragma unroll
+        for (int jb = 0; jb < 2; ++jb) {
+          const EwOp &o0 = chains[jb].op[0], &o1 = chains[jb].op[1];
+          const float4 a = *reinterpret_cast<const float4*>(tile_s + rl * ld + jb * bu + 4 * g);
+          const float4 gt = act4(o0.act, add4(a, v(rl, 2 * jb)));
+          pr[jb] = o1.fac[0] == o0.out ? mul4(gt, v(rl, 2 * jb + 1)) : mul4(v(rl, 2 * jb + 1), gt);
+        }
+        const bool a_first = ew.term[0] == chains[0].op[1].out;
+        const float4 t0 = a_first ? pr[0] : pr[1], t1 = a_first ? pr[1] : pr[0];
+        const float4 c = act4(ew.act, add4(add4(zero, t0), t1));
+        if (ok) ring_store4(ew.out, e, rr, N, ew.out_is_ring, rings[2], c);
+      } else {
+        const float4 a = *reinterpret_cast<const float4*>(tile_s + rl * ld + 4 * g);
+        const float4 d = add4(zero, add4(add4(a, v(rl, 0)), v(rl, 1)));
+#pragma unroll
+        for (int q = 3; q <= 4; ++q) {
+          const float4 s = mul4(d, v(rl, q - 1));
+          const float4 w = mul4(add4(zero, s), dact4(o[q].act, v(rl, q + 1)));
+          if (ok) st4(o[q].out, e, w);
+        }
+      }
+    }
+  }
+}
+
+// Sums rows [r_lo, r_hi) of the csplit partial tiles of a cluster (DSMEM,
+// split order) into this CTA's tile_s; NB remote loads per thread in flight
+// (a DSMEM round trip is ~200 cycles; serial loads made this 3.5 us).
+template <int G4, int NB>
+__device__ __forceinline__ void reduce_split_rows(float* tile_s, int ld, int r_lo, int r_hi, int csplit, int tid) {
+  const int nq = (r_hi - r_lo) * G4;
+  for (int q0 = tid; q0 < nq; q0 += 256 * NB) {
+    float4 a[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int q = q0 + 256 * i;
+      const int off = (r_lo + q / G4) * ld + (q % G4) * 4;
+      a[i] = q < nq ? ld_dsmem4(tile_s + off, 0u) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int k = 1; k < csplit; ++k) {
+      float4 b[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int q = q0 + 256 * i;
+        const int off = (r_lo + q / G4) * ld + (q % G4) * 4;
+        b[i] = q < nq ? ld_dsmem4(tile_s + off, (uint32_t)k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) a[i] = add4(a[i], b[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int q = q0 + 256 * i;
+      if (q < nq) *reinterpret_cast<float4*>(tile_s + (r_lo + q / G4) * ld + (q % G4) * 4) = a[i];
+    }
+  }
+}
+
 // A chain over rows [r_lo, r_hi) x units [u0, u0 + bu) of the tile; with
 // `acc`, op 0 takes the staged accumulator columns [c0, c0 + bu) of tile_s.
 // 16-byte groups, R rows per thread and pass (one operand latency per op
@@ -2253,7 +2415,8 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
   uint64_t* read_done = part_ready + 1;  // split-K: peers finished reading this CTA's tile
   uint64_t* st_go = read_done + 1;       // LSTM patterns: pass 1 of a frame may start
   uint64_t* st_done = st_go + 1;         // LSTM patterns: pass 1 of a frame is done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_done + 1);
+  uint64_t* pre_full = st_done + 1;      // LSTM patterns: the frame's chain operands are in shared memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pre_full + 1);
   EwChain* chains = reinterpret_cast<EwChain*>(smem + NST * C::STAGE_BYTES + C::TILE_BYTES + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -2283,6 +2446,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
     mbar_init(read_done, csplit);
     mbar_init(st_go, 1);
     mbar_init(st_done, 1);
+    mbar_init(pre_full, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 9) {
@@ -2308,13 +2472,22 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
     const int stid = threadIdx.x - 384;
     const int rlo = csplit > 1 ? split * BM / csplit : 0;
     const int rhi = min(csplit > 1 ? (split + 1) * BM / csplit : BM, M - m0);
-    for (int f = 0; f < fl.nframes; ++f) {
-      mbar_wait(st_go, f & 1);
-      const GemmGroup& pf = fl.frames[f];
-      RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)f * fl.n_ew].ring : pf.ring};
-      lstm_chains<2>(fl.pattern, 1, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, rlo, rhi, stid, 128);
-      asm volatile("bar.sync 5, 128;" ::: "memory");
-      if (stid == 0) mbar_arrive(st_done);
+    const bool use_pre = NST >= 3 && fl.preload && lstm_pre_ok<(C::A_BYTES < C::B_BYTES ? C::A_BYTES : C::B_BYTES)>(bu, N, u0, rlo, rhi);
+    const uint32_t pipe = smem_u32(smem);
+    for (int f = 0; f <= fl.nframes; ++f) {
+      if (f > 0) {  // pass 1 of frame f - 1
+        mbar_wait(st_go, (f - 1) & 1);
+        const GemmGroup& pf = fl.frames[f - 1];
+        RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)(f - 1) * fl.n_ew].ring : pf.ring};
+        lstm_chains<2>(fl.pattern, 1, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, rlo, rhi, stid, 128);
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+        if (stid == 0) mbar_arrive(st_done);
+      }
+      if (use_pre && f < fl.nframes) {  // frame f's chain operands, once its MMAs are done with the slabs
+        mbar_wait(done, f & 1);
+        lstm_pre<C::STAGE_BYTES, C::A_BYTES, C::B_BYTES>(fl.pattern, fl.frames[f], m0, u0, bu, N, rlo, rhi, stid,
+                                                          128, pipe, pre_full);
+      }
     }
     }
   } else if (warp < 12) {
@@ -2483,6 +2656,12 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       for (int j = 0; j < J; ++j) stage_chain(&chains[j], pf.job[j].epi, tid, 256);
       if (fl.fuse_ew)
         for (int e = 0; e < fl.n_ew; ++e) stage_chain(&chains[J + e], fl.ew[(size_t)f * fl.n_ew + e].chain[0], tid, 256);
+      // the rows this CTA finishes (split-K: its slice of the reduced tile)
+      const int r_lo = csplit > 1 ? split * BM / csplit : 0, r_hi = csplit > 1 ? (split + 1) * BM / csplit : BM;
+      const int rows_hi = min(r_hi, M - m0);
+      const uint32_t pipe = smem_u32(smem);
+      const bool use_pre = NST >= 3 && fl.pattern && fl.preload &&
+                           lstm_pre_ok<(C::A_BYTES < C::B_BYTES ? C::A_BYTES : C::B_BYTES)>(bu, N, u0, r_lo, rows_hi);
       if (csplit > 1 && f > 0) mbar_wait_cluster(read_done, (f - 1) & 1);  // peers done with tile_s
       mbar_wait(done, f & 1);
       if (tid == 0) FL_MARK(f, 1);
@@ -2507,42 +2686,11 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid == 0) mbar_arrive(acc_empty);
       if (tid == 0) FL_MARK(f, 2);
-      int r_lo = 0, r_hi = BM;
       if (csplit > 1) {
         // this CTA sums rows [r_lo, r_hi) of the cluster's partial tiles in split order
         if (tid < csplit) mbar_arrive_cluster(part_ready, (uint32_t)tid);
         mbar_wait_cluster(part_ready, f & 1);
-        r_lo = split * BM / csplit;
-        r_hi = (split + 1) * BM / csplit;
-        // every remote load of a batch is issued before the first is used
-        // (a DSMEM round trip is ~200 cycles; serial loads made this 3.5 us)
-        constexpr int G4 = BN / 4;
-        const int nq = (r_hi - r_lo) * G4;
-        for (int q0 = tid; q0 < nq; q0 += 256 * 8) {
-          float4 a[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int q = q0 + 256 * i;
-            const int off = (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4;
-            a[i] = q < nq ? ld_dsmem4(tile_s + off, 0u) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          for (int k = 1; k < csplit; ++k) {
-            float4 b[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int q = q0 + 256 * i;
-              const int off = (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4;
-              b[i] = q < nq ? ld_dsmem4(tile_s + off, (uint32_t)k) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = add4(a[i], b[i]);
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int q = q0 + 256 * i;
-            if (q < nq) *reinterpret_cast<float4*>(tile_s + (r_lo + q / G4) * C::EPI_LD + (q % G4) * 4) = a[i];
-          }
-        }
+        reduce_split_rows<BN / 4, 8>(tile_s, C::EPI_LD, r_lo, r_hi, csplit, tid);
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (tid < csplit) mbar_arrive_cluster(read_done, (uint32_t)tid);
       }
@@ -2550,11 +2698,16 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
 #ifdef RGB_FL_TRACE
       if (tid == 0 && blockIdx.x == 0) g_fl_frame = f;
 #endif
-      const int rows_hi = min(r_hi, M - m0);
       const int nch = J + (fl.fuse_ew ? fl.n_ew : 0);
       if (fl.pattern) {
         RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)f * fl.n_ew].ring : pf.ring};
-        lstm_chains<2>(fl.pattern, 0, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid, 256);
+        if (use_pre) {
+          mbar_wait(pre_full, f & 1);  // the store warps' copies of the chain operands
+          lstm_post<C::STAGE_BYTES, C::A_BYTES, C::B_BYTES>(fl.pattern, chains, rings, tile_s, C::EPI_LD, m0, u0,
+                                                             bu, N, r_lo, rows_hi, tid, 256, pipe);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the next frame's TMA reuses the slabs
+        } else
+          lstm_chains<2>(fl.pattern, 0, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, r_lo, rows_hi, tid, 256);
       } else if (fl.forward && chains_vec_ok(chains, nch, N) && min(bu, N - u0) % 4 == 0) {
         RingWrite rings[4];
         for (int c = 0; c < nch; ++c) rings[c] = c < J ? pf.ring : fl.ew[(size_t)f * fl.n_ew + (c - J)].ring;
@@ -2943,7 +3096,12 @@ int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const E
     pat_env = e ? atoi(e) != 0 : 1;
   }
   if (!pat_env || (pattern == 1 && !(J == 2 && bu % 4 == 0)) || (pattern == 2 && J != 1)) pattern = 0;
-  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, bar};
+  static int preload = -1;  // RGB_FL_PRELOAD=0: the pattern's operands are loaded after the reduction
+  if (preload < 0) {
+    const char* e = getenv("RGB_FL_PRELOAD");
+    preload = e ? atoi(e) != 0 : 1;
+  }
+  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, preload, bar};
   auto launch = [&](auto kernel, int smem) -> int {
     static bool bad = false;  // cooperative cluster launches unsupported: stay per-frame
     if (bad) return -1;
