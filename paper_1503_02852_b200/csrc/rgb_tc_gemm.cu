@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 
 #include "rgb_ew.cuh"
 #include "rgb_kernels.cuh"
@@ -1160,15 +1161,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // tile geometry shared by every role of the persistent kernel
 template <int BN, bool IS_DW, bool PAIR, class P>
 struct PTile {
-  int jid, m0, n0, nb0, M, N, nstages;
-  __device__ __forceinline__ PTile(const P& p, int t, uint32_t rank) {
+  int jid, m0, n0, nb0, M, N, nstages, width;
+  // t >= tail: the last wave's tiles cut in two column halves (tail split),
+  // half h of tile tail + h / 2
+  __device__ __forceinline__ PTile(const P& p, int t, uint32_t rank, int tail) {
     constexpr int NCTA = PAIR ? 2 : 1;
-    int tile;
+    int tile, half = -1;
+    if (t >= tail) {
+      half = (t - tail) & 1;
+      t = tail + (t - tail) / 2;
+    }
     find_job(p.tile_start, p.njobs, t, jid, tile);
     const int tiles_n = p.tiles_n[jid];
     m0 = (tile / tiles_n) * (BM * NCTA) + (int)rank * BM;
     n0 = (tile % tiles_n) * BN;
-    nb0 = n0 + (int)rank * (BN / NCTA);
+    width = BN;
+    if (half >= 0) {
+      width = BN / 2;
+      n0 += half * width;
+    }
+    nb0 = n0 + (int)rank * (width / NCTA);
     if constexpr (IS_DW) {
       M = p.job[jid].m;
       N = p.job[jid].n;
@@ -1183,7 +1195,7 @@ struct PTile {
 };
 
 template <int BN, bool IS_DW, bool PAIR, class P>
-__global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles, int kc) {
+__global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles, int kc, int tail) {
   constexpr int NCTA = PAIR ? 2 : 1;
   constexpr int BNL = BN / NCTA;
   using C = PCfg<BN, BNL>;
@@ -1251,7 +1263,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
         const bool load_a = warp == 12;
         int g = 0;  // global stage counter
         for (int t = first; t < ntiles; t += stride) {
-          const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+          const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
           const auto& job = p.job[T.jid];
           int seg = 0, k0 = 0;
           for (int it = 0; it < T.nstages; ++it, ++g) {
@@ -1278,13 +1290,15 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
       }
     } else if (warp == 13 && lane == 0 && rank == 0) {
       // ---------------- MMA issuer: every chunk into a fresh X ----------------
-      const uint32_t idesc = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+      const uint32_t idesc_full = idesc_tf32(BM * NCTA, BN, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
+      const uint32_t idesc_half = idesc_tf32(BM * NCTA, BN / 2, IS_DW ? 1 : 0, IS_DW ? 1 : 0);
       const bool split = p.terms != 1;
       int g = 0, xc = 0;
       for (int t = first; t < ntiles; t += stride) {
-        const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+        const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
         int xb = -1, chunk_end = 0;
         uint32_t acc = tmem;
+        const uint32_t idesc = T.width == BN ? idesc_full : idesc_half;
         for (int it = 0; it < T.nstages; ++it, ++g) {
           if (it == chunk_end) {  // next chunk: the other accumulator, once the epilogue folded it
             if (xb >= 0) {
@@ -1349,7 +1363,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     // ---------------- converters (warps 0-3) ----------------
     int g = 0;
     for (int t = first; t < ntiles; t += stride) {
-      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
       for (int it = 0; it < T.nstages; ++it, ++g) {
         const int s = g % NST;
         mbar_wait(&tma_full[s], (g / NST) & 1);
@@ -1408,13 +1422,14 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     float R[HALF];
     int staged_job = -1, xc = 0;
     for (int t = first; t < ntiles; t += stride) {
-      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank);
+      const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
       const int nch = (T.nstages + kc - 1) / kc;
       for (int c = 0; c < nch; ++c, ++xc) {
         const int xb = xc & 1;
         mbar_wait(&x_full[xb], (xc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t xacc = tmem + xb * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+        // (a tail half tile folds stale columns into R too: never read)
 #pragma unroll
         for (int q = 0; q < HALF / 16; ++q) {
           float v[16];
@@ -1436,7 +1451,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           staged_job = T.jid;
         }
       }
-      const int ncols = (T.N - T.n0) < BN ? (T.N - T.n0) : BN;
+      const int ncols = (T.N - T.n0) < T.width ? (T.N - T.n0) : T.width;
       const int nrows = (T.M - T.m0) < BM ? (T.M - T.m0) : BM;
       bool vec;
       float* g_out = nullptr;
@@ -1575,6 +1590,20 @@ void launch_persistent(const P& p, int ntiles, int max_stages, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int units = PAIR ? sms / 2 : sms;
+  // tail split: when the last wave would hold at most half the units, its
+  // tiles run as column halves on twice as many units (one half-length wave
+  // instead of a full one; RGB_TC_TAIL=0 disables)
+  static int tail_env = -1;
+  if (tail_env < 0) {
+    const char* e = getenv("RGB_TC_TAIL");
+    tail_env = e ? atoi(e) != 0 : 1;
+  }
+  int tail = ntiles;
+  const int rem = ntiles % units;
+  if (!IS_DW && tail_env && ntiles > units && rem && 2 * rem <= units) {
+    tail = ntiles - rem;
+    ntiles += rem;
+  }
   const int blocks = (ntiles < units ? ntiles : units) * (PAIR ? 2 : 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
@@ -1588,7 +1617,7 @@ void launch_persistent(const P& p, int ntiles, int max_stages, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, p, ntiles, chunk_stages(p.terms, max_stages, IS_DW));
+  cudaLaunchKernelEx(&cfg, k, p, ntiles, chunk_stages(p.terms, max_stages, IS_DW), tail);
 }
 
 template <int BN, bool IS_DW, bool PAIR, class P>
@@ -2998,6 +3027,12 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
   }
   const int blocks = p.tile_start[p.njobs] * c.splits * (c.pair ? 2 : 1);
   if (blocks == 0) return 0;
+  static const bool log = getenv("RGB_TC_LOG") != nullptr;  // shape log (tuning)
+  if (log) {
+    fprintf(stderr, "[tc nt] rows %d jobs %d n0 %d kst %d nseg %d epi_ops %d bn %d pair %d splits %d tiles %d blocks %d persistent %d\n",
+            p.rows, p.njobs, p.job[0].n, nt_max_stages(p), p.job[0].nseg, p.job[0].epi.nops, c.bn, (int)c.pair,
+            c.splits, p.tile_start[p.njobs], blocks, (int)(p.tma && c.splits == 1 && use_persistent(blocks, c.bn, acc_stages)));
+  }
   if (p.tma && c.splits == 1 && use_persistent(blocks, c.bn, acc_stages)) {
     const int ntiles = p.tile_start[p.njobs];
     if (c.pair) {
