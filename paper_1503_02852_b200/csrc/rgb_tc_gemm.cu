@@ -1117,6 +1117,11 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // accumulations per chunk.  (Round 2 first kept R in TMEM beside a single
 // chunk accumulator at 256-column tiles, so the MMA waited for every fold:
 // ~6% of the cfg4 step; R in registers with two X removes the wait.)
+#ifndef RGB_PERS_SPEC
+// 1: the chain epilogue uses the specialised ops (every operand of an op
+// loaded before its first store: one memory latency per op instead of two)
+#define RGB_PERS_SPEC 1
+#endif
 #ifndef RGB_PERS_RE
 #define RGB_PERS_RE 2  // rows per thread per pass of the persistent epilogue's row walk
 #endif
@@ -1505,7 +1510,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
                         make_float4(p.alpha * a4[u].x, p.alpha * a4[u].y, p.alpha * a4[u].z, p.alpha * a4[u].w));
               } else {
                 const RingWrite ring = p.ring;
-                ew_chain_vec<RE, false>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
+                ew_chain_vec<RE, RGB_PERS_SPEC != 0>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
               }
             }
           }
