@@ -1117,6 +1117,9 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // accumulations per chunk.  (Round 2 first kept R in TMEM beside a single
 // chunk accumulator at 256-column tiles, so the MMA waited for every fold:
 // ~6% of the cfg4 step; R in registers with two X removes the wait.)
+#ifndef RGB_PERS_BWD3
+#define RGB_PERS_BWD3 1  // 1: product-layer backward chains through chain_bwd3
+#endif
 #ifndef RGB_PERS_SPEC
 // 1: the chain epilogue uses the specialised ops (every operand of an op
 // loaded before its first store: one memory latency per op instead of two)
@@ -1198,6 +1201,64 @@ struct PTile {
     }
   }
 };
+
+// The backward chain of a product layer fed by a GEMM (the LSTM out_prod:
+// engine.py:519-566): op 0 d = acc, eps_i = d * f_(1-i) over two co-factors;
+// ops 1, 2 the two factor layers' deltas  d_q = (0 + eps_k) * f'(y_q).  Every
+// operand the three ops read from memory (the co-factors, y_1, y_2) is loaded
+// up front and the eps are forwarded in registers: one memory latency per row
+// group instead of one per op.  Arithmetic exactly as ew_apply_vec.
+__device__ __forceinline__ bool chain_is_bwd3(const EwChain& ch) {
+  if (ch.nops != 3) return false;
+  const EwOp& o = ch.op[0];
+  if (o.kind != EW_BWD || o.act != ACT_IDENTITY || o.nterm || o.base || o.nrank1 || o.nfac != 2 || !o.eps[0] ||
+      !o.eps[1] || o.inj || o.y)
+    return false;
+  for (int q = 1; q <= 2; ++q) {
+    const EwOp& d = ch.op[q];
+    if (d.kind != EW_BWD || (d.act != ACT_SIGMOID && d.act != ACT_TANH) || d.nterm != 1 || d.base || d.nrank1 ||
+        d.nfac || d.inj || !d.y || (d.term[0] != o.eps[0] && d.term[0] != o.eps[1]))
+      return false;
+    // the deltas must not overwrite an operand a later op of the chain reads
+    if (d.out == o.fac[0] || d.out == o.fac[1] || d.out == o.eps[0] || d.out == o.eps[1] || d.out == o.out) return false;
+  }
+  if (ch.op[1].out == ch.op[2].y || ch.op[2].out == ch.op[1].y || ch.op[1].out == ch.op[2].out) return false;
+  return true;
+}
+
+__device__ __forceinline__ float4 bwd3_dact(int act, float4 y) {
+  return make_float4(act_deriv(act, y.x), act_deriv(act, y.y), act_deriv(act, y.z), act_deriv(act, y.w));
+}
+
+template <int R>
+__device__ __forceinline__ void chain_bwd3(const EwChain& ch, int width, const int64_t (&r)[R], int j,
+                                           const bool (&ok)[R], const float4 (&acc)[R]) {
+  const EwOp &o = ch.op[0], &p1 = ch.op[1], &p2 = ch.op[2];
+  const float4 one = make_float4(1.f, 1.f, 1.f, 1.f), zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t e[R];
+  float4 f0[R], f1[R], y1[R], y2[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    e[u] = r[u] * width + j;
+    f0[u] = ok[u] ? ld4(o.fac[0], e[u]) : one;
+    f1[u] = ok[u] ? ld4(o.fac[1], e[u]) : one;
+    y1[u] = ok[u] ? ld4(p1.y, e[u]) : zero;
+    y2[u] = ok[u] ? ld4(p2.y, e[u]) : zero;
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    if (!ok[u]) continue;
+    const float4 d = acc[u];
+    const float4 e0 = mul4(d, f1[u]), e1 = mul4(d, f0[u]);
+    st4(o.out, e[u], d);
+    st4(o.eps[0], e[u], e0);
+    st4(o.eps[1], e[u], e1);
+    const float4 t1 = p1.term[0] == o.eps[0] ? e0 : e1;
+    const float4 t2 = p2.term[0] == o.eps[0] ? e0 : e1;
+    st4(p1.out, e[u], mul4(add4(zero, t1), bwd3_dact(p1.act, y1[u])));
+    st4(p2.out, e[u], mul4(add4(zero, t2), bwd3_dact(p2.act, y2[u])));
+  }
+}
 
 template <int BN, bool IS_DW, bool PAIR, class P>
 __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __grid_constant__ P p, int ntiles, int kc, int tail) {
@@ -1426,6 +1487,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     auto gsync = [&] { asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory"); };
     float R[HALF];
     int staged_job = -1, xc = 0;
+    bool bwd3 = false;  // the staged chain is the product-layer backward chain (chain_bwd3)
     for (int t = first; t < ntiles; t += stride) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
       const int nch = (T.nstages + kc - 1) / kc;
@@ -1454,6 +1516,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           stage_chain(my_chain, p.job[T.jid].epi, et, 128);
           gsync();
           staged_job = T.jid;
+          bwd3 = RGB_PERS_BWD3 && chain_is_bwd3(*my_chain);
         }
       }
       const int ncols = (T.N - T.n0) < T.width ? (T.N - T.n0) : T.width;
@@ -1510,7 +1573,8 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
                         make_float4(p.alpha * a4[u].x, p.alpha * a4[u].y, p.alpha * a4[u].z, p.alpha * a4[u].w));
               } else {
                 const RingWrite ring = p.ring;
-                ew_chain_vec<RE, RGB_PERS_SPEC != 0>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
+                if (bwd3) chain_bwd3<RE>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, a4);
+                else ew_chain_vec<RE, RGB_PERS_SPEC != 0>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
               }
             }
           }
