@@ -1118,7 +1118,7 @@ void launch_one(P p, int tiles, cudaStream_t s) {
 // chunk accumulator at 256-column tiles, so the MMA waited for every fold:
 // ~6% of the cfg4 step; R in registers with two X removes the wait.)
 #ifndef RGB_PERS_BWD3
-#define RGB_PERS_BWD3 1  // 1: product-layer backward chains through chain_bwd3
+#define RGB_PERS_BWD3 1  // 1: product-layer chains through chain_bwd3 / chain_fwd2
 #endif
 #ifndef RGB_PERS_SPEC
 // 1: the chain epilogue uses the specialised ops (every operand of an op
@@ -1201,6 +1201,54 @@ struct PTile {
     }
   }
 };
+
+// The forward chain of a gate feeding a product layer (the LSTM out_gate ->
+// out_prod: engine.py:405-413 hoisted): op 0 g = act(acc + terms + rank-1),
+// op 1 p = f_0 * f_1 with g one of the factors.  The other factor, the terms
+// and the rank-1 operands are loaded up front and g is forwarded: one memory
+// latency per row group instead of two.  Arithmetic exactly as ew_apply_vec.
+__device__ __forceinline__ bool chain_is_fwd2(const EwChain& ch) {
+  if (ch.nops != 2) return false;
+  const EwOp &o = ch.op[0], &m = ch.op[1];
+  if (o.kind != EW_FWD_ADD || o.base || o.nterm > 2 || o.nrank1 > 1) return false;
+  if (m.kind != EW_FWD_MUL || m.nfac != 2 || (m.fac[0] != o.out) == (m.fac[1] != o.out)) return false;
+  for (int i = 0; i < o.nterm; ++i)
+    if (o.term[i] == o.out) return false;
+  return m.out != o.out && m.out != m.fac[0] && m.out != m.fac[1];
+}
+
+template <int R>
+__device__ __forceinline__ void chain_fwd2(const EwChain& ch, int width, const int64_t (&r)[R], int j,
+                                           const bool (&ok)[R], const RingWrite& ring, const float4 (&acc)[R]) {
+  const EwOp &o = ch.op[0], &m = ch.op[1];
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int gi = m.fac[0] == o.out ? 0 : 1;
+  int64_t e[R];
+  float4 t0[R], t1[R], x[R];
+  float src[R];
+  const bool r1 = o.nrank1 > 0;
+  const float4 w = r1 ? ld4(o.r1w[0], j) : zero;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    e[u] = r[u] * width + j;
+    t0[u] = (o.nterm > 0 && ok[u]) ? ld4(o.term[0], e[u]) : zero;
+    t1[u] = (o.nterm > 1 && ok[u]) ? ld4(o.term[1], e[u]) : zero;
+    x[u] = ok[u] ? ld4(m.fac[1 - gi], e[u]) : zero;
+    src[u] = (r1 && ok[u]) ? o.r1src[0][r[u]] : 0.0f;
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    if (!ok[u]) continue;
+    float4 v = acc[u];
+    if (o.nterm > 0) v = add4(v, t0[u]);
+    if (o.nterm > 1) v = add4(v, t1[u]);
+    if (r1) v = add4(v, make_float4(w.x * src[u], w.y * src[u], w.z * src[u], w.w * src[u]));
+    const float4 g = make_float4(act_apply(o.act, v.x), act_apply(o.act, v.y), act_apply(o.act, v.z),
+                                 act_apply(o.act, v.w));
+    ring_store4(o.out, e[u], r[u], width, o.out_is_ring, ring, g);
+    ring_store4(m.out, e[u], r[u], width, m.out_is_ring, ring, gi == 0 ? mul4(g, x[u]) : mul4(x[u], g));
+  }
+}
 
 // The backward chain of a product layer fed by a GEMM (the LSTM out_prod:
 // engine.py:519-566): op 0 d = acc, eps_i = d * f_(1-i) over two co-factors;
@@ -1488,6 +1536,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
     float R[HALF];
     int staged_job = -1, xc = 0;
     bool bwd3 = false;  // the staged chain is the product-layer backward chain (chain_bwd3)
+    bool fwd2 = false;  // ... the gate -> product forward chain (chain_fwd2)
     for (int t = first; t < ntiles; t += stride) {
       const PTile<BN, IS_DW, PAIR, P> T(p, t, rank, tail);
       const int nch = (T.nstages + kc - 1) / kc;
@@ -1517,6 +1566,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
           gsync();
           staged_job = T.jid;
           bwd3 = RGB_PERS_BWD3 && chain_is_bwd3(*my_chain);
+          fwd2 = RGB_PERS_BWD3 && chain_is_fwd2(*my_chain);
         }
       }
       const int ncols = (T.N - T.n0) < T.width ? (T.N - T.n0) : T.width;
@@ -1574,6 +1624,7 @@ __global__ void __launch_bounds__(kPersThreads, 1) tma_gemm_persistent(const __g
               } else {
                 const RingWrite ring = p.ring;
                 if (bwd3) chain_bwd3<RE>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, a4);
+                else if (fwd2) chain_fwd2<RE>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, a4);
                 else ew_chain_vec<RE, RGB_PERS_SPEC != 0>(*my_chain, T.N, rr, T.n0 + c0 + cl, ok, ring, true, a4);
               }
             }
