@@ -2336,6 +2336,9 @@ __device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain
 // stage k / 2: idle from the frame's last MMA until the next frame's A loads
 // (which wait for this CTA's barrier arrival) and conversions (done by these
 // same threads).  Same operands and arithmetic order as lstm_chains pass 0.
+#ifndef RGB_FL_POST_U
+#define RGB_FL_POST_U 2
+#endif
 __device__ __forceinline__ int lstm_nops(int pattern) { return pattern == 1 ? 4 : 6; }
 
 template <int SLAB>
@@ -2416,7 +2419,7 @@ __device__ __forceinline__ void lstm_post(int pattern, const EwChain* chains, co
   auto v = [&](int rl, int k) {
     return lds4(lstm_slab<STAGE_BYTES, A_BYTES, B_BYTES>(pipe, k) + (uint32_t)(rl - r_lo) * row_bytes + 16u * g);
   };
-  constexpr int U = 2;  // row groups in flight per thread
+  constexpr int U = RGB_FL_POST_U;  // row groups in flight per thread
 #pragma unroll 1
   for (int rb = r_lo + layer; rb < r_hi; rb += U * layers) {
 #pragma unroll
@@ -2852,6 +2855,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
         RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)f * fl.n_ew].ring : pf.ring};
         if (use_pre) {
           mbar_wait(pre_full, f & 1);  // the store warps' copies of the chain operands
+          if (tid == 0) FL_MARK(f, 7);
           lstm_post<C::STAGE_BYTES, C::A_BYTES, C::B_BYTES>(fl.pattern, chains, rings, tile_s, C::EPI_LD, m0, u0,
                                                              bu, N, r_lo, rows_hi, tid, 256, pipe);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the next frame's TMA reuses the slabs

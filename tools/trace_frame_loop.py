@@ -40,7 +40,8 @@ def dump(L, label, nframes):
             ops += f" | again: {(r[14] - last) / 1000.0:5.2f} {(r[15] - r[14]) / 1000.0:5.2f}"
         print(f"  f{f:2d}  {d(r[0], r[1]):6.2f} {d(r[1], r[2]):6.2f} {d(r[2], r[3]):6.2f} {d(r[3], r[4]):6.2f} "
               f"{d(r[4], r[5]):6.2f} {d(r[5], r[6]):6.2f}   {d(end, nxt):6.2f}   total {d(r[0], nxt):6.2f}"
-              f"   ops(us after reduce, last pass) {ops}")
+              f"   ops(us after reduce, last pass) {ops}"
+              + (f"   preload wait {d(r[3], r[7]):6.2f}" if r[7] else ""))
 
 
 def main():
