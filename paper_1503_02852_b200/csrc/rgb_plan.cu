@@ -323,7 +323,7 @@ struct rgb_plan {
     return 0;
   }
   std::map<std::vector<int64_t>, FrameLoopBlocks> frame_loops;
-  unsigned* fl_bar = nullptr;
+  unsigned* fl_bar = nullptr;  // frame-loop counter barrier: [0] arrivals, [1] launch base, [2] finished CTAs
   // blocks are carved from one device + one pinned arena, allocated at the
   // first (eager) frame loop: a CUDA graph capture may not allocate
   char* fl_dev = nullptr;
@@ -1134,8 +1134,8 @@ struct rgb_plan {
         } else {
           fl_cap = (size_t)64 << 20;
           if (cudaMalloc(&fl_dev, fl_cap) != cudaSuccess || cudaMallocHost(&fl_host, fl_cap) != cudaSuccess ||
-              cudaMalloc(&fl_bar, 2 * sizeof(unsigned)) != cudaSuccess ||
-              cudaMemset(fl_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+              cudaMalloc(&fl_bar, 4 * sizeof(unsigned)) != cudaSuccess ||
+              cudaMemset(fl_bar, 0, 4 * sizeof(unsigned)) != cudaSuccess)
             return fail(RGB_ERR_CUDA, "frame-loop arena allocation");
         }
       }

@@ -1876,7 +1876,7 @@ struct FrameLoop {
   int forward;              // 1: fused chain evaluation with register forwarding (frame_chains_fused)
   int pattern;              // 1 / 2: the LSTM cell forward / backward chains (lstm_chains), 0: generic
   int preload;              // 1: the pattern's operands are loaded before the split-K reduction (lstm_pre)
-  unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
+  unsigned* bar;            // counter barrier: [0] arrivals (monotonic), [1] count at launch, [2] finished CTAs
 };
 
 template <int BN>
@@ -1932,6 +1932,39 @@ __device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) 
     if (t - t0 > 4000000000LL) __trap();  // 4 s: a lost CTA -- fail loudly instead of hanging the GPU
   }
   (void)ld_acquire_u32(bar + 1);
+}
+
+// Counter barrier of the frame loop: bar[0] counts arrivals monotonically
+// across launches, bar[1] holds the count at the start of the running
+// launch (written by the last CTA to finish the previous one, bar[2] counts
+// finished CTAs).  Arrive = fence + fire-and-forget add (no last-arriver
+// round trips: the waiters watch the counter itself); barrier k of a launch
+// is complete when bar[0] >= base + k * nblocks.
+__device__ __forceinline__ void ctr_arrive(unsigned* bar) {
+  __threadfence();  // this CTA's stores before its arrival (cumulative over the bar.sync before it)
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+
+__device__ __forceinline__ void ctr_wait(const unsigned* bar, unsigned target) {
+  long long t0 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while ((int)(ld_relaxed_u32(bar) - target) < 0) {
+    __nanosleep(32);
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000LL) __trap();  // 4 s: a lost CTA -- fail loudly instead of hanging the GPU
+  }
+  (void)ld_acquire_u32(bar);
+}
+
+// end of a launch: the last CTA publishes the arrival count as the next base
+__device__ __forceinline__ void ctr_finish(unsigned* bar, unsigned next_base, unsigned nblocks) {
+  __threadfence();
+  if (atomicAdd(&bar[2], 1u) == nblocks - 1) {
+    bar[2] = 0u;
+    bar[1] = next_base;
+    __threadfence();
+  }
 }
 
 #ifdef RGB_FL_TRACE
@@ -2608,7 +2641,9 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
   }
   // the barrier generation at launch; every CTA reads it before its first
   // arrival, and no barrier completes before every CTA arrived
-  const unsigned gen0 = *reinterpret_cast<volatile unsigned*>(fl.bar + 1);
+  const unsigned gen0 = *reinterpret_cast<volatile unsigned*>(fl.bar + 1);  // counter base of this launch
+  const unsigned nblk = gridDim.x;
+  auto bar_target = [&](unsigned k) { return gen0 + k * nblk; };  // barrier k (1-based) complete
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (csplit > 1) cluster_sync();
   else __syncthreads();
@@ -2651,7 +2686,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
     // delayed state, co-factors, ...) while the main loop runs: the chains
     // are latency-bound on these loads (~1-2 us per op from HBM)
     for (int f = 0; f < fl.nframes; ++f) {
-      if (f > 0) grid_wait(fl.bar, gen0 + (unsigned)f * nbar);
+      if (f > 0) ctr_wait(fl.bar, bar_target((unsigned)f * nbar));
       const GemmGroup& pf = fl.frames[f];
       const int rlo = csplit > 1 ? split * BM / csplit : 0, rhi = min(csplit > 1 ? (split + 1) * BM / csplit : BM, M - m0);
       const int bytes = min(bu, N - u0) * 4;
@@ -2689,7 +2724,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       for (int f = 0; f < fl.nframes; ++f) {
         const GemmGroup& pf = fl.frames[f];
         if (load_a && f > 0) {
-          grid_wait(fl.bar, gen0 + (unsigned)f * nbar);
+          ctr_wait(fl.bar, bar_target((unsigned)f * nbar));
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (load_a) FL_MARK(f, 0);
@@ -2819,7 +2854,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       if (tid == 0) FL_MARK(f, 1);
       // acquire the frame barrier the A loads waited on: the chains read
       // operands other SMs stored in earlier frames (no stale L1 lines)
-      if (f > 0) (void)ld_acquire_u32(fl.bar + 1);
+      if (f > 0) (void)ld_acquire_u32(fl.bar);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       {  // accumulator -> tile_s (warp w: TMEM lane quarter w%4, column half w/4)
@@ -2884,14 +2919,14 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid == 0) FL_MARK(f, 4);
-      if (tid == 0) grid_arrive(fl.bar, gridDim.x);
+      if (tid == 0) ctr_arrive(fl.bar);
       if (fl.pattern && tid == 0) mbar_arrive(st_go);  // the store warps take the rest of the frame
       // ---- unfused elementwise steps of frame f (all CTAs, between grid barriers) ----
       for (int e = 0; e < (fl.fuse_ew ? 0 : fl.n_ew); ++e) {
         const EwLaunch& L = fl.ew[(size_t)f * fl.n_ew + e];
-        if (tid == 0) grid_wait(fl.bar, gen0 + (unsigned)f * nbar + 1u + (unsigned)e);
+        if (tid == 0) ctr_wait(fl.bar, bar_target((unsigned)f * nbar + 1u + (unsigned)e));
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        (void)ld_acquire_u32(fl.bar + 1);  // every thread: acquire before reading other SMs' stores
+        (void)ld_acquire_u32(fl.bar);  // every thread: acquire before reading other SMs' stores
         if (tid == 0) FL_MARK(f, 5);
         for (int c = 0; c < L.nchains; ++c) {
           stage_chain(&chains[0], L.chain[c], tid, 256);
@@ -2919,7 +2954,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
           asm volatile("bar.sync 1, 256;" ::: "memory");
         }
         if (tid == 0) FL_MARK(f, 6);
-        if (tid == 0) grid_arrive(fl.bar, gridDim.x);
+        if (tid == 0) ctr_arrive(fl.bar);
       }
     }
   }
@@ -2927,6 +2962,7 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
   if (csplit > 1) cluster_sync();  // peers' last DSMEM reads of this CTA's tile are done
   else __syncthreads();
   if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (threadIdx.x == 0) ctr_finish(fl.bar, bar_target((unsigned)fl.nframes * nbar), nblk);
 }
 
 // Widest N tile that still gives most of the 148 SMs a tile.
