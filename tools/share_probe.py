@@ -2,9 +2,10 @@
 
     python tools/share_probe.py [S ...]
 
-cfg4 with S streams on this GPU: graph-replayed step time with the plain
-backward and with the bucketed backward + NCCL exchange (world size 1: the
-schedule and stream fork/join of the multi-GPU step, no peer traffic)."""
+cfg4 with S streams on this GPU: graph-replayed step time with no exchange,
+with the default exchange (plain backward + one NCCL all-reduce) and with the
+bucketed backward + NCCL exchange (world size 1: the schedule and stream
+fork/join of the multi-GPU step, no peer traffic)."""
 from __future__ import annotations
 
 import json
@@ -42,12 +43,15 @@ def step_ms(S, exchange, steps=20):
 def main():
     sizes = [int(a) for a in sys.argv[1:]] or [64, 128, 256, 512]
     ex = NcclExchange()
+    exb = NcclExchange(bucketed=True)
     out = {}
     for S in sizes:
-        out[S] = {"plain_ms": step_ms(S, None), "bucketed_nccl1_ms": step_ms(S, ex)}
+        out[S] = {"plain_ms": step_ms(S, None), "allreduce_nccl1_ms": step_ms(S, ex),
+                  "bucketed_nccl1_ms": step_ms(S, exb)}
         print(S, out[S], flush=True)
     torch.cuda.synchronize()
     ex.close()
+    exb.close()
     print(json.dumps(out))
 
 
