@@ -233,6 +233,29 @@ def test_gemm_nt_tma_kernel_variants(m, n, k, mode, restore_tc_modes):
     assert normwise(tc.cpu().numpy(), ref) < 1e-5
 
 
+@pytest.mark.parametrize("mode", [(1, 1, 1), (0, 1, 1)])
+@pytest.mark.parametrize("m,n,k", [(8192, 3072, 1024), (16384, 1000, 512), (16384, 1024, 4096)])
+def test_gemm_nt_persistent_tail_split(m, n, k, mode, restore_tc_modes):
+    """Persistent launches whose last wave runs as column-half tiles
+    (launch_persistent's tail split: 384 / 256 pair tiles on 74 pairs, 512
+    single tiles on 148 SMs), ragged N included, deep K (chunked accumulation
+    across the halves); every output element written (NaN-initialised)."""
+    _set_modes(mode)
+    rng = np.random.default_rng(m + n + k + 7)
+    a = rng.uniform(-1, 1, size=(m, k))
+    b = rng.uniform(-1, 1, size=(n, k))
+    ta = torch.tensor(a, dtype=torch.float32, device="cuda")
+    tb = torch.tensor(b, dtype=torch.float32, device="cuda")
+    tc = torch.full((m, n), float("nan"), device="cuda")
+    _lib.check(_lib.lib().rgb_gemm_nt_tma(ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()),
+                                          ctypes.c_void_p(tb.data_ptr()), ctypes.c_void_p(tc.data_ptr()),
+                                          m, n, k, _stream()))
+    out = tc.cpu().numpy()
+    assert not np.isnan(out).any()
+    ref = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    assert normwise(out, ref) < 1e-5
+
+
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("m,n,k", [(4096, 4096, 512), (1024, 1024, 2080), (96, 160, 333)])
 def test_gemm_dw_tma(m, n, k, mode, restore_tc_modes):
