@@ -3291,11 +3291,14 @@ int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const E
     pat_env = e ? atoi(e) != 0 : 1;
   }
   if (!pat_env || (pattern == 1 && !(J == 2 && bu % 4 == 0)) || (pattern == 2 && J != 1)) pattern = 0;
-  static int preload = -1;  // RGB_FL_PRELOAD=0: the pattern's operands are loaded after the reduction
-  if (preload < 0) {
+  // RGB_FL_PRELOAD: 0 the pattern's operands are loaded after the reduction,
+  // 1 preloaded by the store warps (forward and backward), 2 forward only
+  static int preload_env = -1;
+  if (preload_env < 0) {
     const char* e = getenv("RGB_FL_PRELOAD");
-    preload = e ? atoi(e) != 0 : 1;
+    preload_env = e ? atoi(e) : 1;
   }
+  const int preload = preload_env == 1 || (preload_env == 2 && pattern == 1);
   tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, preload, bar};
   auto launch = [&](auto kernel, int smem) -> int {
     static bool bad = false;  // cooperative cluster launches unsupported: stay per-frame
