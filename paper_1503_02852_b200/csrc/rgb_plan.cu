@@ -537,7 +537,12 @@ struct rgb_plan {
         return sp;  // softmax / nested loop / dW: not in a recurrent body
       }
     }
-    if (W <= 0 || macs > 64.0 * 1024 * 1024 || S > 256 || nsteps > 8 || nslots > 512) return sp;
+    static double max_macs = -1;  // RGB_SCC_MAXMAC: per-frame MAC ceiling of the persistent SCC kernel
+    if (max_macs < 0) {
+      const char* e = getenv("RGB_SCC_MAXMAC");
+      max_macs = e ? atof(e) : 64.0 * 1024 * 1024;
+    }
+    if (W <= 0 || macs > max_macs || S > 256 || nsteps > 8 || nslots > 512) return sp;
     // Preferred: row blocks of streams x a column split of W over ncb <= 16
     // CTAs, one hardware cluster per row block (cluster barrier ~0.2-0.6 us;
     // streams never exchange data, so row blocks run independently) with
