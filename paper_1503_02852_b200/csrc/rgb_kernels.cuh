@@ -59,7 +59,8 @@ void launch_tc_gemm_dw(DwGroup p, cudaStream_t s);
 // persistent tensor-core frame loop of a recurrent SCC (rgb_tc_gemm.cu): -1 if
 // the loop's GEMM shape does not suit it, else a cudaError_t
 int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const EwLaunch* d_ew, int n_ew,
-                         int fuse_ew, int pattern, int nframes, unsigned* bar, cudaStream_t s);
+                         int fuse_ew, int pattern, const EwLaunch* d_tail, int nframes, unsigned* bar,
+                         cudaStream_t s);
 void launch_softmax(float* y, int rows, int width, RingWrite ring, bool is_ring, cudaStream_t s);
 // target_kind: 0 = int64 class ids, 1 = int32 class ids, 2 = dense fp32 targets.
 // criterion: 0 = cross entropy (softmax output), 1 = mse (identity output).

@@ -265,10 +265,36 @@ struct rgb_plan {
     int ok = 1;  // 0: the loop's shape does not suit the kernel (per-frame launches)
     GemmGroup* d_groups = nullptr;
     EwLaunch* d_ew = nullptr;
+    EwLaunch* d_tail = nullptr;  // per frame: the fused elementwise step that follows the loop (or null)
     void* h_pinned = nullptr;
     int n_ew = 0, fuse_ew = 0, pattern = 0;
+    int64_t tail_words = 0;      // > 0: the loop consumes the next program step (tail_words long)
     double flops = 0;
   };
+
+  // The single-op elementwise step right after an LSTM-pattern loop that the
+  // loop's store warps can evaluate per frame from values they hold in
+  // registers (tc::lstm_chains pass 1): forward cell_act = act(0 + cell(t)),
+  // backward delta(cell_in) = (0 + eps) * f'(y) with eps one of the loop's
+  // co-factor eps.  Returns true if `e` (one frame's parse) qualifies.
+  static bool tail_fusable(int pattern, const GemmGroup& g, const EwLaunch* ew, const EwLaunch& e) {
+    if (e.nchains != 1 || e.chain[0].nops != 1) return false;
+    const EwOp& o = e.chain[0].op[0];
+    if (e.chain[0].width != g.job[0].n || o.nrank1 || o.base || o.inj || !a16(o.out) || o.nterm != 1 ||
+        !a16(o.term[0]))
+      return false;
+    if (pattern == 1) {
+      return o.kind == EW_FWD_ADD && o.nfac == 0 && ew && o.term[0] == ew[0].chain[0].op[0].out &&
+             o.out != ew[0].chain[0].op[0].out;
+    }
+    if (pattern == 2) {
+      const EwOp* q = g.job[0].epi.op;
+      const float* t = o.term[0];
+      return o.kind == EW_BWD && o.nfac == 0 && (o.act == ACT_SIGMOID || o.act == ACT_TANH) && o.y && a16(o.y) &&
+             (t == q[1].eps[0] || t == q[1].eps[1] || t == q[2].eps[0] || t == q[2].eps[1]);
+    }
+    return false;
+  }
 
   // The LSTM cell chain sets the frame loop evaluates in registers with the
   // next frame's inputs stored first (tc::lstm_chains): 1 forward (two gate
@@ -1074,8 +1100,10 @@ struct rgb_plan {
   // steps runs as ONE persistent tensor-core launch over all its frames
   // (tma_frame_loop_kernel) when the per-frame GEMM is tensor-core sized.
   // *handled = false: not eligible, the caller launches frame by frame.
-  int try_frame_loop(const int32_t* body, int64_t len, const Ctx& c, bool reverse, cudaStream_t st, bool* handled) {
+  int try_frame_loop(const int32_t* body, int64_t len, const Ctx& c, bool reverse, cudaStream_t st, bool* handled,
+                     const int32_t* next, int64_t next_len, int64_t* consumed) {
     *handled = false;
+    *consumed = 0;
     std::vector<int64_t> starts;
     for (int64_t i = 0; i < len;) {
       const int64_t w = step_words(body, i, len);
@@ -1094,6 +1122,11 @@ struct rgb_plan {
                                 (int64_t)get_tc_terms()};
     auto it = frame_loops.find(key);
     if (it != frame_loops.end() && !it->second.ok) return RGB_OK;
+    static int tail_env = -1;  // RGB_FL_TAIL=0: the elementwise step after the loop runs as its own launch
+    if (tail_env < 0) {
+      const char* e = getenv("RGB_FL_TAIL");
+      tail_env = e ? atoi(e) != 0 : 1;
+    }
     if (it == frame_loops.end()) {
       // build the per-frame blocks (host), check eligibility, upload
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1132,7 +1165,26 @@ struct rgb_plan {
       for (int e = 0; e < n_ew && fb.fuse_ew; ++e)
         fb.fuse_ew = ews[e].nchains == 1 && ews[e].chain[0].width == groups[0].job[0].n;
       if (c.frames >= 2) fb.pattern = lstm_pattern(groups[0], groups[1], ews.data(), n_ew, fb.fuse_ew != 0);
-      const size_t need = (gbytes + ebytes + 255) & ~size_t(255);
+      // the elementwise step right after the loop, fused into the store warps' pass
+      std::vector<EwLaunch> tails;
+      if (fb.ok && fb.pattern && tail_env && next && next_len > 0 && next[0] == STEP_EW) {
+        const int64_t w = step_words(next, 0, next_len);
+        bool ok = w > 1;
+        tails.resize(c.frames);
+        for (int f = 0; f < c.frames && ok; ++f) {
+          Ctx ci = c;
+          ci.t_a = reverse ? c.t_a + c.frames - 1 - f : c.t_a + f;
+          ci.frames = 1;
+          Reader re{next + 1, w - 1};
+          int rc = parse_ew(re, ci, tails[f]);
+          if (rc) return rc;
+          ok = tail_fusable(fb.pattern, groups[f], n_ew ? &ews[(size_t)f * n_ew] : nullptr, tails[f]);
+        }
+        if (ok) fb.tail_words = w;
+        else tails.clear();
+      }
+      const size_t tbytes = sizeof(EwLaunch) * tails.size();
+      const size_t need = (gbytes + ebytes + tbytes + 255) & ~size_t(255);
       if (fb.ok && !fl_dev) {
         if (cs != cudaStreamCaptureStatusNone) {
           fb.ok = 0;  // first seen inside a capture: no allocation possible; per-frame launches
@@ -1148,15 +1200,16 @@ struct rgb_plan {
       if (fb.ok) {
         fb.d_groups = reinterpret_cast<GemmGroup*>(fl_dev + fl_used);
         fb.d_ew = ebytes ? reinterpret_cast<EwLaunch*>(fl_dev + fl_used + gbytes) : nullptr;
+        fb.d_tail = tbytes ? reinterpret_cast<EwLaunch*>(fl_dev + fl_used + gbytes + ebytes) : nullptr;
         fb.h_pinned = fl_host + fl_used;
         fl_used += need;
         std::memcpy(fb.h_pinned, groups.data(), gbytes);
         if (ebytes) std::memcpy(static_cast<char*>(fb.h_pinned) + gbytes, ews.data(), ebytes);
+        if (tbytes) std::memcpy(static_cast<char*>(fb.h_pinned) + gbytes + ebytes, tails.data(), tbytes);
         // enqueued (and, inside a capture, recorded) on the stream; the pinned
         // source stays alive and unchanged with the cache entry
-        if (cudaMemcpyAsync(fb.d_groups, fb.h_pinned, gbytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            (ebytes && cudaMemcpyAsync(fb.d_ew, static_cast<char*>(fb.h_pinned) + gbytes, ebytes,
-                                       cudaMemcpyHostToDevice, st) != cudaSuccess))
+        if (cudaMemcpyAsync(fb.d_groups, fb.h_pinned, gbytes + ebytes + tbytes, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess)
           return fail(RGB_ERR_CUDA, "frame-loop block upload");
         fb.ok = 2;  // uploaded; the launch below decides the shape
         (void)cs;
@@ -1167,11 +1220,13 @@ struct rgb_plan {
       it->second.ok = 1;
       GemmGroup g0 = groups[0];
       const int slot = prof_start(st);
-      const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, n_ew, fb.fuse_ew, fb.pattern, c.frames, fl_bar, st);
+      const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, n_ew, fb.fuse_ew, fb.pattern, fb.d_tail, c.frames,
+                                           fl_bar, st);
       if (lrc < 0) {
         it->second.ok = 0;
         return RGB_OK;
       }
+      *consumed = fb.d_tail ? fb.tail_words : 0;
       note_launch();
       prof_stop(slot, st, PROF_GEMM_FRAME, fb.flops, 0.0);
       if (lrc) return fail(RGB_ERR_CUDA, "frame-loop launch: %s", cudaGetErrorString((cudaError_t)lrc));
@@ -1183,9 +1238,10 @@ struct rgb_plan {
     const FrameLoopBlocks& fb = it->second;
     const GemmGroup& g0 = *static_cast<const GemmGroup*>(fb.h_pinned);
     const int slot = prof_start(st);
-    const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, fb.n_ew, fb.fuse_ew, fb.pattern, c.frames, fl_bar,
-                                         st);
+    const int lrc = launch_tc_frame_loop(g0, fb.d_groups, fb.d_ew, fb.n_ew, fb.fuse_ew, fb.pattern, fb.d_tail, c.frames,
+                                         fl_bar, st);
     if (lrc < 0) return RGB_OK;
+    *consumed = fb.d_tail ? fb.tail_words : 0;
     note_launch();
     prof_stop(slot, st, PROF_GEMM_FRAME, fb.flops, 0.0);
     if (lrc) return fail(RGB_ERR_CUDA, "frame-loop launch: %s", cudaGetErrorString((cudaError_t)lrc));
@@ -1337,9 +1393,12 @@ struct rgb_plan {
         }
         if (g_frame_loop && !id_mode && !g_wavefront_active && g_gemm_mode != 1 && c.section >= 0 && c.frames >= 2) {
           bool handled = false;
-          if ((rc = try_frame_loop(body, len, c, reverse != 0, st, &handled))) return rc;
+          int64_t consumed = 0;
+          if ((rc = try_frame_loop(body, len, c, reverse != 0, st, &handled, p + rd.i + len, n - (rd.i + len),
+                                   &consumed)))
+            return rc;
           if (handled) {
-            rd.i += len;
+            rd.i += len + consumed;  // + the elementwise step the loop evaluated per frame
             continue;
           }
         }

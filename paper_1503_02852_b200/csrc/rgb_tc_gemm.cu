@@ -1876,6 +1876,7 @@ struct FrameLoop {
   int forward;              // 1: fused chain evaluation with register forwarding (frame_chains_fused)
   int pattern;              // 1 / 2: the LSTM cell forward / backward chains (lstm_chains), 0: generic
   int preload;              // 1: the pattern's operands are loaded before the split-K reduction (lstm_pre)
+  const EwLaunch* tail;     // [nframes] or null: the one-op elementwise step after the loop, run in pass 1
   unsigned* bar;            // counter barrier: [0] arrivals (monotonic), [1] count at launch, [2] finished CTAs
 };
 
@@ -2208,7 +2209,8 @@ __device__ __forceinline__ float4 dact4(int act, float4 y) {
 template <int R>
 __device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain* chains, const RingWrite* rings,
                                             const float* tile_s, int ld, int m0, int u0, int bu, int N, int r_lo,
-                                            int r_hi, int tid, int nthr) {
+                                            int r_hi, int tid, int nthr, const EwOp* tail = nullptr,
+                                            const RingWrite* tail_ring = nullptr) {
   const int ncols = min(bu, N - u0);
   if (ncols <= 0 || r_hi <= r_lo) return;
   const int g4 = ncols / 4, lanes = nthr / g4 * g4;
@@ -2275,6 +2277,18 @@ __device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain
           else pb[u] = pr[u];
         }
       }
+      if (pass == 1 && tail) {  // the fused step after the loop: act(0 + cell(t))
+        const bool a_first = ew.term[0] == chains[0].op[1].out;
+        float4 v[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          const float4 t0 = a_first ? pa[u] : pb[u], t1 = a_first ? pb[u] : pa[u];
+          v[u] = act4(tail->act, add4(zero, act4(ew.act, add4(add4(zero, t0), t1))));
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+          if (ok[u]) ring_store4(tail->out, e[u], rr[u], N, tail->out_is_ring, *tail_ring, v[u]);
+      }
       if (pass == 0) {
         const bool a_first = ew.term[0] == chains[0].op[1].out;
         float4 c[R];
@@ -2332,6 +2346,18 @@ __device__ __forceinline__ void lstm_chains(int pattern, int pass, const EwChain
         store_to(o[2].out, d2);
         store_to(o[2].eps[0], e20);
         store_to(o[2].eps[1], e21);
+        if (tail) {  // the fused step after the loop: (0 + eps) * f'(y)
+          const float* src = tail->term[0];
+          float4 y[R], v[R];
+          load(tail->y, y);
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            const float4 s = src == o[1].eps[0] ? e10[u] : src == o[1].eps[1] ? e11[u]
+                           : src == o[2].eps[0] ? e20[u] : e21[u];
+            v[u] = mul4(add4(zero, s), dact4(tail->act, y[u]));
+          }
+          store_to(tail->out, v);
+        }
       }
     }
   }
@@ -2645,7 +2671,10 @@ __global__ void __launch_bounds__(kFrameThreads, 1)
         mbar_wait(st_go, (f - 1) & 1);
         const GemmGroup& pf = fl.frames[f - 1];
         RingWrite rings[3] = {pf.ring, pf.ring, fl.n_ew ? fl.ew[(size_t)(f - 1) * fl.n_ew].ring : pf.ring};
-        lstm_chains<2>(fl.pattern, 1, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, rlo, rhi, stid, 128);
+        const EwOp* tail = fl.tail ? &fl.tail[f - 1].chain[0].op[0] : nullptr;
+        const RingWrite tring = fl.tail ? fl.tail[f - 1].ring : pf.ring;
+        lstm_chains<2>(fl.pattern, 1, chains, rings, tile_s, C::EPI_LD, m0, u0, bu, N, rlo, rhi, stid, 128, tail,
+                       &tring);
         asm volatile("bar.sync 5, 128;" ::: "memory");
         if (stid == 0) mbar_arrive(st_done);
       }
@@ -3209,7 +3238,8 @@ int launch_tc_gemm_nt(GemmGroup p, cudaStream_t s) {
 // run, preferring no split (no DSMEM reduction).  fuse_ew: the elementwise
 // steps are element-local over the jobs' width and run in the epilogue.
 int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const EwLaunch* d_ew, int n_ew,
-                         int fuse_ew, int pattern, int nframes, unsigned* bar, cudaStream_t s) {
+                         int fuse_ew, int pattern, const EwLaunch* d_tail, int nframes, unsigned* bar,
+                         cudaStream_t s) {
   GemmGroup p = g0;
   p.terms = g_tc_terms;
   if (!p.tma || p.njobs < 1 || p.njobs > 4) return -1;
@@ -3278,7 +3308,8 @@ int launch_tc_frame_loop(const GemmGroup& g0, const GemmGroup* d_frames, const E
     preload_env = e ? atoi(e) : 1;
   }
   const int preload = preload_env == 1 || (preload_env == 2 && pattern == 1);
-  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, preload, bar};
+  tc::FrameLoop fl{d_frames, d_ew, nframes, n_ew, fuse_ew, bu, prefetch, fwd, pattern, preload,
+                   pattern ? d_tail : nullptr, bar};
   auto launch = [&](auto kernel, int smem) -> int {
     static bool bad = false;  // cooperative cluster launches unsupported: stay per-frame
     if (bad) return -1;
