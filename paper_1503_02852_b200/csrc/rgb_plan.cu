@@ -1125,7 +1125,7 @@ struct rgb_plan {
     static int tail_env = -1;  // RGB_FL_TAIL=0: the elementwise step after the loop runs as its own launch
     if (tail_env < 0) {
       const char* e = getenv("RGB_FL_TAIL");
-      tail_env = e ? atoi(e) != 0 : 1;
+      tail_env = e ? atoi(e) : 1;
     }
     if (it == frame_loops.end()) {
       // build the per-frame blocks (host), check eligibility, upload
@@ -1167,7 +1167,9 @@ struct rgb_plan {
       if (c.frames >= 2) fb.pattern = lstm_pattern(groups[0], groups[1], ews.data(), n_ew, fb.fuse_ew != 0);
       // the elementwise step right after the loop, fused into the store warps' pass
       std::vector<EwLaunch> tails;
-      if (fb.ok && fb.pattern && tail_env && next && next_len > 0 && next[0] == STEP_EW) {
+      // RGB_FL_TAIL: 0 off, 1 both directions, 2 backward (pattern 2) only
+      if (fb.ok && fb.pattern && (tail_env == 1 || (tail_env == 2 && fb.pattern == 2)) && next && next_len > 0 &&
+          next[0] == STEP_EW) {
         const int64_t w = step_words(next, 0, next_len);
         bool ok = w > 1;
         tails.resize(c.frames);
